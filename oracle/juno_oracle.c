@@ -1,0 +1,737 @@
+/*
+ * juno_oracle.c -- CPU restatement of the Juno benchmark fork-join programs.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the CUDA
+ * kernels in paper_2503_10855_b200/csrc.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  The
+ * product path never links or calls it.
+ *
+ * Semantics follow the reference value-semantics interpreter
+ * (/root/reference/pkg/src/skiff/runtime/oracle.py, values.py):
+ *   - every f32 add/sub/mul/div is rounded once (numpy float32 scalar ops,
+ *     values.py:55-71) -> this file is compiled with -ffp-contract=off and
+ *     never uses fma();
+ *   - forks iterate lexicographically, dim 0 outermost, and reduces fold in
+ *     that order (oracle.py:288-304);
+ *   - min/max are Python builtins: max(a,b) = (b > a) ? b : a, min(a,b) =
+ *     (b < a) ? b : a  (values.py:88-91);
+ *   - `x[i] += v` is read -> add(old, v) -> write (lower.py:412-421).
+ * Where a benchmark needs sqrt/exp/log (not expressible in the reference
+ * frontend) we use IEEE sqrtf (correctly rounded) and
+ * exp/log evaluated in double then rounded to f32.
+ * Global float reductions that the paper's schedules re-associate
+ * (monoid-reassociate) are accumulated in f64 here and in the
+ * CUDA kernels, so both sides agree to the last f32 bit in practice.
+ *
+ * Parallelism: OpenMP over the outermost parallel fork (the paper's
+ * multicore schedule) -- results are independent of the
+ * thread count because every parallel fork has only parallel reductions.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define EXPORT __attribute__((visibility("default")))
+
+static inline float pymax(float a, float b) { return (b > a) ? b : a; }
+static inline float pymin(float a, float b) { return (b < a) ? b : a; }
+static inline float exp_ref(float x) { return (float)exp((double)x); }
+static inline float log_ref(float x) { return (float)log((double)x); }
+
+EXPORT int jo_version(void) { return 3; }
+
+EXPORT int jo_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+EXPORT void jo_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+/* ------------------------------------------------------------------------
+ * matmul<n,m,l>(a: f32[n,m], b: f32[m,l]) -> f32[n,l]
+ * res[i,j] += a[i,k]*b[k,j], k ascending, res zero-initialised.
+ * ---------------------------------------------------------------------- */
+EXPORT void jo_matmul_f32(int64_t n, int64_t m, int64_t l, const float *a,
+                          const float *b, float *res) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; i++) {
+    float *r = res + i * l;
+    for (int64_t j = 0; j < l; j++) r[j] = 0.0f;
+    for (int64_t k = 0; k < m; k++) {
+      const float aik = a[i * m + k];
+      const float *bk = b + k * l;
+      for (int64_t j = 0; j < l; j++) r[j] = r[j] + aik * bk[j];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------
+ * edge_detection<n,m,gs,sz,sb>(input f32[n,m], gaussian f32[gs,gs],
+ *     structure f32[sz,sz], sx f32[sb,sb], sy f32[sb,sb], theta f32)
+ *   -> f32[n,m]
+ * Stages (EDGE): gaussian_smoothing (clamp-to-edge),
+ * laplacian_estimate (dilate pad 0 / erode pad 1, minus 2*input),
+ * zero_crossings (dilate - erode of the sign image), gradient (sobel on the
+ * smoothed image, sqrt), max_gradient (max fold, initialised with
+ * gradient[0,0]), reject_zero_crossings.
+ * Optional intermediates (any may be NULL) are filled for stage-level tests.
+ * ---------------------------------------------------------------------- */
+static inline int64_t clampi(int64_t v, int64_t hi) {
+  return v < 0 ? 0 : (v > hi ? hi : v);
+}
+
+EXPORT void jo_edge_frame_f32(int64_t n, int64_t m, int64_t gs, int64_t sz,
+                              int64_t sb, const float *in, const float *gf,
+                              const float *st, const float *sx,
+                              const float *sy, float theta, float *out,
+                              float *smoothed_o, float *lap_o, float *zc_o,
+                              float *grad_o, float *maxgrad_o) {
+  const int64_t N = n * m;
+  float *sm = smoothed_o ? smoothed_o : (float *)malloc(N * sizeof(float));
+  float *lp = lap_o ? lap_o : (float *)malloc(N * sizeof(float));
+  float *zc = zc_o ? zc_o : (float *)malloc(N * sizeof(float));
+  float *gr = grad_o ? grad_o : (float *)malloc(N * sizeof(float));
+  const int64_t g2 = gs / 2, r2 = sz / 2, b2 = sb / 2;
+
+  /* gaussian_smoothing */
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t c = 0; c < m; c++) {
+      float s = 0.0f;
+      for (int64_t i = 0; i < gs; i++)
+        for (int64_t j = 0; j < gs; j++) {
+          const float v = in[clampi(r + i - g2, n - 1) * m +
+                             clampi(c + j - g2, m - 1)];
+          s = s + v * gf[i * gs + j];
+        }
+      sm[r * m + c] = s;
+    }
+
+  /* laplacian_estimate */
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t c = 0; c < m; c++) {
+      float d = 0.0f, e = 1.0f;
+      for (int64_t i = 0; i < sz; i++)
+        for (int64_t j = 0; j < sz; j++) {
+          const int64_t y = r + i - r2, x = c + j - r2;
+          const int inside = (y >= 0 && y < n && x >= 0 && x < m);
+          const float v = inside ? sm[y * m + x] : 0.0f;
+          d = pymax(d, v * st[i * sz + j]);
+        }
+      for (int64_t i = 0; i < sz; i++)
+        for (int64_t j = 0; j < sz; j++) {
+          const int64_t y = r + i - r2, x = c + j - r2;
+          const int inside = (y >= 0 && y < n && x >= 0 && x < m);
+          const float v = inside ? sm[y * m + x] : 1.0f;
+          e = pymin(e, v * st[i * sz + j]);
+        }
+      lp[r * m + c] = (d + e) - 2.0f * sm[r * m + c];
+    }
+
+  /* zero_crossings */
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t c = 0; c < m; c++) {
+      float d = 0.0f, e = 1.0f;
+      for (int64_t i = 0; i < sz; i++)
+        for (int64_t j = 0; j < sz; j++) {
+          const int64_t y = r + i - r2, x = c + j - r2;
+          const int inside = (y >= 0 && y < n && x >= 0 && x < m);
+          const float v = inside ? (lp[y * m + x] > 0.0f ? 1.0f : 0.0f) : 0.0f;
+          d = pymax(d, v * st[i * sz + j]);
+        }
+      for (int64_t i = 0; i < sz; i++)
+        for (int64_t j = 0; j < sz; j++) {
+          const int64_t y = r + i - r2, x = c + j - r2;
+          const int inside = (y >= 0 && y < n && x >= 0 && x < m);
+          const float v = inside ? (lp[y * m + x] > 0.0f ? 1.0f : 0.0f) : 1.0f;
+          e = pymin(e, v * st[i * sz + j]);
+        }
+      zc[r * m + c] = d - e;
+    }
+
+  /* gradient */
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < n; r++)
+    for (int64_t c = 0; c < m; c++) {
+      float gx = 0.0f, gy = 0.0f;
+      for (int64_t i = 0; i < sb; i++)
+        for (int64_t j = 0; j < sb; j++) {
+          const float v = sm[clampi(r + i - b2, n - 1) * m +
+                             clampi(c + j - b2, m - 1)];
+          gx = gx + v * sx[i * sb + j];
+          gy = gy + v * sy[i * sb + j];
+        }
+      gr[r * m + c] = sqrtf(gx * gx + gy * gy);
+    }
+
+  /* max_gradient: sequential fold starting at gradient[0,0] */
+  float mx = gr[0];
+  for (int64_t k = 0; k < N; k++) mx = pymax(mx, gr[k]);
+  if (maxgrad_o) *maxgrad_o = mx;
+
+  /* reject_zero_crossings */
+  const float thr = theta * mx;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++)
+    out[k] = (zc[k] > 0.0f && gr[k] > thr) ? 1.0f : 0.0f;
+
+  if (!smoothed_o) free(sm);
+  if (!lap_o) free(lp);
+  if (!zc_o) free(zc);
+  if (!grad_o) free(gr);
+}
+
+EXPORT void jo_edge_f32(int64_t batch, int64_t n, int64_t m, int64_t gs,
+                        int64_t sz, int64_t sb, const float *in,
+                        const float *gf, const float *st, const float *sx,
+                        const float *sy, float theta, float *out) {
+  for (int64_t f = 0; f < batch; f++)
+    jo_edge_frame_f32(n, m, gs, sz, sb, in + f * n * m, gf, st, sx, sy, theta,
+                      out + f * n * m, NULL, NULL, NULL, NULL, NULL);
+}
+
+/* ------------------------------------------------------------------------
+ * cava<r,c,P>(input u8[3,r,c], TsTw f32[3,3], ctrl_pts f32[P,3],
+ *             weights f32[P,3], coefs f32[4,3], tonemap f32[256,3])
+ *   -> u8[3,r,c]                          (CAVA)
+ * scale -> demosaic (bilinear RGGB, 1-pixel border left 0) -> denoise
+ * (per-channel 3x3 median, border copied) -> transform (3x3) -> gamut map
+ * (RBF over P control points + affine) -> tone map (LUT) -> descale.
+ * ---------------------------------------------------------------------- */
+static inline float median9(float *w) {
+  /* insertion sort of 9 values; the median is exact selection */
+  for (int i = 1; i < 9; i++) {
+    float v = w[i];
+    int j = i - 1;
+    while (j >= 0 && w[j] > v) {
+      w[j + 1] = w[j];
+      j--;
+    }
+    w[j + 1] = v;
+  }
+  return w[4];
+}
+
+static inline float clamp255(float t) {
+  return pymin(pymax(t, 0.0f), 255.0f);
+}
+
+/* stage functions (planes are [3][R][C]) */
+EXPORT void jo_cava_scale(int64_t R, int64_t C, const uint8_t *in, float *sc) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < 3 * R * C; k++) sc[k] = ((float)in[k] * 1.0f) / 255.0f;
+}
+
+EXPORT void jo_cava_demosaic(int64_t R, int64_t C, const float *sc, float *dm) {
+  const int64_t N = R * C;
+#define SC(ch, y, x) sc[(ch) * N + (y) * C + (x)]
+  memset(dm, 0, 3 * N * sizeof(float));
+#pragma omp parallel for schedule(static)
+  for (int64_t y = 1; y < R - 1; y++)
+    for (int64_t x = 1; x < C - 1; x++) {
+      float rr, gg, bb;
+      if (y % 2 == 0 && x % 2 == 0) { /* red site */
+        rr = SC(0, y, x);
+        gg = (((SC(1, y - 1, x) + SC(1, y + 1, x)) + SC(1, y, x - 1)) +
+              SC(1, y, x + 1)) / 4.0f;
+        bb = (((SC(2, y - 1, x - 1) + SC(2, y - 1, x + 1)) +
+               SC(2, y + 1, x - 1)) + SC(2, y + 1, x + 1)) / 4.0f;
+      } else if (y % 2 == 0) { /* green site on a red row */
+        rr = (SC(0, y, x - 1) + SC(0, y, x + 1)) / 2.0f;
+        gg = SC(1, y, x);
+        bb = (SC(2, y - 1, x) + SC(2, y + 1, x)) / 2.0f;
+      } else if (x % 2 == 0) { /* green site on a blue row */
+        rr = (SC(0, y - 1, x) + SC(0, y + 1, x)) / 2.0f;
+        gg = SC(1, y, x);
+        bb = (SC(2, y, x - 1) + SC(2, y, x + 1)) / 2.0f;
+      } else { /* blue site */
+        rr = (((SC(0, y - 1, x - 1) + SC(0, y - 1, x + 1)) +
+               SC(0, y + 1, x - 1)) + SC(0, y + 1, x + 1)) / 4.0f;
+        gg = (((SC(1, y - 1, x) + SC(1, y + 1, x)) + SC(1, y, x - 1)) +
+              SC(1, y, x + 1)) / 4.0f;
+        bb = SC(2, y, x);
+      }
+      dm[0 * N + y * C + x] = rr;
+      dm[1 * N + y * C + x] = gg;
+      dm[2 * N + y * C + x] = bb;
+    }
+#undef SC
+}
+
+EXPORT void jo_cava_denoise(int64_t R, int64_t C, const float *dm, float *dn) {
+  const int64_t N = R * C;
+#pragma omp parallel for schedule(static)
+  for (int64_t y = 0; y < R; y++)
+    for (int64_t x = 0; x < C; x++)
+      for (int ch = 0; ch < 3; ch++) {
+        if (y == 0 || x == 0 || y == R - 1 || x == C - 1) {
+          dn[ch * N + y * C + x] = dm[ch * N + y * C + x];
+        } else {
+          float w[9];
+          int t = 0;
+          for (int i = -1; i <= 1; i++)
+            for (int j = -1; j <= 1; j++)
+              w[t++] = dm[ch * N + (y + i) * C + (x + j)];
+          dn[ch * N + y * C + x] = median9(w);
+        }
+      }
+}
+
+EXPORT void jo_cava_transform(int64_t N, const float *in, const float *tstw, float *tr) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++)
+    for (int ch = 0; ch < 3; ch++) {
+      float s = 0.0f;
+      for (int q = 0; q < 3; q++) s = s + tstw[ch * 3 + q] * in[q * N + k];
+      tr[ch * N + k] = s;
+    }
+}
+
+EXPORT void jo_cava_gamut(int64_t N, int64_t P, const float *tr, const float *ctrl,
+                          const float *wts, const float *coefs, float *gm) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++) {
+    const float x0 = tr[0 * N + k], x1 = tr[1 * N + k], x2 = tr[2 * N + k];
+    float gv[3] = {0.0f, 0.0f, 0.0f};
+    for (int64_t p = 0; p < P; p++) {
+      const float d0 = x0 - ctrl[p * 3 + 0];
+      const float d1 = x1 - ctrl[p * 3 + 1];
+      const float d2 = x2 - ctrl[p * 3 + 2];
+      const float dist = sqrtf((d0 * d0 + d1 * d1) + d2 * d2);
+      for (int ch = 0; ch < 3; ch++) gv[ch] = gv[ch] + dist * wts[p * 3 + ch];
+    }
+    for (int ch = 0; ch < 3; ch++) {
+      const float aff = ((coefs[0 * 3 + ch] + coefs[1 * 3 + ch] * x0) +
+                         coefs[2 * 3 + ch] * x1) + coefs[3 * 3 + ch] * x2;
+      gm[ch * N + k] = gv[ch] + aff;
+    }
+  }
+}
+
+EXPORT void jo_cava_tonemap_descale(int64_t N, const float *gm, const float *tmap,
+                                    uint8_t *out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++)
+    for (int ch = 0; ch < 3; ch++) {
+      const int idx = (int)clamp255(gm[ch * N + k] * 255.0f);
+      const float tm = tmap[idx * 3 + ch];
+      out[ch * N + k] = (uint8_t)(int)clamp255(tm * 255.0f);
+    }
+}
+
+EXPORT void jo_cava_frame_u8(int64_t R, int64_t C, int64_t P,
+                             const uint8_t *in, const float *tstw,
+                             const float *ctrl, const float *wts,
+                             const float *coefs, const float *tmap,
+                             uint8_t *out, float *demosaic_o,
+                             float *denoise_o, float *gamut_o) {
+  const int64_t N = R * C;
+  float *sc = (float *)malloc(3 * N * sizeof(float));
+  float *dm = demosaic_o ? demosaic_o : (float *)malloc(3 * N * sizeof(float));
+  float *dn = denoise_o ? denoise_o : (float *)malloc(3 * N * sizeof(float));
+  float *gm = gamut_o ? gamut_o : (float *)malloc(3 * N * sizeof(float));
+  jo_cava_scale(R, C, in, sc);
+  jo_cava_demosaic(R, C, sc, dm);
+  jo_cava_denoise(R, C, dm, dn);
+  jo_cava_transform(N, dn, tstw, sc); /* sc reused for the transformed planes */
+  jo_cava_gamut(N, P, sc, ctrl, wts, coefs, gm);
+  jo_cava_tonemap_descale(N, gm, tmap, out);
+  free(sc);
+  if (!demosaic_o) free(dm);
+  if (!denoise_o) free(dn);
+  if (!gamut_o) free(gm);
+}
+
+EXPORT void jo_cava_u8(int64_t batch, int64_t R, int64_t C, int64_t P,
+                       const uint8_t *in, const float *tstw, const float *ctrl,
+                       const float *wts, const float *coefs,
+                       const float *tmap, uint8_t *out) {
+  for (int64_t f = 0; f < batch; f++)
+    jo_cava_frame_u8(R, C, P, in + f * 3 * R * C, tstw, ctrl, wts, coefs, tmap,
+                     out + f * 3 * R * C, NULL, NULL, NULL);
+}
+
+/* ------------------------------------------------------------------------
+ * srad<rows,cols>(niter, lambda, image f32[rows,cols]) -> f32[rows,cols]
+ * Rodinia srad_v1 restated on a row-major image:
+ *   J = exp(I/255); per iteration: q0^2 from Σ J, Σ J^2 (f64 accumulation);
+ *   diffusion coefficient with clamped neighbour indices; J += (λ/4)·D;
+ *   out = log(J)·255.
+ * q0sqr_o (niter floats, may be NULL) receives each iteration's q0^2.
+ * ---------------------------------------------------------------------- */
+/* one iteration given q0sqr: coefficient pass then update pass (in place) */
+EXPORT void jo_srad_iter(int64_t rows, int64_t cols, float q0sqr, float lambda,
+                         float *J, float *c, float *dN, float *dS, float *dW,
+                         float *dE) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; i++) {
+    const int64_t iN = i > 0 ? i - 1 : 0, iS = i < rows - 1 ? i + 1 : rows - 1;
+    for (int64_t j = 0; j < cols; j++) {
+      const int64_t jW = j > 0 ? j - 1 : 0, jE = j < cols - 1 ? j + 1 : cols - 1;
+      const int64_t k = i * cols + j;
+      const float Jc = J[k];
+      const float n_ = J[iN * cols + j] - Jc, s_ = J[iS * cols + j] - Jc;
+      const float w_ = J[i * cols + jW] - Jc, e_ = J[i * cols + jE] - Jc;
+      dN[k] = n_; dS[k] = s_; dW[k] = w_; dE[k] = e_;
+      const float G2 = (((n_ * n_ + s_ * s_) + w_ * w_) + e_ * e_) / (Jc * Jc);
+      const float L = (((n_ + s_) + w_) + e_) / Jc;
+      const float num = (0.5f * G2) - (0.0625f * (L * L));
+      const float den = 1.0f + (0.25f * L);
+      const float qsqr = num / (den * den);
+      const float den2 = (qsqr - q0sqr) / (q0sqr * (1.0f + q0sqr));
+      float cc = 1.0f / (1.0f + den2);
+      cc = cc < 0.0f ? 0.0f : (cc > 1.0f ? 1.0f : cc);
+      c[k] = cc;
+    }
+  }
+  const float ql = 0.25f * lambda;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; i++) {
+    const int64_t iS = i < rows - 1 ? i + 1 : rows - 1;
+    for (int64_t j = 0; j < cols; j++) {
+      const int64_t jE = j < cols - 1 ? j + 1 : cols - 1;
+      const int64_t k = i * cols + j;
+      const float cN = c[k], cS = c[iS * cols + j], cW = c[k],
+                  cE = c[i * cols + jE];
+      const float D = ((cN * dN[k] + cS * dS[k]) + cW * dW[k]) + cE * dE[k];
+      J[k] = J[k] + ql * D;
+    }
+  }
+}
+
+/* q0^2 of the current image: f64 sums (see header), rounded once to f32 */
+EXPORT float jo_srad_q0sqr(int64_t N, const float *J) {
+  double sum = 0.0, sum2 = 0.0;
+  for (int64_t k = 0; k < N; k++) {
+    const double t = (double)J[k];
+    sum += t;
+    sum2 += t * t;
+  }
+  const double mean = sum / (double)N;
+  const double var = sum2 / (double)N - mean * mean;
+  return (float)(var / (mean * mean));
+}
+
+EXPORT void jo_srad_f32(int64_t rows, int64_t cols, int64_t niter,
+                        float lambda, const float *image, float *out,
+                        float *q0sqr_o) {
+  const int64_t N = rows * cols;
+  float *J = (float *)malloc(N * sizeof(float));
+  float *c = (float *)malloc(N * sizeof(float));
+  float *dN = (float *)malloc(N * sizeof(float));
+  float *dS = (float *)malloc(N * sizeof(float));
+  float *dW = (float *)malloc(N * sizeof(float));
+  float *dE = (float *)malloc(N * sizeof(float));
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++) J[k] = exp_ref(image[k] / 255.0f);
+  for (int64_t it = 0; it < niter; it++) {
+    const float q0sqr = jo_srad_q0sqr(N, J);
+    if (q0sqr_o) q0sqr_o[it] = q0sqr;
+    jo_srad_iter(rows, cols, q0sqr, lambda, J, c, dN, dS, dW, dE);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < N; k++) out[k] = log_ref(J[k]) * 255.0f;
+  free(J); free(c); free(dN); free(dS); free(dW); free(dE);
+}
+
+/* ------------------------------------------------------------------------
+ * euler<nelr>(iterations, areas f32[nelr], neighbors i32[4,nelr],
+ *             normals f32[4,3,nelr], ff_variable f32[5],
+ *             variables f32[5,nelr]) -> f32[5,nelr]
+ * Rodinia cfd/euler3d restated (CFD/EULER), SoA
+ * layout: variables[v*nelr+i], neighbors[j*nelr+i],
+ * normals[(j*3+d)*nelr+i].  Neighbour -1 = wall, -2 = far field.
+ * ---------------------------------------------------------------------- */
+#define GAMMA 1.4f
+#define NNB 4
+#define NVAR 5
+#define RK 3
+
+typedef struct { float x, y, z; } f3;
+
+static inline f3 velocity(float rho, f3 mom) {
+  f3 v = {mom.x / rho, mom.y / rho, mom.z / rho};
+  return v;
+}
+static inline float speed_sqd(f3 v) { return (v.x * v.x + v.y * v.y) + v.z * v.z; }
+static inline float pressure(float rho, float rhoE, float ssq) {
+  return (GAMMA - 1.0f) * (rhoE - (0.5f * rho) * ssq);
+}
+static inline float sound(float rho, float p) { return sqrtf((GAMMA * p) / rho); }
+static inline void flux_contrib(float rhoE, float p, f3 mom, f3 v, f3 *fx,
+                                f3 *fy, f3 *fz, f3 *fe) {
+  fx->x = v.x * mom.x + p; fx->y = v.x * mom.y; fx->z = v.x * mom.z;
+  fy->x = fx->y; fy->y = v.y * mom.y + p; fy->z = v.y * mom.z;
+  fz->x = fx->z; fz->y = fy->z; fz->z = v.z * mom.z + p;
+  const float dep = rhoE + p;
+  fe->x = v.x * dep; fe->y = v.y * dep; fe->z = v.z * dep;
+}
+
+EXPORT void jo_euler_step_factor(int64_t nelr, const float *vars,
+                                 const float *areas, float *sf) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nelr; i++) {
+    const float rho = vars[0 * nelr + i];
+    const f3 mom = {vars[1 * nelr + i], vars[2 * nelr + i], vars[3 * nelr + i]};
+    const float rhoE = vars[4 * nelr + i];
+    const f3 v = velocity(rho, mom);
+    const float ssq = speed_sqd(v);
+    const float p = pressure(rho, rhoE, ssq);
+    const float a = sound(rho, p);
+    sf[i] = 0.5f / (sqrtf(areas[i]) * (sqrtf(ssq) + a));
+  }
+}
+
+EXPORT void jo_euler_flux(int64_t nelr, const int32_t *nbrs,
+                          const float *normals, const float *ff,
+                          const float *vars, float *fluxes) {
+  /* far-field flux contributions */
+  const f3 ffm = {ff[1], ff[2], ff[3]};
+  const f3 ffv = velocity(ff[0], ffm);
+  const float ffp = pressure(ff[0], ff[4], speed_sqd(ffv));
+  f3 ffx, ffy, ffz, ffe;
+  flux_contrib(ff[4], ffp, ffm, ffv, &ffx, &ffy, &ffz, &ffe);
+  const float smoothing = 0.2f;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nelr; i++) {
+    const float rho_i = vars[0 * nelr + i];
+    const f3 mom_i = {vars[1 * nelr + i], vars[2 * nelr + i], vars[3 * nelr + i]};
+    const float rhoE_i = vars[4 * nelr + i];
+    const f3 v_i = velocity(rho_i, mom_i);
+    const float ssq_i = speed_sqd(v_i);
+    const float sp_i = sqrtf(ssq_i);
+    const float p_i = pressure(rho_i, rhoE_i, ssq_i);
+    const float a_i = sound(rho_i, p_i);
+    f3 fx_i, fy_i, fz_i, fe_i;
+    flux_contrib(rhoE_i, p_i, mom_i, v_i, &fx_i, &fy_i, &fz_i, &fe_i);
+    float f_rho = 0.0f, f_rhoE = 0.0f;
+    f3 f_mom = {0.0f, 0.0f, 0.0f};
+    for (int j = 0; j < NNB; j++) {
+      const int32_t nb = nbrs[j * nelr + i];
+      const f3 nrm = {normals[(j * 3 + 0) * nelr + i],
+                      normals[(j * 3 + 1) * nelr + i],
+                      normals[(j * 3 + 2) * nelr + i]};
+      const float nlen = sqrtf((nrm.x * nrm.x + nrm.y * nrm.y) + nrm.z * nrm.z);
+      if (nb >= 0) {
+        const float rho_n = vars[0 * nelr + nb];
+        const f3 mom_n = {vars[1 * nelr + nb], vars[2 * nelr + nb], vars[3 * nelr + nb]};
+        const float rhoE_n = vars[4 * nelr + nb];
+        const f3 v_n = velocity(rho_n, mom_n);
+        const float ssq_n = speed_sqd(v_n);
+        const float p_n = pressure(rho_n, rhoE_n, ssq_n);
+        const float a_n = sound(rho_n, p_n);
+        f3 fx_n, fy_n, fz_n, fe_n;
+        flux_contrib(rhoE_n, p_n, mom_n, v_n, &fx_n, &fy_n, &fz_n, &fe_n);
+        float factor = (((-nlen) * smoothing) * 0.5f) *
+                       (((sp_i + sqrtf(ssq_n)) + a_i) + a_n);
+        f_rho = f_rho + factor * (rho_i - rho_n);
+        f_rhoE = f_rhoE + factor * (rhoE_i - rhoE_n);
+        f_mom.x = f_mom.x + factor * (mom_i.x - mom_n.x);
+        f_mom.y = f_mom.y + factor * (mom_i.y - mom_n.y);
+        f_mom.z = f_mom.z + factor * (mom_i.z - mom_n.z);
+        factor = 0.5f * nrm.x;
+        f_rho = f_rho + factor * (mom_n.x + mom_i.x);
+        f_rhoE = f_rhoE + factor * (fe_n.x + fe_i.x);
+        f_mom.x = f_mom.x + factor * (fx_n.x + fx_i.x);
+        f_mom.y = f_mom.y + factor * (fy_n.x + fy_i.x);
+        f_mom.z = f_mom.z + factor * (fz_n.x + fz_i.x);
+        factor = 0.5f * nrm.y;
+        f_rho = f_rho + factor * (mom_n.y + mom_i.y);
+        f_rhoE = f_rhoE + factor * (fe_n.y + fe_i.y);
+        f_mom.x = f_mom.x + factor * (fx_n.y + fx_i.y);
+        f_mom.y = f_mom.y + factor * (fy_n.y + fy_i.y);
+        f_mom.z = f_mom.z + factor * (fz_n.y + fz_i.y);
+        factor = 0.5f * nrm.z;
+        f_rho = f_rho + factor * (mom_n.z + mom_i.z);
+        f_rhoE = f_rhoE + factor * (fe_n.z + fe_i.z);
+        f_mom.x = f_mom.x + factor * (fx_n.z + fx_i.z);
+        f_mom.y = f_mom.y + factor * (fy_n.z + fy_i.z);
+        f_mom.z = f_mom.z + factor * (fz_n.z + fz_i.z);
+      } else if (nb == -1) {
+        f_mom.x = f_mom.x + nrm.x * p_i;
+        f_mom.y = f_mom.y + nrm.y * p_i;
+        f_mom.z = f_mom.z + nrm.z * p_i;
+      } else if (nb == -2) {
+        float factor = 0.5f * nrm.x;
+        f_rho = f_rho + factor * (ffm.x + mom_i.x);
+        f_rhoE = f_rhoE + factor * (ffe.x + fe_i.x);
+        f_mom.x = f_mom.x + factor * (ffx.x + fx_i.x);
+        f_mom.y = f_mom.y + factor * (ffy.x + fy_i.x);
+        f_mom.z = f_mom.z + factor * (ffz.x + fz_i.x);
+        factor = 0.5f * nrm.y;
+        f_rho = f_rho + factor * (ffm.y + mom_i.y);
+        f_rhoE = f_rhoE + factor * (ffe.y + fe_i.y);
+        f_mom.x = f_mom.x + factor * (ffx.y + fx_i.y);
+        f_mom.y = f_mom.y + factor * (ffy.y + fy_i.y);
+        f_mom.z = f_mom.z + factor * (ffz.y + fz_i.y);
+        factor = 0.5f * nrm.z;
+        f_rho = f_rho + factor * (ffm.z + mom_i.z);
+        f_rhoE = f_rhoE + factor * (ffe.z + fe_i.z);
+        f_mom.x = f_mom.x + factor * (ffx.z + fx_i.z);
+        f_mom.y = f_mom.y + factor * (ffy.z + fy_i.z);
+        f_mom.z = f_mom.z + factor * (ffz.z + fz_i.z);
+      }
+    }
+    fluxes[0 * nelr + i] = f_rho;
+    fluxes[1 * nelr + i] = f_mom.x;
+    fluxes[2 * nelr + i] = f_mom.y;
+    fluxes[3 * nelr + i] = f_mom.z;
+    fluxes[4 * nelr + i] = f_rhoE;
+  }
+}
+
+EXPORT void jo_euler_f32(int64_t nelr, int64_t iterations, const float *areas,
+                         const int32_t *nbrs, const float *normals,
+                         const float *ff, float *vars) {
+  float *old = (float *)malloc(NVAR * nelr * sizeof(float));
+  float *sf = (float *)malloc(nelr * sizeof(float));
+  float *fl = (float *)malloc(NVAR * nelr * sizeof(float));
+  for (int64_t it = 0; it < iterations; it++) {
+    memcpy(old, vars, NVAR * nelr * sizeof(float));
+    jo_euler_step_factor(nelr, vars, areas, sf);
+    for (int j = 0; j < RK; j++) {
+      jo_euler_flux(nelr, nbrs, normals, ff, vars, fl);
+      const float div = (float)(RK + 1 - j);
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < nelr; i++) {
+        const float factor = sf[i] / div;
+        for (int v = 0; v < NVAR; v++)
+          vars[v * nelr + i] = old[v * nelr + i] + factor * fl[v * nelr + i];
+      }
+    }
+  }
+  free(old); free(sf); free(fl);
+}
+
+/* ------------------------------------------------------------------------
+ * bfs<n,m>(starting u32[n], no_of_edges u32[n], edges u32[m], source)
+ *   -> i32[n]              (Rodinia BFS; level = cost[u] + 1, -1 unreachable)
+ * ---------------------------------------------------------------------- */
+EXPORT void jo_bfs(int64_t n, int64_t m, const uint32_t *starting,
+                   const uint32_t *nedges, const uint32_t *edges,
+                   uint32_t source, int32_t *cost) {
+  (void)m;
+  uint32_t *q = (uint32_t *)malloc((n > 0 ? n : 1) * sizeof(uint32_t));
+  for (int64_t i = 0; i < n; i++) cost[i] = -1;
+  if (n == 0) { free(q); return; }
+  int64_t head = 0, tail = 0;
+  cost[source] = 0;
+  q[tail++] = source;
+  while (head < tail) {
+    const uint32_t u = q[head++];
+    const uint32_t s = starting[u], e = s + nedges[u];
+    for (uint32_t k = s; k < e; k++) {
+      const uint32_t v = edges[k];
+      if (cost[v] < 0) {
+        cost[v] = cost[u] + 1;
+        q[tail++] = v;
+      }
+    }
+  }
+  free(q);
+}
+
+/* ------------------------------------------------------------------------
+ * backprop<n_in,n_hid,n_out>: one Rodinia bpnn_train step
+ *   layerforward(in->hid), layerforward(hid->out), output_error,
+ *   hidden_error, adjust_weights(hid->out), adjust_weights(in->hid).
+ * Weight matrices are (n_from+1) x (n_to+1) row-major, unit 0 = bias.
+ * acc64 = 1: the layer sums are accumulated in f64 and rounded once (the
+ * re-associated reduction the GPU computes); acc64 = 0: sequential f32.
+ * outs: hidden[n_hid+1], output[n_out+1], delta_o[n_out+1],
+ *       delta_h[n_hid+1], errs[2] = {out_err, hid_err}.
+ * ---------------------------------------------------------------------- */
+#define ETA 0.3f
+#define MOMENTUM 0.3f
+
+static inline float squash(float x) { return 1.0f / (1.0f + exp_ref(-x)); }
+
+EXPORT void jo_bp_layerforward(int64_t n1, int64_t n2, float *l1,
+                               const float *conn, float *l2, int acc64) {
+  l1[0] = 1.0f;
+  for (int64_t j = 1; j <= n2; j++) {
+    float s;
+    if (acc64) {
+      double d = 0.0;
+#pragma omp parallel for reduction(+ : d) schedule(static)
+      for (int64_t k = 0; k <= n1; k++) d += (double)(conn[k * (n2 + 1) + j] * l1[k]);
+      s = (float)d;
+    } else {
+      s = 0.0f;
+      for (int64_t k = 0; k <= n1; k++) s = s + conn[k * (n2 + 1) + j] * l1[k];
+    }
+    l2[j] = squash(s);
+  }
+}
+
+/* raw layer sums (no squash), sequential f32 or f64-accumulated */
+EXPORT void jo_bp_layer_sums(int64_t n1, int64_t n2, const float *l1,
+                             const float *conn, float *sums, int acc64) {
+  for (int64_t j = 0; j <= n2; j++) {
+    if (acc64) {
+      double d = 0.0;
+      for (int64_t k = 0; k <= n1; k++) d += (double)(conn[k * (n2 + 1) + j] * l1[k]);
+      sums[j] = (float)d;
+    } else {
+      float s = 0.0f;
+      for (int64_t k = 0; k <= n1; k++) s = s + conn[k * (n2 + 1) + j] * l1[k];
+      sums[j] = s;
+    }
+  }
+}
+
+EXPORT void jo_bp_adjust_weights(const float *delta, int64_t ndelta, float *ly,
+                                 int64_t nly, float *w, float *oldw) {
+  ly[0] = 1.0f;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k <= nly; k++)
+    for (int64_t j = 1; j <= ndelta; j++) {
+      const int64_t x = k * (ndelta + 1) + j;
+      const float new_dw = ((ETA * delta[j]) * ly[k]) + (MOMENTUM * oldw[x]);
+      w[x] = w[x] + new_dw;
+      oldw[x] = new_dw;
+    }
+}
+
+EXPORT void jo_bp_train(int64_t n_in, int64_t n_hid, int64_t n_out,
+                        float *input, float *in_w, float *hid_w,
+                        const float *target, float *in_prev_w,
+                        float *hid_prev_w, float *hidden, float *output,
+                        float *delta_o, float *delta_h, float *errs,
+                        int acc64) {
+  jo_bp_layerforward(n_in, n_hid, input, in_w, hidden, acc64);
+  jo_bp_layerforward(n_hid, n_out, hidden, hid_w, output, 0);
+  float eo = 0.0f;
+  for (int64_t j = 1; j <= n_out; j++) {
+    const float o = output[j], t = target[j];
+    delta_o[j] = (o * (1.0f - o)) * (t - o);
+    eo = eo + fabsf(delta_o[j]);
+  }
+  float eh = 0.0f;
+  for (int64_t j = 1; j <= n_hid; j++) {
+    const float h = hidden[j];
+    float s = 0.0f;
+    for (int64_t k = 1; k <= n_out; k++) s = s + delta_o[k] * hid_w[j * (n_out + 1) + k];
+    delta_h[j] = (h * (1.0f - h)) * s;
+    eh = eh + fabsf(delta_h[j]);
+  }
+  errs[0] = eo;
+  errs[1] = eh;
+  jo_bp_adjust_weights(delta_o, n_out, hidden, n_hid, hid_w, hid_prev_w);
+  jo_bp_adjust_weights(delta_h, n_hid, input, n_in, in_w, in_prev_w);
+}

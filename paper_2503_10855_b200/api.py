@@ -1,0 +1,481 @@
+"""Host-side mirror of the reference's execution interface.
+
+The reference executes a Juno entry function with
+``oracle_execute(module, entry, dyn_consts, args, max_steps)``
+(/root/reference/pkg/src/skiff/runtime/oracle.py:28-32): dynamic constants
+in declaration order, then arguments in parameter order, numpy arrays in and
+numpy arrays out, value semantics (inputs never mutated, fresh outputs;
+oracle.py:119-129).  ``execute``/``oracle_execute`` below keep that contract
+for the seven Juno benchmark entries and run them on the B200 through
+libjunob200.so.  Per-benchmark functions (``matmul``, ``edge_detection`` ...)
+are the same calls without the dyn-const list (they are inferred from the
+shapes, like the paper's runner).
+
+Arguments may be numpy arrays (host: copied to the device, result copied
+back -- the end-to-end path) or CUDA torch tensors (device-resident: the
+result stays on the device).  PyTorch is used only for device memory and
+streams; all arithmetic happens in the CUDA kernels.
+
+Errors mirror the reference's classes: ``DynConstError`` for negative or
+inconsistent dynamic constants (dynconst.py:16-17,179-204) and
+``RuntimeError_`` for shape violations (values.py:20, oracle.py:158-159).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Any, Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+
+
+class RuntimeError_(Exception):
+    """Mirror of skiff.runtime.values.RuntimeError_."""
+
+
+class DynConstError(Exception):
+    """Mirror of skiff.dynconst.DynConstError."""
+
+
+class OracleLimitError(RuntimeError_):
+    """Mirror of skiff.runtime.oracle.OracleLimitError (never raised: the
+    device path has no interpreter step budget)."""
+
+
+class UnsupportedError(RuntimeError_):
+    """The entry/config has no kernel in this build (JB_ENOTSUP)."""
+
+
+def _torch():
+    import torch  # deferred: importing the package must not need a GPU
+    return torch
+
+
+def _check(status: int, what: str) -> None:
+    if status == _lib.JB_OK:
+        return
+    msg = f"{what}: {_lib.last_error()}"
+    if status == _lib.JB_EINVAL:
+        raise RuntimeError_(msg)
+    if status == _lib.JB_ENOTSUP:
+        raise UnsupportedError(msg)
+    raise RuntimeError(msg)
+
+
+# ----------------------------------------------------------------- marshalling
+_NP2TORCH = {}
+
+
+def _torch_dtype(np_dtype):
+    torch = _torch()
+    if not _NP2TORCH:
+        _NP2TORCH.update({np.dtype(np.float32): torch.float32, np.dtype(np.int32): torch.int32,
+                          np.dtype(np.uint8): torch.uint8, np.dtype(np.uint32): torch.uint32,
+                          np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64})
+    return _NP2TORCH[np.dtype(np_dtype)]
+
+
+class _Call:
+    """Collects device buffers for one call; remembers whether results must
+    be copied back to the host (numpy in -> numpy out)."""
+
+    def __init__(self, args, device=None):
+        torch = _torch()
+        self.host = not any(isinstance(a, torch.Tensor) for a in args)
+        if device is None:
+            dev = next((a.device for a in args if isinstance(a, torch.Tensor) and a.is_cuda), None)
+            device = dev if dev is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise RuntimeError_("libjunob200 computes on CUDA devices only (no CPU fallback)")
+        self.stream = torch.cuda.current_stream(self.device)
+
+    def dev(self, x, np_dtype, name: str, copy: bool = False):
+        torch = _torch()
+        want = _torch_dtype(np_dtype)
+        if isinstance(x, torch.Tensor):
+            if x.dtype != want:
+                raise RuntimeError_(f"{name}: expected {np.dtype(np_dtype).name}, got {x.dtype}")
+            t = x.to(self.device, non_blocking=True)
+            if not t.is_contiguous():
+                t = t.contiguous()
+            elif copy and t.data_ptr() == x.data_ptr():
+                t = t.clone()
+            return t
+        a = np.asarray(x)
+        if a.dtype != np.dtype(np_dtype):
+            if a.dtype.kind != np.dtype(np_dtype).kind and not (a.dtype.kind in "iu" and
+                                                                np.dtype(np_dtype).kind in "iu"):
+                raise RuntimeError_(f"{name}: expected {np.dtype(np_dtype).name}, got {a.dtype}")
+            a = a.astype(np_dtype)
+        a = np.ascontiguousarray(a)
+        # uint32 has limited torch support: move the raw bytes as int32
+        if a.dtype == np.uint32:
+            return torch.from_numpy(a.view(np.int32)).to(self.device, non_blocking=False)
+        return torch.from_numpy(a).to(self.device, non_blocking=False)
+
+    def empty(self, shape, np_dtype):
+        torch = _torch()
+        return torch.empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype), device=self.device)
+
+    def out(self, t):
+        if self.host:
+            return t.cpu().numpy()
+        return t
+
+    @property
+    def s(self):
+        return self.stream.cuda_stream
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _shape(x) -> tuple:
+    return tuple(int(s) for s in x.shape)
+
+
+def _need(cond: bool, msg: str):
+    if not cond:
+        raise RuntimeError_(msg)
+
+
+def _scalar(x, ty=float):
+    if hasattr(x, "item"):
+        x = x.item()
+    return ty(x)
+
+
+# ---------------------------------------------------------------------- matmul
+def matmul(a, b):
+    """matmul<n,m,l>(a: f32[n,m], b: f32[m,l]) -> f32[n,l]."""
+    _need(len(_shape(a)) == 2 and len(_shape(b)) == 2, "matmul: a and b must be 2-D")
+    n, m = _shape(a)
+    m2, l = _shape(b)
+    _need(m == m2, f"matmul: inner extents differ ({m} vs {m2})")
+    c = _Call([a, b])
+    da, db = c.dev(a, np.float32, "a"), c.dev(b, np.float32, "b")
+    out = c.empty((n, l), np.float32)
+    _check(_lib.load().jb_matmul_f32(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+    return c.out(out)
+
+
+# ------------------------------------------------------------------------ edge
+def edge_detection(input, gaussian_filter, structure, sx, sy, theta):
+    """edge_detection<n,m,gs,sz,sb>(input f32[n,m] | f32[batch,n,m], ...) -> f32.
+
+    A 3-D input is a batch of independent frames (the north star's batched
+    edge workload); each frame has its own max-gradient reduction."""
+    shp = _shape(input)
+    _need(len(shp) in (2, 3), "edge_detection: input must be f32[n,m] or f32[batch,n,m]")
+    batch, n, m = (1, *shp) if len(shp) == 2 else shp
+    gs, sz, sb = (_shape(x)[0] for x in (gaussian_filter, structure, sx))
+    _need(_shape(gaussian_filter) == (gs, gs), "edge_detection: gaussian_filter must be square")
+    _need(_shape(structure) == (sz, sz), "edge_detection: structure must be square")
+    _need(_shape(sx) == (sb, sb) and _shape(sy) == (sb, sb), "edge_detection: sx/sy must be sb x sb")
+    c = _Call([input, gaussian_filter, structure, sx, sy])
+    din = c.dev(input, np.float32, "input")
+    dg, dst, dsx, dsy = (c.dev(x, np.float32, nm) for x, nm in
+                         ((gaussian_filter, "gaussian_filter"), (structure, "structure"), (sx, "sx"),
+                          (sy, "sy")))
+    out = c.empty(shp, np.float32)
+    _check(_lib.load().jb_edge_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst), _ptr(dsx),
+                                   _ptr(dsy), _scalar(theta), _ptr(out), c.s), "edge_detection")
+    return c.out(out)
+
+
+_PIPE_CACHE: dict = {}
+
+
+def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 8):
+    """Host-buffer edge detection with copy/compute overlap.
+
+    ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
+    memory gives full PCIe bandwidth).  Frames move in chunks through two
+    device slots on three streams -- H2D of chunk i+1 and D2H of chunk i-1
+    overlap the kernels of chunk i -- so the call is bound by the slower
+    PCIe direction instead of the sum of copy and compute time.  Returns
+    ``out`` (a host f32 tensor/array of the input's shape)."""
+    torch = _torch()
+    x = input if isinstance(input, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(input, np.float32))
+    _need(x.dtype == torch.float32 and x.dim() == 3 and not x.is_cuda,
+          "edge_detection_pipelined: input must be a host f32[batch,n,m]")
+    B, n, m = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty_like(x, pin_memory=x.is_pinned())
+    gs, sz, sb = (_shape(f)[0] for f in (gaussian_filter, structure, sx))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = (dev.index, n, m, chunk)
+    st = _PIPE_CACHE.get(key)
+    if st is None:
+        st = dict(inb=[torch.empty((chunk, n, m), dtype=torch.float32, device=dev) for _ in range(2)],
+                  outb=[torch.empty((chunk, n, m), dtype=torch.float32, device=dev) for _ in range(2)],
+                  s_in=torch.cuda.Stream(dev), s_out=torch.cuda.Stream(dev))
+        _PIPE_CACHE[key] = st
+    comp = torch.cuda.current_stream(dev)
+    filt = [(f.to(dev) if isinstance(f, torch.Tensor) else
+             torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
+            for f in (gaussian_filter, structure, sx, sy)]
+    lib = _lib.load()
+    s_in, s_out = st["s_in"], st["s_out"]
+    c_done = [None, None]
+    d_done = [None, None]
+    for i, f0 in enumerate(range(0, B, chunk)):
+        k = min(chunk, B - f0)
+        slot = i & 1
+        din, dout = st["inb"][slot], st["outb"][slot]
+        with torch.cuda.stream(s_in):
+            if c_done[slot] is not None:
+                s_in.wait_event(c_done[slot])
+            din[:k].copy_(x[f0:f0 + k], non_blocking=True)
+            h_ev = torch.cuda.Event()
+            h_ev.record(s_in)
+        comp.wait_event(h_ev)
+        if d_done[slot] is not None:
+            comp.wait_event(d_done[slot])
+        _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
+                               filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(),
+                               comp.cuda_stream), "edge_detection")
+        c_ev = torch.cuda.Event()
+        c_ev.record(comp)
+        c_done[slot] = c_ev
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(c_ev)
+            out[f0:f0 + k].copy_(dout[:k], non_blocking=True)
+            d_ev = torch.cuda.Event()
+            d_ev.record(s_out)
+        d_done[slot] = d_ev
+    s_out.synchronize()
+    comp.wait_stream(s_out)
+    return out
+
+
+def edge_detection_stages(input, gaussian_filter, structure, sx, sy, theta):
+    """Stage-level variant (tests): returns dict of every intermediate."""
+    shp = _shape(input)
+    batch, n, m = (1, *shp) if len(shp) == 2 else shp
+    gs, sz, sb = (_shape(x)[0] for x in (gaussian_filter, structure, sx))
+    c = _Call([input, gaussian_filter, structure, sx, sy])
+    din = c.dev(input, np.float32, "input")
+    dg, dst, dsx, dsy = (c.dev(x, np.float32, "filter") for x in (gaussian_filter, structure, sx, sy))
+    out, sm, lp, zc, gr = (c.empty(shp, np.float32) for _ in range(5))
+    mx = c.empty((batch,), np.float32)
+    _check(_lib.load().jb_edge_stages_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst),
+                                          _ptr(dsx), _ptr(dsy), _scalar(theta), _ptr(out), _ptr(sm),
+                                          _ptr(lp), _ptr(zc), _ptr(gr), _ptr(mx), c.s),
+           "edge_detection_stages")
+    return dict(out=c.out(out), smoothed=c.out(sm), laplacian=c.out(lp), zero_crossings=c.out(zc),
+                gradient=c.out(gr), max_gradient=c.out(mx))
+
+
+# ------------------------------------------------------------------------ cava
+def cava(input, tstw, ctrl_pts, weights, coefs, tonemap):
+    """cava<r,c,num_ctrl_pts>(input u8[3,r,c] | u8[batch,3,r,c], TsTw f32[3,3],
+    ctrl_pts f32[P,3], weights f32[P,3], coefs f32[4,3], tonemap f32[256,3]) -> u8."""
+    shp = _shape(input)
+    _need(len(shp) in (3, 4) and shp[-3] == 3, "cava: input must be u8[3,r,c] or u8[batch,3,r,c]")
+    batch = 1 if len(shp) == 3 else shp[0]
+    r, cc = shp[-2], shp[-1]
+    P = _shape(ctrl_pts)[0]
+    _need(_shape(tstw) == (3, 3), "cava: TsTw must be f32[3,3]")
+    _need(_shape(ctrl_pts) == (P, 3) and _shape(weights) == (P, 3), "cava: ctrl_pts/weights must be f32[P,3]")
+    _need(_shape(coefs) == (4, 3), "cava: coefs must be f32[4,3]")
+    _need(_shape(tonemap) == (256, 3), "cava: tonemap must be f32[256,3]")
+    c = _Call([input, tstw, ctrl_pts, weights, coefs, tonemap])
+    din = c.dev(input, np.uint8, "input")
+    dt, dc, dw, dco, dtm = (c.dev(x, np.float32, nm) for x, nm in
+                            ((tstw, "TsTw"), (ctrl_pts, "ctrl_pts"), (weights, "weights"),
+                             (coefs, "coefs"), (tonemap, "tonemap")))
+    out = c.empty(shp, np.uint8)
+    _check(_lib.load().jb_cava_u8(batch, r, cc, P, _ptr(din), _ptr(dt), _ptr(dc), _ptr(dw), _ptr(dco),
+                                  _ptr(dtm), _ptr(out), c.s), "cava")
+    return c.out(out)
+
+
+# ------------------------------------------------------------------------ srad
+def srad(niter, lam, image, return_q0sqr: bool = False):
+    """srad<rows,cols>(niter, lambda, image f32[rows,cols]) -> f32[rows,cols]."""
+    niter = _scalar(niter, int)
+    if niter < 0:
+        raise DynConstError(f"srad: niter must be >= 0 (got {niter})")
+    _need(len(_shape(image)) == 2, "srad: image must be f32[rows,cols]")
+    rows, cols = _shape(image)
+    c = _Call([image])
+    dimg = c.dev(image, np.float32, "image")
+    out = c.empty((rows, cols), np.float32)
+    q0 = c.empty((max(niter, 1),), np.float32)
+    _check(_lib.load().jb_srad_f32(rows, cols, niter, _scalar(lam), _ptr(dimg), _ptr(out), _ptr(q0), c.s),
+           "srad")
+    if return_q0sqr:
+        return c.out(out), c.out(q0[:niter])
+    return c.out(out)
+
+
+# ----------------------------------------------------------------------- euler
+def euler(iterations, areas, neighbors, normals, ff_variable, variables):
+    """euler<nelr>(iterations, areas f32[nelr], neighbors i32[4,nelr],
+    normals f32[4,3,nelr], ff_variable f32[5], variables f32[5,nelr]) -> f32[5,nelr]."""
+    iterations = _scalar(iterations, int)
+    if iterations < 0:
+        raise DynConstError("euler: iterations must be >= 0")
+    nelr = _shape(areas)[0]
+    _need(_shape(neighbors) == (4, nelr), "euler: neighbors must be i32[4,nelr]")
+    _need(_shape(normals) == (4, 3, nelr), "euler: normals must be f32[4,3,nelr]")
+    _need(_shape(ff_variable) == (5,), "euler: ff_variable must be f32[5]")
+    _need(_shape(variables) == (5, nelr), "euler: variables must be f32[5,nelr]")
+    c = _Call([areas, neighbors, normals, ff_variable, variables])
+    da = c.dev(areas, np.float32, "areas")
+    dn = c.dev(neighbors, np.int32, "neighbors")
+    dno = c.dev(normals, np.float32, "normals")
+    dff = c.dev(ff_variable, np.float32, "ff_variable")
+    dv = c.dev(variables, np.float32, "variables", copy=True)  # value semantics
+    _check(_lib.load().jb_euler_f32(nelr, iterations, _ptr(da), _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), c.s),
+           "euler")
+    return c.out(dv)
+
+
+def euler_step_factor(variables, areas):
+    nelr = _shape(areas)[0]
+    c = _Call([variables, areas])
+    dv, da = c.dev(variables, np.float32, "variables"), c.dev(areas, np.float32, "areas")
+    out = c.empty((nelr,), np.float32)
+    _check(_lib.load().jb_euler_step_factor_f32(nelr, _ptr(dv), _ptr(da), _ptr(out), c.s), "euler_step_factor")
+    return c.out(out)
+
+
+def euler_flux(neighbors, normals, ff_variable, variables):
+    nelr = _shape(neighbors)[1]
+    c = _Call([neighbors, normals, ff_variable, variables])
+    dn = c.dev(neighbors, np.int32, "neighbors")
+    dno, dff, dv = (c.dev(x, np.float32, "f") for x in (normals, ff_variable, variables))
+    out = c.empty((5, nelr), np.float32)
+    _check(_lib.load().jb_euler_flux_f32(nelr, _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), _ptr(out), c.s),
+           "euler_flux")
+    return c.out(out)
+
+
+# ------------------------------------------------------------------------- bfs
+def bfs(starting, no_of_edges, edges, source):
+    """bfs<n,m>(starting u32[n], no_of_edges u32[n], edges u32[m], source) -> i32[n]."""
+    n = _shape(starting)[0]
+    m = _shape(edges)[0]
+    _need(_shape(no_of_edges) == (n,), "bfs: no_of_edges must be u32[n]")
+    source = _scalar(source, int)
+    _need(n == 0 or 0 <= source < n, f"bfs: source {source} out of bounds for n={n}")
+    c = _Call([starting, no_of_edges, edges])
+    ds = c.dev(starting, np.uint32, "starting")
+    dne = c.dev(no_of_edges, np.uint32, "no_of_edges")
+    de = c.dev(edges, np.uint32, "edges") if m else c.empty((1,), np.int32)
+    cost = c.empty((n,), np.int32)
+    _check(_lib.load().jb_bfs(n, m, _ptr(ds), _ptr(dne), _ptr(de), source, _ptr(cost), c.s), "bfs")
+    return c.out(cost)
+
+
+# -------------------------------------------------------------------- backprop
+def backprop(input_vals, input_weights, hidden_weights, target, input_prev_weights, hidden_prev_weights):
+    """One Rodinia bpnn_train step (layerforward x2, output/hidden error,
+    adjust_weights x2).  Returns (out_err, hid_err, input_weights,
+    hidden_weights, input_prev_weights, hidden_prev_weights) -- fresh arrays
+    (value semantics; the inputs are not mutated)."""
+    n_in1, n_hid1 = _shape(input_weights)
+    n_hid1b, n_out1 = _shape(hidden_weights)
+    _need(n_hid1 == n_hid1b, "backprop: weight shapes disagree on the hidden layer")
+    _need(_shape(input_vals) == (n_in1,), "backprop: input_vals must be f32[n_in+1]")
+    _need(_shape(target) == (n_out1,), "backprop: target must be f32[n_out+1]")
+    _need(_shape(input_prev_weights) == (n_in1, n_hid1), "backprop: input_prev_weights shape")
+    _need(_shape(hidden_prev_weights) == (n_hid1, n_out1), "backprop: hidden_prev_weights shape")
+    c = _Call([input_vals, input_weights, hidden_weights, target, input_prev_weights, hidden_prev_weights])
+    dx = c.dev(input_vals, np.float32, "input_vals", copy=True)
+    diw = c.dev(input_weights, np.float32, "input_weights", copy=True)
+    dhw = c.dev(hidden_weights, np.float32, "hidden_weights", copy=True)
+    dt = c.dev(target, np.float32, "target")
+    dipw = c.dev(input_prev_weights, np.float32, "input_prev_weights", copy=True)
+    dhpw = c.dev(hidden_prev_weights, np.float32, "hidden_prev_weights", copy=True)
+    hidden = c.empty((n_hid1,), np.float32)
+    output = c.empty((n_out1,), np.float32)
+    errs = c.empty((2,), np.float32)
+    _check(_lib.load().jb_bp_train_f32(n_in1 - 1, n_hid1 - 1, n_out1 - 1, _ptr(dx), _ptr(diw), _ptr(dhw),
+                                       _ptr(dt), _ptr(dipw), _ptr(dhpw), _ptr(hidden), _ptr(output),
+                                       _ptr(errs), c.s), "backprop")
+    e = c.out(errs)
+    return (e[0], e[1], c.out(diw), c.out(dhw), c.out(dipw), c.out(dhpw))
+
+
+# --------------------------------------------------------- oracle_execute mirror
+@dataclass(frozen=True)
+class Entry:
+    dyn_consts: tuple[str, ...]
+    shapes: Callable[[Sequence[int], Sequence[Any]], list]  # expected (arg idx, shape) pairs
+    run: Callable[..., Any]
+
+
+def _sh(*pairs):
+    return list(pairs)
+
+
+ENTRIES: dict[str, Entry] = {
+    "matmul": Entry(("n", "m", "l"),
+                    lambda d, a: _sh((0, (d[0], d[1])), (1, (d[1], d[2]))),
+                    lambda d, a: matmul(*a)),
+    "edge_detection": Entry(("n", "m", "gs", "sz", "sb"),
+                            lambda d, a: _sh((0, (d[0], d[1])), (1, (d[2], d[2])), (2, (d[3], d[3])),
+                                             (3, (d[4], d[4])), (4, (d[4], d[4]))),
+                            lambda d, a: edge_detection(*a)),
+    "cava": Entry(("r", "c", "num_ctrl_pts"),
+                  lambda d, a: _sh((0, (3, d[0], d[1])), (1, (3, 3)), (2, (d[2], 3)), (3, (d[2], 3)),
+                                   (4, (4, 3)), (5, (256, 3))),
+                  lambda d, a: cava(*a)),
+    "srad": Entry(("nrows", "ncols"),
+                  lambda d, a: _sh((2, (d[0], d[1]))),
+                  lambda d, a: srad(*a)),
+    "euler": Entry(("nelr",),
+                   lambda d, a: _sh((1, (d[0],)), (2, (4, d[0])), (3, (4, 3, d[0])), (4, (5,)), (5, (5, d[0]))),
+                   lambda d, a: euler(*a)),
+    "bfs": Entry(("n", "m"),
+                 lambda d, a: _sh((0, (d[0],)), (1, (d[0],)), (2, (d[1],))),
+                 lambda d, a: bfs(*a)),
+    "backprop": Entry(("input_n", "hidden_n", "output_n"),
+                      lambda d, a: _sh((0, (d[0] + 1,)), (1, (d[0] + 1, d[1] + 1)), (2, (d[1] + 1, d[2] + 1)),
+                                       (3, (d[2] + 1,)), (4, (d[0] + 1, d[1] + 1)), (5, (d[1] + 1, d[2] + 1))),
+                      lambda d, a: backprop(*a)),
+}
+
+
+def execute(entry: str, dyn_consts, args):
+    """Run Juno ``entry`` on the B200: ``oracle_execute`` without the module."""
+    if entry not in ENTRIES:
+        raise RuntimeError_(f"no B200 kernel for entry {entry!r}; known: {sorted(ENTRIES)}")
+    spec = ENTRIES[entry]
+    dcs = [int(x) for x in dyn_consts]
+    if len(dcs) != len(spec.dyn_consts):
+        raise DynConstError(f"{entry}: expected {len(spec.dyn_consts)} dynamic constants "
+                            f"{spec.dyn_consts}, got {len(dcs)}")
+    for nm, v in zip(spec.dyn_consts, dcs):
+        if v < 0:
+            raise DynConstError(f"{entry}: dynamic constant {nm} = {v} is negative")
+    args = list(args)
+    for idx, want in spec.shapes(dcs, args):
+        if idx >= len(args):
+            raise RuntimeError_(f"{entry}: missing argument {idx}")
+        got = _shape(args[idx])
+        # edge/cava also accept a leading batch dimension
+        if got != tuple(want) and got[1:] != tuple(want):
+            raise RuntimeError_(f"{entry}: argument {idx} has shape {got}, expected {tuple(want)} "
+                                f"under dyn-consts {dict(zip(spec.dyn_consts, dcs))}")
+    return spec.run(dcs, args)
+
+
+def oracle_execute(module, entry: str, dyn_consts, args, max_steps: int = 50_000_000):
+    """Drop-in for skiff.runtime.oracle.oracle_execute (oracle.py:28-32).
+
+    ``module`` may be a skiff ``Module`` (its function table must contain
+    ``entry``) or None.  ``max_steps`` is accepted for signature parity; the
+    device path has no interpreter budget."""
+    del max_steps
+    fns = getattr(module, "functions", None)
+    if fns is not None and entry not in fns:
+        raise KeyError(entry)
+    return execute(entry, dyn_consts, args)

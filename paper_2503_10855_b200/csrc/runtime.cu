@@ -1,0 +1,192 @@
+// runtime.cu -- host runtime of libjunob200.so: status/error reporting, the
+// per-device scratch arena and launch accounting.
+//
+// The arena is the stand-in for the reference runner's allocation model
+// ("one allocation per device"): every entry
+// point asks for the scratch it needs, the arena grows to the largest request
+// seen on that device and is reused by later calls.
+#include <stdarg.h>
+#include <string.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace jb {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+struct Arena {
+  void *ptr = nullptr;
+  size_t cap = 0;
+};
+static Arena g_arena[64];
+static std::mutex g_arena_mu;
+
+void *workspace(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  Arena &a = g_arena[dev];
+  if (bytes <= a.cap) return a.ptr;
+  // growing: wait for in-flight users of the old block before freeing it
+  if (a.ptr) {
+    cudaStreamSynchronize(s);
+    cudaDeviceSynchronize();
+    cudaFree(a.ptr);
+    a.ptr = nullptr;
+    a.cap = 0;
+  }
+  size_t want = bytes + (bytes >> 3);  // 12.5% headroom against regrowth
+  want = (want + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+  if (cudaMalloc(&a.ptr, want) != cudaSuccess) {
+    cudaGetLastError();
+    a.ptr = nullptr;
+    set_error("scratch arena: cudaMalloc(%zu) failed", want);
+    return nullptr;
+  }
+  a.cap = want;
+  return a.ptr;
+}
+
+jb_status after_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s launch failed: %s", what, cudaGetErrorString(e));
+    return JB_ECUDA;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return JB_OK;
+}
+
+// ---------------------------------------------------------------- profiler
+// When enabled, prof_begin/prof_end record a CUDA event pair around a kernel
+// launch on the launching stream; jb_prof_read synchronises the events and
+// returns the summed device time per kernel name.  Used by bench.py to time
+// the dominant kernel inside the timed region.
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof_pending;
+static std::map<std::string, std::pair<double, uint64_t>> g_prof_acc;
+static std::vector<cudaEvent_t> g_prof_free;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) {
+    cudaEvent_t e = g_prof_free.back();
+    g_prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void *prof_begin(const char *name, cudaStream_t s) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return nullptr;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_pending.push_back(ProfRec{name, prof_event(), prof_event()});
+  cudaEventRecord(g_prof_pending.back().a, s);
+  return (void *)(uintptr_t)g_prof_pending.size();
+}
+
+void prof_end(void *tok, cudaStream_t s) {
+  if (!tok) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  size_t i = (size_t)(uintptr_t)tok - 1;
+  if (i < g_prof_pending.size()) cudaEventRecord(g_prof_pending[i].b, s);
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return kNumSMs;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = kNumSMs;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+}  // namespace jb
+
+extern "C" {
+
+const char *jb_last_error(void) { return jb::g_err; }
+int jb_abi_version(void) { return JB_ABI_VERSION; }
+uint64_t jb_launch_count(void) { return jb::g_launches.load(); }
+
+void jb_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(jb::g_prof_mu);
+  jb::g_prof_on.store(on ? 1 : 0);
+}
+
+void jb_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(jb::g_prof_mu);
+  for (auto &r : jb::g_prof_pending) {
+    cudaEventSynchronize(r.b);
+    jb::g_prof_free.push_back(r.a);
+    jb::g_prof_free.push_back(r.b);
+  }
+  jb::g_prof_pending.clear();
+  jb::g_prof_acc.clear();
+}
+
+jb_status jb_prof_read(const char *name, double *ms, uint64_t *count) {
+  std::lock_guard<std::mutex> lk(jb::g_prof_mu);
+  for (auto &r : jb::g_prof_pending) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) {
+      jb::set_error("jb_prof_read: event sync failed");
+      return JB_ECUDA;
+    }
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    auto &acc = jb::g_prof_acc[r.name];
+    acc.first += t;
+    acc.second += 1;
+    jb::g_prof_free.push_back(r.a);
+    jb::g_prof_free.push_back(r.b);
+  }
+  jb::g_prof_pending.clear();
+  auto it = jb::g_prof_acc.find(name ? name : "");
+  *ms = it == jb::g_prof_acc.end() ? 0.0 : it->second.first;
+  *count = it == jb::g_prof_acc.end() ? 0 : it->second.second;
+  return JB_OK;
+}
+
+jb_status jb_release_workspace(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    jb::set_error("jb_release_workspace: no current device");
+    return JB_ECUDA;
+  }
+  std::lock_guard<std::mutex> lk(jb::g_arena_mu);
+  jb::Arena &a = jb::g_arena[dev];
+  if (a.ptr) {
+    cudaDeviceSynchronize();
+    cudaFree(a.ptr);
+  }
+  a.ptr = nullptr;
+  a.cap = 0;
+  return JB_OK;
+}
+
+}  // extern "C"

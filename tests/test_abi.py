@@ -1,0 +1,50 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/junob200.h declares, and the host layer validates arguments
+the way the reference does before any device work."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2503_10855_b200 import _lib
+
+
+def test_header_declares_entries():
+    syms = _lib.header_symbols()
+    for want in ("jb_matmul_f32", "jb_edge_f32", "jb_cava_u8", "jb_srad_f32", "jb_euler_f32",
+                 "jb_bfs", "jb_bp_train_f32", "jb_last_error", "jb_abi_version"):
+        assert want in syms
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in _lib.header_symbols() if not hasattr(lib, s)]
+    assert not missing, f"libjunob200.so lacks {missing}"
+
+
+def test_abi_version_and_signatures():
+    lib = _lib.load()
+    assert lib.jb_abi_version() == 1
+    for name in _lib.SIGNATURES:
+        assert name in _lib.header_symbols()
+
+
+def test_execute_validates_like_the_reference():
+    import paper_2503_10855_b200 as jb
+    a = np.zeros((4, 3), np.float32)
+    b = np.zeros((3, 5), np.float32)
+    with pytest.raises(jb.DynConstError):
+        jb.execute("matmul", [4, -3, 5], [a, b])
+    with pytest.raises(jb.DynConstError):
+        jb.execute("matmul", [4, 3], [a, b])
+    with pytest.raises(jb.RuntimeError_):
+        jb.execute("matmul", [4, 4, 5], [a, b])
+    with pytest.raises(jb.RuntimeError_):
+        jb.execute("no_such_entry", [], [])
+
+
+def test_oracle_execute_signature_parity():
+    import inspect
+    import paper_2503_10855_b200 as jb
+    params = list(inspect.signature(jb.oracle_execute).parameters)
+    assert params == ["module", "entry", "dyn_consts", "args", "max_steps"]

@@ -1,0 +1,79 @@
+"""Pin the C restatement (oracle/juno_oracle.c) to the reference interpreter.
+
+tests/golden/*.npz were produced by oracle/gen_golden.py, which runs Juno
+fixture programs through skiff's ``oracle_execute``
+(/root/reference/pkg/src/skiff/runtime/oracle.py:28-32).  Every comparison is
+bit-exact (np.array_equal on float32 / int32 arrays).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+
+
+def _eq(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape and a.dtype == b.dtype, (a.shape, b.shape, a.dtype, b.dtype)
+    assert np.array_equal(a.view(np.uint32) if a.dtype == np.float32 else a,
+                          b.view(np.uint32) if b.dtype == np.float32 else b), \
+        f"max |diff| = {np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)))}"
+
+
+@pytest.mark.parametrize("tag", ["8x8x8", "5x13x7", "16x16x16"])
+def test_matmul_pinned(oracle, tag):
+    g = golden("matmul")
+    _eq(oracle.matmul(g[f"{tag}_a"], g[f"{tag}_b"]), g[f"{tag}_res"])
+
+
+def test_matmul_identity_spec_example(oracle):
+    # matmul(I2, A) = A
+    g = golden("matmul")
+    _eq(g["eye_res"], g["eye_a"])
+    _eq(oracle.matmul(np.eye(2, dtype=np.float32), g["eye_a"]), g["eye_a"])
+
+
+@pytest.mark.parametrize("name", ["edge_12x16_g7", "edge_9x11_g3"])
+def test_edge_stages_pinned(oracle, name):
+    g = golden(name)
+    st = oracle.edge_frame(g["input"], g["gaussian"], g["structure"], g["sx"], g["sy"], g["theta"],
+                           stages=True)
+    _eq(st["smoothed"], g["smoothed"])
+    _eq(st["laplacian"], g["laplacian"])
+    _eq(st["zero_crossings"], g["zero_crossings"])
+    _eq(st["gradient"], g["gradient"])
+    assert np.float32(st["max_gradient"]).view(np.uint32) == np.float32(g["max_gradient"]).view(np.uint32)
+    _eq(st["out"], g["out"])
+
+
+@pytest.mark.parametrize("name", ["bfs_60", "bfs_200", "bfs_1000"])
+def test_bfs_pinned(oracle, name):
+    g = golden(name)
+    _eq(oracle.bfs(g["starting"], g["no_of_edges"], g["edges"], int(g["source"])), g["cost"])
+
+
+def test_srad_iteration_pinned(oracle):
+    g = golden("srad_iter_10x13")
+    _eq(oracle.srad_iter(g["J"], float(g["q0sqr"]), float(g["lam"])), g["out"])
+
+
+def test_bp_stages_pinned(oracle):
+    g = golden("bp_33x5")
+    w, _ = oracle.bp_adjust_weights(g["delta"], g["ly"], g["w"], g["oldw"])
+    # the fixture leaves column 0 (the bias unit j=0) at zero: compare j>=1
+    _eq(w[:, 1:], g["adjusted"][:, 1:])
+    _eq(oracle.bp_layer_sums(g["ly"], g["w"], acc64=False), g["layer_sum"])
+
+
+def test_cava_stages_pinned(oracle):
+    g = golden("cava_stages_6x8")
+    sc = oracle.cava_stage("scale", g["raw"])
+    _eq(sc, g["scaled"])
+    _eq(oracle.cava_stage("transform", sc, g["tstw"]), g["transformed"])
+
+
+def test_spec_known_answers(oracle):
+    # SPEC.md:276 (sum of 1..8 = 36) and :326 (1..1000 = 500500) as matmul
+    # reductions: ones(1,n) @ v
+    for n, want in ((8, 36.0), (1000, 500500.0)):
+        v = np.arange(1, n + 1, dtype=np.float32)[:, None]
+        assert oracle.matmul(np.ones((1, n), np.float32), v)[0, 0] == want
