@@ -31,6 +31,7 @@ _vp = ctypes.c_void_p
 # name -> argtypes (all pointers are passed as c_void_p device addresses)
 SIGNATURES = {
     "jb_matmul_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp],
+    "jb_matmul_exact_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp],
     "jb_edge_f32": [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _vp],
     "jb_edge_stages_f32": [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _f32, _vp,
                            _vp, _vp, _vp, _vp, _vp, _vp],

@@ -150,8 +150,12 @@ def _scalar(x, ty=float):
 
 
 # ---------------------------------------------------------------------- matmul
-def matmul(a, b):
-    """matmul<n,m,l>(a: f32[n,m], b: f32[m,l]) -> f32[n,l]  (PAPER.md:121-132)."""
+def matmul(a, b, exact: bool = False):
+    """matmul<n,m,l>(a: f32[n,m], b: f32[m,l]) -> f32[n,l]  (PAPER.md:121-132).
+
+    Default: 3xTF32 on tcgen05 tensor cores (fp32 tolerance, the k-reduce is
+    re-associated).  ``exact=True``: SIMT kernel in the oracle's k order,
+    bit-identical to the reference interpreter."""
     _need(len(_shape(a)) == 2 and len(_shape(b)) == 2, "matmul: a and b must be 2-D")
     n, m = _shape(a)
     m2, l = _shape(b)
@@ -159,7 +163,8 @@ def matmul(a, b):
     c = _Call([a, b])
     da, db = c.dev(a, np.float32, "a"), c.dev(b, np.float32, "b")
     out = c.empty((n, l), np.float32)
-    _check(_lib.load().jb_matmul_f32(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+    fn = _lib.load().jb_matmul_exact_f32 if exact else _lib.load().jb_matmul_f32
+    _check(fn(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
     return c.out(out)
 
 

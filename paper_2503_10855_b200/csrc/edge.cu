@@ -62,7 +62,7 @@ struct Smem {
   float inB[IR][IP];      // same, shifted left by one column
   float sm[SR][SR];       // smoothed tile (out-of-frame = clamped replica)
   uint32_t lapbits[LR][2];// laplacian > 0, bit = column within 32-col chunk
-  unsigned long long zcbits[TH];
+  uint32_t zcw[TH][2];    // zero crossing, bit = column within 32-col chunk
   float wmax[THREADS / 32];
   int fast;
 };
@@ -95,8 +95,263 @@ struct FusedArgs {
   int n, m, frames, tiles_x, tiles_y;
 };
 
+// fast-path data guard: v == +-0 or 2^-60 <= v <= 2^64 (raw-bit compare)
 __device__ __forceinline__ bool pix_ok(float v) {
-  return v == 0.0f || (v >= 0x1p-60f && v <= 0x1p64f);
+  const unsigned u = __float_as_uint(v);
+  return (u - 0x21800000u) <= (0x5f800000u - 0x21800000u) || (u + u) == 0u;
+}
+
+// stages 1-2 of one 60x60 tile whose clamped input is staged in S.inA/S.inB.
+// FAST: packed/FTZ gaussian, FMNMX morphology, FFMA sobel (guarded exact);
+// otherwise the oracle's operation order with single-rounding scalar ops.
+// BORDER: the tile's halo leaves the frame (pads / clamped replicas needed).
+template <bool FAST, bool BORDER>
+__device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
+                                          int lane, int warp) {
+  const int n = a.n, m = a.m;
+  // ---- stage 1: gaussian on the 64x64 smoothed region
+  {
+    const int r0 = warp * 8;  // 8 smoothed rows per warp, 2 columns per lane
+    if (FAST) {
+      unsigned long long acc[8];
+#pragma unroll
+      for (int o = 0; o < 8; o++) acc[o] = 0ull;  // (+0.0f, +0.0f)
+#pragma unroll
+      for (int iy = 0; iy < 14; iy++) {
+        const unsigned long long *ra = reinterpret_cast<const unsigned long long *>(&S.inA[r0 + iy][0]);
+        const unsigned long long *rb = reinterpret_cast<const unsigned long long *>(&S.inB[r0 + iy][0]);
+        unsigned long long v[7];
+#pragma unroll
+        for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + (j >> 1)] : ra[lane + (j >> 1)];
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+          const int i = iy - o;
+          if (i >= 0 && i < 7) {
+#pragma unroll
+            for (int j = 0; j < 7; j++) acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[i * 7 + j]));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 8; o++) *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
+    } else {
+      float2 acc[8];
+#pragma unroll
+      for (int o = 0; o < 8; o++) acc[o] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+      for (int iy = 0; iy < 14; iy++) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[j] = S.inA[r0 + iy][2 * lane + j];
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+          const int i = iy - o;
+          if (i >= 0 && i < 7) {
+#pragma unroll
+            for (int j = 0; j < 7; j++) {
+              const float g = c_gauss[i * 7 + j];
+              acc[o].x = add_rn(acc[o].x, mul_rn(v[j], g));
+              acc[o].y = add_rn(acc[o].y, mul_rn(v[j + 1], g));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 8; o++) *reinterpret_cast<float2 *>(&S.sm[r0 + o][2 * lane]) = acc[o];
+    }
+  }
+  __syncthreads();
+  // out-of-frame smoothed positions take the clamped in-frame value, which is
+  // what the gradient's clamp-to-edge indexing reads
+  if (BORDER) {
+    for (int idx = tid; idx < SR * SR; idx += THREADS) {
+      const int r = idx >> 6, c = idx & 63;
+      const int gy = y0 - 2 + r, gx = x0 - 2 + c;
+      const int cy = min(max(gy, 0), n - 1), cx = min(max(gx, 0), m - 1);
+      if (cy != gy || cx != gx) S.sm[r][c] = S.sm[cy - (y0 - 2)][cx - (x0 - 2)];
+    }
+    __syncthreads();
+  }
+
+  // ---- stage 2a: laplacian sign bits on the 62x62 region
+  {
+    const int cc = warp & 1, rb = warp >> 1;
+    const int lc = cc * 32 + lane;         // laplacian column (region)
+    const bool col_ok = lc < LR;
+    const int gxc = x0 - 1 + lc;           // frame column of the centre
+    const int scol = col_ok ? lc : LR - 1; // keep smem reads in bounds
+    if (FAST) {
+      // separable 3x3 max/min rolled down the column
+      float hx0 = 0.f, hx1 = 0.f, hn0 = 0.f, hn1 = 0.f, cprev = 0.f;
+      bool i0 = true, i1 = true, i2 = true;
+      if (BORDER) {
+        i0 = gxc - 1 >= 0 && gxc - 1 < m;
+        i1 = gxc >= 0 && gxc < m;
+        i2 = gxc + 1 >= 0 && gxc + 1 < m;
+      }
+#pragma unroll
+      for (int k = 0; k < 18; k++) {
+        const int sr = min(rb * 16 + k, SR - 1);
+        const float a0 = S.sm[sr][scol], a1 = S.sm[sr][scol + 1], a2 = S.sm[sr][scol + 2];
+        float hx2, hn2;
+        if (BORDER) {
+          const int gy = y0 - 2 + rb * 16 + k;
+          const bool rin = gy >= 0 && gy < n;
+          hx2 = fmaxf(fmaxf(rin && i0 ? a0 : -INFINITY, rin && i1 ? a1 : -INFINITY), rin && i2 ? a2 : -INFINITY);
+          hn2 = fminf(fminf(rin && i0 ? a0 : INFINITY, rin && i1 ? a1 : INFINITY), rin && i2 ? a2 : INFINITY);
+        } else {
+          hx2 = fmaxf(fmaxf(a0, a1), a2);
+          hn2 = fminf(fminf(a0, a1), a2);
+        }
+        if (k >= 2) {
+          const int lr = rb * 16 + k - 2;
+          const float d = fmaxf(0.0f, fmaxf(fmaxf(hx0, hx1), hx2));
+          const float e = fminf(1.0f, fminf(fminf(hn0, hn1), hn2));
+          const float lap = fmaf(-2.0f, cprev, add_rn(d, e));  // 2*x is exact
+          const unsigned bits = __ballot_sync(0xffffffffu, col_ok && lap > 0.0f);
+          if (lane == 0 && lr < LR) S.lapbits[lr][cc] = bits;
+        }
+        hx0 = hx1; hx1 = hx2; hn0 = hn1; hn1 = hn2; cprev = a1;
+      }
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < 16; k++) {
+        const int lr = rb * 16 + k;
+        bool pos = false;
+        if (col_ok && lr < LR) {
+          const int gyc = y0 - 1 + lr;
+          float d = 0.0f, e = 1.0f;
+#pragma unroll
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+              const int gy = gyc + i - 1, gx = gxc + j - 1;
+              const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
+              d = py_max(d, mul_rn(in ? S.sm[lr + i][lc + j] : 0.0f, c_struct[i * 3 + j]));
+            }
+#pragma unroll
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+              const int gy = gyc + i - 1, gx = gxc + j - 1;
+              const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
+              e = py_min(e, mul_rn(in ? S.sm[lr + i][lc + j] : 1.0f, c_struct[i * 3 + j]));
+            }
+          pos = sub_rn(add_rn(d, e), mul_rn(2.0f, S.sm[lr + 1][lc + 1])) > 0.0f;
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, pos);
+        if (lane == 0 && lr < LR) S.lapbits[lr][cc] = bits;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- stage 2b: zero crossings (bit masks), one thread per output row
+  if (tid < TH) {
+    const int orow = tid;
+    unsigned long long zc = 0;
+    if (FAST) {
+      // frame-column validity of laplacian columns lc = 0..61 (x0-1+lc)
+      unsigned long long colmask = ~0ull;
+      if (BORDER) {
+        const int lo = max(0, 1 - x0), hi = min(LR - 1, m - x0);
+        colmask = hi >= lo ? (((hi - lo + 1) >= 64 ? ~0ull : ((1ull << (hi - lo + 1)) - 1)) << lo) : 0ull;
+      }
+      unsigned long long orr = 0, andd = ~0ull;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        const int lr = orow + i;
+        const int gy = y0 - 1 + lr;
+        if (!BORDER || (gy >= 0 && gy < n)) {
+          const unsigned long long b =
+              (unsigned long long)S.lapbits[lr][0] | ((unsigned long long)S.lapbits[lr][1] << 32);
+          orr |= b & colmask;
+          andd &= b | ~colmask;
+        }
+      }
+      zc = (orr | (orr >> 1) | (orr >> 2)) & ~(andd & (andd >> 1) & (andd >> 2));
+    } else {
+      const int gyc = y0 + orow;
+      for (int oc = 0; oc < TW; oc++) {
+        const int gxc = x0 + oc;
+        float d = 0.0f, e = 1.0f;
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) {
+            const int lr = orow + i, lc = oc + j;
+            const int gy = gyc + i - 1, gx = gxc + j - 1;
+            const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
+            const float sg = ((S.lapbits[lr][lc >> 5] >> (lc & 31)) & 1u) ? 1.0f : 0.0f;
+            d = py_max(d, mul_rn(in ? sg : 0.0f, c_struct[i * 3 + j]));
+          }
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) {
+            const int lr = orow + i, lc = oc + j;
+            const int gy = gyc + i - 1, gx = gxc + j - 1;
+            const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
+            const float sg = ((S.lapbits[lr][lc >> 5] >> (lc & 31)) & 1u) ? 1.0f : 0.0f;
+            e = py_min(e, mul_rn(in ? sg : 1.0f, c_struct[i * 3 + j]));
+          }
+        if (sub_rn(d, e) > 0.0f) zc |= 1ull << oc;
+      }
+    }
+    S.zcw[orow][0] = (unsigned)zc;
+    S.zcw[orow][1] = (unsigned)(zc >> 32);
+  }
+  __syncthreads();
+
+  // ---- stage 2c: sobel gradient, pack with zc, block max
+  float bmax = 0.0f;
+  {
+    const int cc = warp & 1, rb = warp >> 1;
+    const int oc = cc * 32 + lane;
+    const bool col_ok = oc < TW && (!BORDER || x0 + oc < m);
+    const int scol = min(oc, TW - 1);
+    const int orow0 = rb * 15;
+    uint32_t *prow = a.packed + ((size_t)f * n + y0 + orow0) * m + x0 + scol;
+    float sx[9], sy[9];
+#pragma unroll
+    for (int q = 0; q < 9; q++) { sx[q] = c_sx[q]; sy[q] = c_sy[q]; }
+    float gxs[3] = {0.f, 0.f, 0.f}, gys[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 17; r++) {
+      const int sr = orow0 + 1 + r;  // smoothed row
+      const float v0 = S.sm[sr][scol + 1], v1 = S.sm[sr][scol + 2], v2 = S.sm[sr][scol + 3];
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        const int k = r - q;  // output row k (0..14) gets tap row q
+        if (k >= 0 && k < 15) {
+          float gx = q == 0 ? 0.0f : gxs[k % 3], gy = q == 0 ? 0.0f : gys[k % 3];
+          if (FAST) {
+            gx = fmaf(v0, sx[q * 3 + 0], gx); gy = fmaf(v0, sy[q * 3 + 0], gy);
+            gx = fmaf(v1, sx[q * 3 + 1], gx); gy = fmaf(v1, sy[q * 3 + 1], gy);
+            gx = fmaf(v2, sx[q * 3 + 2], gx); gy = fmaf(v2, sy[q * 3 + 2], gy);
+          } else {
+            gx = add_rn(gx, mul_rn(v0, sx[q * 3 + 0])); gy = add_rn(gy, mul_rn(v0, sy[q * 3 + 0]));
+            gx = add_rn(gx, mul_rn(v1, sx[q * 3 + 1])); gy = add_rn(gy, mul_rn(v1, sy[q * 3 + 1]));
+            gx = add_rn(gx, mul_rn(v2, sx[q * 3 + 2])); gy = add_rn(gy, mul_rn(v2, sy[q * 3 + 2]));
+          }
+          gxs[k % 3] = gx; gys[k % 3] = gy;
+          if (q == 2) {
+            const float g = __fsqrt_rn(add_rn(mul_rn(gx, gx), mul_rn(gy, gy)));
+            const unsigned z = (S.zcw[orow0 + k][cc] >> lane) & 1u;
+            if (col_ok && (!BORDER || y0 + orow0 + k < n)) {
+              prow[(size_t)k * m] = __float_as_uint(g) | (z << 31);
+              bmax = fmaxf(bmax, g);  // ignores NaN like the Python fold
+            }
+          }
+        }
+      }
+    }
+  }
+  bmax = warp_max(bmax);
+  if (lane == 0) S.wmax[warp] = bmax;
+  __syncthreads();
+  if (tid == 0) {
+    float v = S.wmax[0];
+#pragma unroll
+    for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
+    if (!(v != v)) atomicMax(a.fmax + f, __float_as_uint(v));
+  }
 }
 
 __global__ void __launch_bounds__(THREADS, 3)
@@ -116,269 +371,49 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     const int y0 = ty * TH, x0 = tx * TW;
     const float *img = a.in + (size_t)f * n * m;
 
-    // ---- stage 0: clamped input tile -> smem (both alignments) + guard
-    bool bad = false;
-    for (int idx = tid; idx < IR * IR; idx += THREADS) {
-      const int r = idx / IR, c = idx - r * IR;
-      const int gy = min(max(y0 - 5 + r, 0), n - 1);
-      const int gx = min(max(x0 - 5 + c, 0), m - 1);
-      const float v = __ldg(img + (size_t)gy * m + gx);
-      bad |= !pix_ok(v);
-      S.inA[r][c] = v;
-      if (c > 0) S.inB[r][c - 1] = v;
+    // ---- stage 0: clamped input tile -> smem (both alignments) + guard.
+    // Warp w loads rows w, w+8, ...; lanes stride the 70 columns.
+    // all loads are issued before any use so ~27 LDGs per lane are in flight
+    constexpr int RPW = (IR + THREADS / 32 - 1) / (THREADS / 32);  // rows per warp (9)
+    float vals[RPW][3];
+    const int cx0 = min(max(x0 - 5 + lane, 0), m - 1);
+    const int cx1 = min(max(x0 + 27 + lane, 0), m - 1);
+    const int cx2 = min(max(x0 + 59 + lane, 0), m - 1);
+#pragma unroll
+    for (int i = 0; i < RPW; i++) {
+      const int r = warp + i * (THREADS / 32);
+      const float *row = img + (size_t)min(max(y0 - 5 + min(r, IR - 1), 0), n - 1) * m;
+      vals[i][0] = __ldg(row + cx0);
+      vals[i][1] = __ldg(row + cx1);
+      vals[i][2] = lane < IR - 64 ? __ldg(row + cx2) : 0.0f;
     }
-    const int any_bad = __syncthreads_or(bad);
-    const bool fast = filters_fast && !any_bad;
-    const bool border = (y0 < 2) || (x0 < 2) || (y0 + SR - 2 > n) || (x0 + SR - 2 > m);
-
-    // ---- stage 1: gaussian on the 64x64 smoothed region
-    {
-      const int r0 = warp * 8;  // 8 smoothed rows per warp, 2 columns per lane
-      if (fast) {
-        unsigned long long acc[8];
+    bool ok = true;
 #pragma unroll
-        for (int o = 0; o < 8; o++) acc[o] = 0ull;  // +0.0f, +0.0f
-#pragma unroll
-        for (int iy = 0; iy < 14; iy++) {
-          const unsigned long long *ra =
-              reinterpret_cast<const unsigned long long *>(&S.inA[r0 + iy][0]);
-          const unsigned long long *rb =
-              reinterpret_cast<const unsigned long long *>(&S.inB[r0 + iy][0]);
-          unsigned long long v[7];
-#pragma unroll
-          for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + (j >> 1)] : ra[lane + (j >> 1)];
-#pragma unroll
-          for (int o = 0; o < 8; o++) {
-            const int i = iy - o;
-            if (i >= 0 && i < 7) {
-#pragma unroll
-              for (int j = 0; j < 7; j++) acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[i * 7 + j]));
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 0; o < 8; o++)
-          *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
-      } else {
-        float2 acc[8];
-#pragma unroll
-        for (int o = 0; o < 8; o++) acc[o] = make_float2(0.0f, 0.0f);
-#pragma unroll 2
-        for (int iy = 0; iy < 14; iy++) {
-          float v[8];
-#pragma unroll
-          for (int j = 0; j < 8; j++) v[j] = S.inA[r0 + iy][2 * lane + j];
-#pragma unroll
-          for (int o = 0; o < 8; o++) {
-            const int i = iy - o;
-            if (i >= 0 && i < 7) {
-#pragma unroll
-              for (int j = 0; j < 7; j++) {
-                const float g = c_gauss[i * 7 + j];
-                acc[o].x = add_rn(acc[o].x, mul_rn(v[j], g));
-                acc[o].y = add_rn(acc[o].y, mul_rn(v[j + 1], g));
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 0; o < 8; o++) *reinterpret_cast<float2 *>(&S.sm[r0 + o][2 * lane]) = acc[o];
-      }
-    }
-    __syncthreads();
-    // out-of-frame smoothed positions take the clamped in-frame value, which is
-    // what the gradient's clamp-to-edge indexing reads
-    if (border) {
-      for (int idx = tid; idx < SR * SR; idx += THREADS) {
-        const int r = idx >> 6, c = idx & 63;
-        const int gy = y0 - 2 + r, gx = x0 - 2 + c;
-        const int cy = min(max(gy, 0), n - 1), cx = min(max(gx, 0), m - 1);
-        if (cy != gy || cx != gx) S.sm[r][c] = S.sm[cy - (y0 - 2)][cx - (x0 - 2)];
-      }
-      __syncthreads();
-    }
-
-    // ---- stage 2a: laplacian sign bits on the 62x62 region
-    {
-      const int cc = warp & 1, rb = warp >> 1;
-      const int lc = cc * 32 + lane;             // laplacian column (region)
-      const bool col_ok = lc < LR;
-      const int gxc = x0 - 1 + lc;               // frame column of the centre
-      const int scol = col_ok ? lc : LR - 1;     // keep smem reads in bounds
-      if (fast) {
-        // separable 3x3 max/min, rolled down the column: hx/hn hold the
-        // horizontal max/min of the last three smoothed rows
-        float hx0 = 0.f, hx1 = 0.f, hn0 = 0.f, hn1 = 0.f, cprev = 0.f;
-#pragma unroll
-        for (int k = 0; k < 18; k++) {
-          const int sr = rb * 16 + k;            // smoothed row of window row
-          const int srr = min(sr, SR - 1);
-          const float a0 = S.sm[srr][scol], a1 = S.sm[srr][scol + 1], a2 = S.sm[srr][scol + 2];
-          float l0 = a0, l1 = a1, l2 = a2, h0 = a0, h1 = a1, h2 = a2;
-          if (border) {
-            const int gy = y0 - 2 + sr;
-            const bool rin = gy >= 0 && gy < n;
-            const bool i0 = rin && gxc - 1 >= 0 && gxc - 1 < m;
-            const bool i1 = rin && gxc >= 0 && gxc < m;
-            const bool i2 = rin && gxc + 1 >= 0 && gxc + 1 < m;
-            l0 = i0 ? a0 : -INFINITY; l1 = i1 ? a1 : -INFINITY; l2 = i2 ? a2 : -INFINITY;
-            h0 = i0 ? a0 : INFINITY;  h1 = i1 ? a1 : INFINITY;  h2 = i2 ? a2 : INFINITY;
-          }
-          const float hx2 = fmaxf(fmaxf(l0, l1), l2);
-          const float hn2 = fminf(fminf(h0, h1), h2);
-          if (k >= 2) {
-            const int lr = rb * 16 + k - 2;
-            const float d = fmaxf(0.0f, fmaxf(fmaxf(hx0, hx1), hx2));
-            const float e = fminf(1.0f, fminf(fminf(hn0, hn1), hn2));
-            const float lap = fmaf(-2.0f, cprev, add_rn(d, e));  // 2*x is exact
-            const unsigned bits = __ballot_sync(0xffffffffu, col_ok && lr < LR && lap > 0.0f);
-            if (lane == 0 && lr < LR) S.lapbits[lr][cc] = bits;
-          }
-          hx0 = hx1; hx1 = hx2; hn0 = hn1; hn1 = hn2; cprev = a1;
-        }
-      } else {
-        for (int k = 0; k < 16; k++) {
-          const int lr = rb * 16 + k;
-          bool pos = false;
-          if (col_ok && lr < LR) {
-            const int gyc = y0 - 1 + lr;
-            float d = 0.0f, e = 1.0f;
-#pragma unroll
-            for (int i = 0; i < 3; i++)
-#pragma unroll
-              for (int j = 0; j < 3; j++) {
-                const int gy = gyc + i - 1, gx = gxc + j - 1;
-                const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
-                const float v = in ? S.sm[lr + i][lc + j] : 0.0f;
-                d = py_max(d, mul_rn(v, c_struct[i * 3 + j]));
-              }
-#pragma unroll
-            for (int i = 0; i < 3; i++)
-#pragma unroll
-              for (int j = 0; j < 3; j++) {
-                const int gy = gyc + i - 1, gx = gxc + j - 1;
-                const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
-                const float v = in ? S.sm[lr + i][lc + j] : 1.0f;
-                e = py_min(e, mul_rn(v, c_struct[i * 3 + j]));
-              }
-            const float lap = sub_rn(add_rn(d, e), mul_rn(2.0f, S.sm[lr + 1][lc + 1]));
-            pos = lap > 0.0f;
-          }
-          const unsigned bits = __ballot_sync(0xffffffffu, pos);
-          if (lane == 0 && lr < LR) S.lapbits[lr][cc] = bits;
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage 2b: zero crossings (bit masks), one thread per output row
-    if (tid < TH) {
-      const int orow = tid;
-      // frame-column validity of laplacian columns lc = 0..61 (x0-1+lc)
-      unsigned long long colmask = 0;
-      {
-        const int lo = max(0, 1 - x0);                  // first lc inside
-        const int hi = min(LR - 1, m - x0);             // last lc inside
-        if (hi >= lo) colmask = ((hi - lo + 1) >= 64 ? ~0ull : ((1ull << (hi - lo + 1)) - 1)) << lo;
-      }
-      unsigned long long zc = 0;
-      if (fast) {
-        unsigned long long orr = 0, andd = ~0ull;
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-          const int lr = orow + i;
-          const int gy = y0 - 1 + lr;
-          if (gy >= 0 && gy < n) {
-            const unsigned long long b =
-                (unsigned long long)S.lapbits[lr][0] | ((unsigned long long)S.lapbits[lr][1] << 32);
-            orr |= b & colmask;
-            andd &= b | ~colmask;
-          }
-        }
-        const unsigned long long ho = orr | (orr >> 1) | (orr >> 2);
-        const unsigned long long ha = andd & (andd >> 1) & (andd >> 2);
-        zc = ho & ~ha;
-      } else {
-        const int gyc = y0 + orow;
-        for (int oc = 0; oc < TW; oc++) {
-          const int gxc = x0 + oc;
-          float d = 0.0f, e = 1.0f;
-          for (int i = 0; i < 3; i++)
-            for (int j = 0; j < 3; j++) {
-              const int lr = orow + i, lc = oc + j;
-              const int gy = gyc + i - 1, gx = gxc + j - 1;
-              const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
-              const float s = ((S.lapbits[lr][lc >> 5] >> (lc & 31)) & 1u) ? 1.0f : 0.0f;
-              d = py_max(d, mul_rn(in ? s : 0.0f, c_struct[i * 3 + j]));
-            }
-          for (int i = 0; i < 3; i++)
-            for (int j = 0; j < 3; j++) {
-              const int lr = orow + i, lc = oc + j;
-              const int gy = gyc + i - 1, gx = gxc + j - 1;
-              const bool in = gy >= 0 && gy < n && gx >= 0 && gx < m;
-              const float s = ((S.lapbits[lr][lc >> 5] >> (lc & 31)) & 1u) ? 1.0f : 0.0f;
-              e = py_min(e, mul_rn(in ? s : 1.0f, c_struct[i * 3 + j]));
-            }
-          if (sub_rn(d, e) > 0.0f) zc |= 1ull << oc;
-        }
-      }
-      S.zcbits[orow] = zc;
-    }
-    __syncthreads();
-
-    // ---- stage 2c: sobel gradient, pack with zc, block max
-    float bmax = 0.0f;
-    {
-      const int cc = warp & 1, rb = warp >> 1;
-      const int oc = cc * 32 + lane;
-      const bool col_ok = oc < TW && x0 + oc < m;
-      const int scol = min(oc, TW - 1);
-      float gxs[3] = {0.f, 0.f, 0.f}, gys[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-      for (int r = 0; r < 17; r++) {
-        const int sr = rb * 15 + 1 + r;  // smoothed row
-        const float v0 = S.sm[sr][scol + 1], v1 = S.sm[sr][scol + 2], v2 = S.sm[sr][scol + 3];
+    for (int i = 0; i < RPW; i++) {
+      const int r = warp + i * (THREADS / 32);
+      if (r < IR) {
 #pragma unroll
         for (int q = 0; q < 3; q++) {
-          const int k = r - q;           // output row k (0..14) with tap row i = q
-          if (k >= 0 && k < 15) {
-            float gx = gxs[k % 3], gy = gys[k % 3];
-            if (q == 0) { gx = 0.0f; gy = 0.0f; }
-            if (fast) {
-              gx = fmaf(v0, c_sx[q * 3 + 0], gx); gy = fmaf(v0, c_sy[q * 3 + 0], gy);
-              gx = fmaf(v1, c_sx[q * 3 + 1], gx); gy = fmaf(v1, c_sy[q * 3 + 1], gy);
-              gx = fmaf(v2, c_sx[q * 3 + 2], gx); gy = fmaf(v2, c_sy[q * 3 + 2], gy);
-            } else {
-              gx = add_rn(gx, mul_rn(v0, c_sx[q * 3 + 0])); gy = add_rn(gy, mul_rn(v0, c_sy[q * 3 + 0]));
-              gx = add_rn(gx, mul_rn(v1, c_sx[q * 3 + 1])); gy = add_rn(gy, mul_rn(v1, c_sy[q * 3 + 1]));
-              gx = add_rn(gx, mul_rn(v2, c_sx[q * 3 + 2])); gy = add_rn(gy, mul_rn(v2, c_sy[q * 3 + 2]));
-            }
-            gxs[k % 3] = gx; gys[k % 3] = gy;
-            if (q == 2) {
-              const float g = __fsqrt_rn(add_rn(mul_rn(gx, gx), mul_rn(gy, gy)));
-              const int orow = rb * 15 + k;
-              const int gyr = y0 + orow;
-              if (col_ok && gyr < n) {
-                const unsigned z = (unsigned)((S.zcbits[orow] >> oc) & 1ull);
-                a.packed[((size_t)f * n + gyr) * m + x0 + oc] = __float_as_uint(g) | (z << 31);
-                bmax = fmaxf(bmax, g);  // ignores NaN like the Python fold
-              }
-            }
+          const int c = q * 32 + lane;
+          if (c < IR) {
+            const float v = vals[i][q];
+            ok &= pix_ok(v);
+            S.inA[r][c] = v;
+            if (c > 0) S.inB[r][c - 1] = v;
           }
         }
       }
     }
-    bmax = warp_max(bmax);
-    if (lane == 0) S.wmax[warp] = bmax;
-    __syncthreads();
-    if (tid == 0) {
-      float v = S.wmax[0];
-#pragma unroll
-      for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
-      if (!(v != v)) atomicMax(a.fmax + f, __float_as_uint(v));
+    const int all_ok = __syncthreads_and(ok);
+    const bool border = (y0 < 5) || (x0 < 5) || (y0 + IR - 5 > n) || (x0 + IR - 5 > m);
+    if (filters_fast && all_ok) {
+      if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp);
+      else edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp);
+    } else {
+      edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp);
     }
-    // next tile's stage 0 overwrites inA/inB only; sm/lapbits/zcbits are
-    // protected by the __syncthreads_or below and the ones above
+    // the next tile's stage 0 only writes inA/inB, which no thread reads
+    // after edge_tile's first __syncthreads
   }
 }
 

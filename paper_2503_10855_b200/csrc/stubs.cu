@@ -10,9 +10,6 @@
 
 extern "C" {
 
-jb_status jb_matmul_f32(uint64_t, uint64_t, uint64_t, const float *, const float *, float *, void *) {
-  JB_STUB("jb_matmul_f32");
-}
 jb_status jb_cava_u8(uint64_t, uint64_t, uint64_t, uint64_t, const uint8_t *, const float *,
                      const float *, const float *, const float *, const float *, uint8_t *, void *) {
   JB_STUB("jb_cava_u8");

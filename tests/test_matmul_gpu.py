@@ -1,0 +1,59 @@
+"""matmul on the B200: 3xTF32 tcgen05 path within the fp32 bound, exact SIMT
+path bit-identical to the reference interpreter (golden) and the oracle."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2503_10855_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -24
+
+
+def _bound(a, b):
+    m = a.shape[1]
+    gamma = m * U / (1 - m * U)
+    return (2 * gamma + 8 * U) * (np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64))
+
+
+def _within(c, ref, a, b):
+    err = np.abs(c.astype(np.float64) - ref.astype(np.float64))
+    bound = _bound(a, b)
+    worst = float(np.max(err / np.maximum(bound, 1e-300)))
+    assert np.all(err <= bound), f"error exceeds (2*gamma_m+8u)|A||B| by x{worst:.3f}"
+    return worst
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (128, 64, 32), (256, 512, 128), (1000, 1000, 1000),
+                                   (130, 36, 68), (1, 4, 4)])
+def test_matmul_tcgen05_within_fp32_bound(jb, oracle, shape):
+    n, m, l = shape
+    a, b = W.matmul_inputs(n, m, l, seed=n + m + l)
+    c = jb.matmul(a, b)
+    ref = oracle.matmul(a, b)
+    _within(c, ref, a, b)
+    # and much tighter than the bound in practice (3xTF32 ~ fp32)
+    rel = np.max(np.abs(c - ref)) / np.max(np.abs(ref))
+    assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("tag", ["8x8x8", "5x13x7", "16x16x16"])
+def test_matmul_exact_matches_reference_interpreter(jb, tag):
+    g = golden("matmul")
+    c = jb.matmul(g[f"{tag}_a"], g[f"{tag}_b"], exact=True)
+    assert np.array_equal(c.view(np.uint32), g[f"{tag}_res"].view(np.uint32))
+
+
+def test_matmul_exact_vs_oracle_bitwise(jb, oracle):
+    a, b = W.matmul_inputs(300, 257, 129, seed=3)
+    c = jb.matmul(a, b, exact=True)
+    assert np.array_equal(c.view(np.uint32), oracle.matmul(a, b).view(np.uint32))
+
+
+def test_matmul_identity_and_zero_k(jb):
+    a = np.random.default_rng(1).standard_normal((64, 64)).astype(np.float32)
+    eye = np.eye(64, dtype=np.float32)
+    assert np.array_equal(jb.matmul(eye, a), a)  # hi*hi exact, lo terms exact
+    z = jb.execute("matmul", [3, 0, 5], [np.zeros((3, 0), np.float32), np.zeros((0, 5), np.float32)])
+    assert z.shape == (3, 5) and not z.any()
