@@ -7,9 +7,11 @@
 //     |C - C_ref| <= (2*gamma_m + 8u) * (|A| |B|)   elementwise, u = 2^-24.
 //
 // B200 design: 3xTF32 on the 5th-gen tensor cores.
-//   split kernel   : A -> (A_hi, A_lo), B -> (B_hi, B_lo) with x_hi =
-//                    rna_tf32(x), x_lo = rna_tf32(x - x_hi) (elementwise, so
-//                    A stays K-major and B stays MN-major: no transpose).
+//   split kernels  : A -> (A_hi, A_lo), B -> (Bt_hi, Bt_lo) with x_hi =
+//                    rna_tf32(x), x_lo = rna_tf32(x - x_hi); B is transposed
+//                    on the way (tiled through shared memory) so both MMA
+//                    operands are K-major (an MN-major tf32 B descriptor
+//                    produced no result on this part, tools/mma_probe.cu).
 //   gemm kernel    : one 128x64 output tile per CTA; warp 0 = TMA producer
 //                    (4 operand tiles per 32-wide k-block, 128B swizzle,
 //                    4-stage mbarrier ring), warp 1 = TMEM allocator + single
@@ -31,7 +33,7 @@ namespace mm {
 constexpr int BM = 128, BN = 64, BK = 32;  // BK fp32 = one 128-byte swizzle row
 constexpr int STAGES = 4;
 constexpr int A_TILE = BM * BK * 4;        // 16 KiB
-constexpr int B_TILE = BK * BN * 4;        // 8 KiB (two 32-column MN atoms)
+constexpr int B_TILE = BK * BN * 4;        // 8 KiB (64 K-major rows of 128 B)
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 64;
@@ -66,6 +68,28 @@ __global__ void split_tf32_kernel(const float4 *__restrict__ x, float4 *__restri
     h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
     hi[i] = h;
     lo[i] = l;
+  }
+}
+
+// B [K][N] -> Bt_hi, Bt_lo [N][K] (32x32 tiles through shared memory)
+__global__ void split_tf32_transpose_kernel(const float *__restrict__ b, float *__restrict__ bt_hi,
+                                            float *__restrict__ bt_lo, int K, int N) {
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const int k = k0 + r, nn = n0 + tx;
+    t[r][tx] = (k < K && nn < N) ? __ldg(b + (size_t)k * N + nn) : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int nn = n0 + r, k = k0 + tx;
+    if (nn < N && k < K) {
+      const float v = t[tx][r];
+      const float h = tf32_rna(v);
+      bt_hi[(size_t)nn * K + k] = h;
+      bt_lo[(size_t)nn * K + k] = tf32_rna(v - h);
+    }
   }
 }
 
@@ -105,16 +129,13 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
         const int k0 = kb * BK;
         tc::tma_load_2d(S.a_hi[s], &tm_ahi, &S.full[s], k0, m0);
         tc::tma_load_2d(S.a_lo[s], &tm_alo, &S.full[s], k0, m0);
-        // B is MN-major: two 32-column atoms of BK rows each
-        tc::tma_load_2d(S.b_hi[s], &tm_bhi, &S.full[s], n0, k0);
-        tc::tma_load_2d(S.b_hi[s] + B_TILE / 2, &tm_bhi, &S.full[s], n0 + 32, k0);
-        tc::tma_load_2d(S.b_lo[s], &tm_blo, &S.full[s], n0, k0);
-        tc::tma_load_2d(S.b_lo[s] + B_TILE / 2, &tm_blo, &S.full[s], n0 + 32, k0);
+        tc::tma_load_2d(S.b_hi[s], &tm_bhi, &S.full[s], k0, n0);
+        tc::tma_load_2d(S.b_lo[s], &tm_blo, &S.full[s], k0, n0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 1);
+    constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 0);
     for (int kb = 0; kb < kblocks; kb++) {
       const int s = kb % STAGES;
       tc::mbar_wait(&S.full[s], (kb / STAGES) & 1);
@@ -124,14 +145,12 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
         const uint32_t bhi = tc::smem_u32(S.b_hi[s]), blo = tc::smem_u32(S.b_lo[s]);
 #pragma unroll
         for (int k = 0; k < BK / 8; k++) {
-          // A: K-major, 128B rows, 8-row atoms of 1 KiB -> SBO = 1024;
-          //    one MMA consumes 8 fp32 of K = 32 bytes of each row.
-          // B: MN-major, atoms of 8 K-rows x 128B (1 KiB) -> SBO = 1024,
-          //    the second 32-column atom is B_TILE/2 further -> LBO.
+          // A and Bt: K-major, 128B rows, 8-row atoms of 1 KiB -> SBO = 1024;
+          // one MMA consumes 8 fp32 of K = 32 bytes of each row.
           const uint64_t da_hi = tc::smem_desc_sw128(ahi + k * 32, 16, 1024);
           const uint64_t da_lo = tc::smem_desc_sw128(alo + k * 32, 16, 1024);
-          const uint64_t db_hi = tc::smem_desc_sw128(bhi + k * 1024, B_TILE / 2, 1024);
-          const uint64_t db_lo = tc::smem_desc_sw128(blo + k * 1024, B_TILE / 2, 1024);
+          const uint64_t db_hi = tc::smem_desc_sw128(bhi + k * 32, 16, 1024);
+          const uint64_t db_lo = tc::smem_desc_sw128(blo + k * 32, 16, 1024);
           const uint32_t acc0 = (kb | k) != 0;
           tc::mma_tf32(tmem_d, da_hi, db_hi, idesc, acc0);
           tc::mma_tf32(tmem_d, da_hi, db_lo, idesc, 1);
@@ -243,12 +262,13 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
                                    float *res, void *stream) {
   JB_REQUIRE(n < (1ull << 31) && m < (1ull << 31) && l < (1ull << 31), "matmul: extents too large");
   if (n == 0 || l == 0) return JB_OK;
-  JB_REQUIRE(a && b && res, "matmul: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  if (m == 0) {
+  JB_REQUIRE(res, "matmul: null result pointer");
+  if (m == 0) {  // empty k-reduce: every element is the zero initialiser
     JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
     return JB_OK;
   }
+  JB_REQUIRE(a && b, "matmul: null pointer");
   const bool tma_ok = (m % 4 == 0) && (l % 4 == 0) && ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
                       n >= 1 && mm::encode_fn() != nullptr;
   if (!tma_ok) {
@@ -264,13 +284,13 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   split_tf32_kernel<<<sm_count() * 4, 256, 0, s>>>((const float4 *)a, (float4 *)a_hi, (float4 *)a_lo,
                                                    (long long)(asz / 4));
   JB_LAUNCHED("matmul_split_a");
-  split_tf32_kernel<<<sm_count() * 4, 256, 0, s>>>((const float4 *)b, (float4 *)b_hi, (float4 *)b_lo,
-                                                   (long long)(bsz / 4));
+  split_tf32_transpose_kernel<<<dim3((unsigned)((l + 31) / 32), (unsigned)((m + 31) / 32)), 256, 0, s>>>(
+      b, b_hi, b_lo, (int)m, (int)l);
   JB_LAUNCHED("matmul_split_b");
 
   CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
   if (!make_map(&m_ahi, a_hi, n, m, BM) || !make_map(&m_alo, a_lo, n, m, BM) ||
-      !make_map(&m_bhi, b_hi, m, l, BK) || !make_map(&m_blo, b_lo, m, l, BK)) {
+      !make_map(&m_bhi, b_hi, l, m, BN) || !make_map(&m_blo, b_lo, l, m, BN)) {
     set_error("matmul: cuTensorMapEncodeTiled failed");
     return JB_ECUDA;
   }

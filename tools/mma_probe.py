@@ -1,0 +1,14 @@
+import ctypes, numpy as np, os, subprocess, sys
+here = os.path.dirname(os.path.abspath(__file__))
+so = os.path.join(here, "mma_probe.so")
+lib = ctypes.CDLL(so)
+rng = np.random.default_rng(0)
+A = rng.integers(-3, 4, (128, 32)).astype(np.float32)
+B = rng.integers(-3, 4, (32, 64)).astype(np.float32)
+P = ctypes.POINTER(ctypes.c_float)
+for mode in [0, 1, 2, 3, 4, 6]:
+    C = np.zeros((128, 64), np.float32); dbg = np.zeros(6, np.float32)
+    rc = lib.run_probe(A.ctypes.data_as(P), B.ctypes.data_as(P), C.ctypes.data_as(P), dbg.ctypes.data_as(P), mode)
+    K = 32 if mode & 2 else 8
+    R = A[:, :K] @ B[:K]
+    print(f"mode {mode} (B {'K' if mode&1 else 'MN'}-major, K={K}) rc={rc} exact={np.array_equal(C, R)} maxerr={np.abs(C-R).max()} C00={C[0,:4]} R00={R[0,:4]} dbg={[hex(x) for x in dbg.view(np.uint32)]}")
