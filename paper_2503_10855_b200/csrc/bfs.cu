@@ -1,0 +1,148 @@
+// bfs.cu -- bfs<n,m>(starting u32[n], no_of_edges u32[n], edges u32[m], source)
+//           -> cost i32[n]    (Rodinia BFS; oracle/juno_oracle.c:jo_bfs)
+//
+// Levels of a breadth-first search are order independent, so the result is
+// bit-identical to the oracle for any traversal order.
+//
+// B200 design: one persistent cooperative kernel runs every
+// level (no host round trip per level):
+//  * top-down frontier-queue expansion, thread per frontier vertex;
+//  * a visited bitmap (n/8 bytes: 2 MiB at n = 2^24, L2-resident) filters
+//    the random neighbour probes before the claiming atomicOr, so the
+//    random traffic stays in the 126 MB L2 instead of HBM;
+//  * newly claimed vertices go to a block-local queue in shared memory
+//    (shared-memory atomics), then one global atomicAdd per block reserves
+//    space in the next frontier (block-aggregated atomics);
+//  * a grid-wide barrier (cooperative groups) separates levels.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace jb {
+namespace bfs {
+
+constexpr int THREADS = 512;
+constexpr int LQ = 4096;  // block-local queue capacity
+
+struct Args {
+  const uint32_t *starting, *nedges, *edges;
+  int32_t *cost;
+  uint32_t *visited;  // bitmap
+  uint32_t *q[2];     // frontier queues
+  uint32_t *qsize;    // [4]: size of q[0], q[1] (+ padding)
+  uint32_t n;
+};
+
+__global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t lq[LQ];
+  __shared__ uint32_t lcount, lbase;
+  const uint32_t gtid = blockIdx.x * THREADS + threadIdx.x;
+  const uint32_t gsize = gridDim.x * THREADS;
+
+  for (int level = 0;; level++) {
+    const int cur = level & 1, nxt = cur ^ 1;
+    const uint32_t fsize = *((volatile uint32_t *)&a.qsize[cur]);
+    if (fsize == 0) break;
+    const uint32_t *fq = a.q[cur];
+    uint32_t *nq = a.q[nxt];
+    const int32_t nl = level + 1;
+    // uniform trip count across the block so __syncthreads stays legal
+    const uint32_t rounds = (fsize + gsize - 1) / gsize;
+    for (uint32_t r = 0; r < rounds; r++) {
+      if (threadIdx.x == 0) lcount = 0;
+      __syncthreads();
+      const uint32_t i = r * gsize + gtid;
+      if (i < fsize) {
+        const uint32_t u = fq[i];
+        const uint32_t e0 = __ldg(a.starting + u), e1 = e0 + __ldg(a.nedges + u);
+        for (uint32_t e = e0; e < e1; e++) {
+          const uint32_t v = __ldg(a.edges + e);
+          const uint32_t bit = 1u << (v & 31);
+          if (a.visited[v >> 5] & bit) continue;  // cheap L2 probe
+          const uint32_t old = atomicOr(a.visited + (v >> 5), bit);
+          if (old & bit) continue;                 // someone else claimed v
+          a.cost[v] = nl;
+          const uint32_t slot = atomicAdd(&lcount, 1u);
+          if (slot < LQ) {
+            lq[slot] = v;
+          } else {  // overflow: warp-aggregated direct append
+            const uint32_t mask = __activemask();
+            const int leader = __ffs(mask) - 1;
+            uint32_t base = 0;
+            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(a.qsize + nxt, __popc(mask));
+            base = __shfl_sync(mask, base, leader);
+            nq[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = v;
+          }
+        }
+      }
+      __syncthreads();
+      const uint32_t cnt = min(lcount, (uint32_t)LQ);
+      if (threadIdx.x == 0 && cnt) lbase = atomicAdd(a.qsize + nxt, cnt);
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < cnt; k += THREADS) nq[lbase + k] = lq[k];
+    }
+    grid.sync();
+    if (gtid == 0) a.qsize[cur] = 0;  // consumed; becomes the next-next queue
+    grid.sync();
+  }
+}
+
+__global__ void bfs_init_kernel(int32_t *cost, uint32_t *visited, uint32_t n, uint32_t words, uint32_t source,
+                                uint32_t *q0, uint32_t *qsize) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) cost[i] = -1;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gridDim.x * blockDim.x) visited[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    qsize[0] = 1;
+    qsize[1] = 0;
+    q0[0] = source;
+  }
+}
+
+__global__ void bfs_seed_kernel(int32_t *cost, uint32_t *visited, uint32_t source) {
+  cost[source] = 0;
+  visited[source >> 5] |= 1u << (source & 31);
+}
+
+}  // namespace bfs
+}  // namespace jb
+
+using namespace jb;
+using namespace jb::bfs;
+
+extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, const uint32_t *nedges,
+                            const uint32_t *edges, uint32_t source, int32_t *cost, void *stream) {
+  JB_REQUIRE(n < (1ull << 32) - 64 && m < (1ull << 32), "bfs: graph too large for u32 indices");
+  if (n == 0) return JB_OK;
+  JB_REQUIRE(source < n, "bfs: source %u out of bounds for n=%llu", source, (unsigned long long)n);
+  JB_REQUIRE(starting && nedges && cost && (edges || m == 0), "bfs: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t words = (uint32_t)((n + 31) / 32);
+  const size_t qbytes = ((n * 4 + 255) / 256) * 256;
+  const size_t vbytes = ((words * 4 + 255) / 256) * 256;
+  char *ws = (char *)workspace(2 * qbytes + vbytes + 256, s);
+  if (!ws) return JB_ECUDA;
+  Args a;
+  a.starting = starting; a.nedges = nedges; a.edges = edges; a.cost = cost;
+  a.q[0] = (uint32_t *)ws;
+  a.q[1] = (uint32_t *)(ws + qbytes);
+  a.visited = (uint32_t *)(ws + 2 * qbytes);
+  a.qsize = (uint32_t *)(ws + 2 * qbytes + vbytes);
+  a.n = (uint32_t)n;
+  bfs_init_kernel<<<sm_count() * 4, 256, 0, s>>>(cost, a.visited, (uint32_t)n, words, source, a.q[0], a.qsize);
+  JB_LAUNCHED("bfs_init");
+  bfs_seed_kernel<<<1, 1, 0, s>>>(cost, a.visited, source);
+  JB_LAUNCHED("bfs_seed");
+  int per_sm = 0;
+  JB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, THREADS, 0));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = sm_count() * per_sm;
+  void *args[] = {&a};
+  void *tok = prof_begin("bfs_levels", s);
+  JB_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)bfs_kernel, dim3(grid), dim3(THREADS), args, 0, s));
+  prof_end(tok, s);
+  JB_LAUNCHED("bfs_levels");
+  return JB_OK;
+}

@@ -1,0 +1,29 @@
+"""CAVA camera pipeline on the B200 vs the oracle restatement: bit-exact u8."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2503_10855_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("shape,P", [((1, 64, 96), 16), ((2, 33, 70), 16), ((1, 135, 240), 64),
+                                     ((1, 3, 3), 4), ((1, 1080, 1920), 16), ((3, 70, 130), 0)])
+def test_cava_matches_oracle(jb, oracle, shape, P):
+    b, r, c = shape
+    raw = W.cava_raw(b, r, c, seed=r)
+    params = W.cava_params(P=max(P, 1))
+    if P == 0:
+        params = (params[0], params[1][:0], params[2][:0], params[3], params[4])
+    got = jb.cava(raw, *params)
+    ref = oracle.cava(raw, *params)
+    assert got.dtype == np.uint8 and got.shape == raw.shape
+    bad = np.count_nonzero(got != ref)
+    assert bad == 0, f"{bad}/{got.size} u8 values differ (max |d| {np.abs(got.astype(int) - ref).max()})"
+
+
+def test_cava_scale_transform_pinned(oracle):
+    g = golden("cava_stages_6x8")
+    sc = oracle.cava_stage("scale", g["raw"])
+    assert np.array_equal(sc.view(np.uint32), g["scaled"].view(np.uint32))

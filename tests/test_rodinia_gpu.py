@@ -1,0 +1,119 @@
+"""SRAD, CFD/Euler, BFS and backprop on the B200 vs the oracle restatement."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2503_10855_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    """Bit patterns, with every NaN mapped to one canonical payload (the
+    reference semantics do not distinguish NaN payloads)."""
+    a = np.ascontiguousarray(a)
+    if a.dtype != np.float32:
+        return a
+    b = a.view(np.uint32).copy()
+    b[np.isnan(a)] = 0x7FC00000
+    return b
+
+
+def _exact(got, ref):
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert got.shape == ref.shape and got.dtype == ref.dtype
+    bad = np.count_nonzero(_bits(got) != _bits(ref))
+    assert bad == 0, f"{bad}/{got.size} differ; max |d| = {np.nanmax(np.abs(got.astype(np.float64) - ref)):.3g}"
+
+
+# ------------------------------------------------------------------ SRAD
+@pytest.mark.parametrize("shape,niter", [((64, 64), 3), ((100, 130), 5), ((257, 129), 4), ((1, 1), 2),
+                                         ((33, 260), 1), ((48, 48), 0), ((512, 512), 10)])
+def test_srad_matches_oracle(jb, oracle, shape, niter):
+    img = W.srad_image(*shape, seed=shape[0])
+    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True)
+    ref, rq0 = oracle.srad(img, niter, 0.5, return_q0=True)
+    if shape == (1, 1):  # zero variance: q0 = 0/0 on both sides
+        assert np.isnan(q0).all() == np.isnan(rq0).all()
+    else:
+        _exact(q0, rq0)  # f64 statistics round to the same f32 q0^2
+    # contract: rel 1e-5 (exp/log evaluated in double on both sides)
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5, equal_nan=True)
+    # observed: bit-identical
+    assert np.count_nonzero(_bits(out) != _bits(ref)) <= out.size // 10000
+
+
+def test_srad_iteration_pinned_to_reference_interpreter(jb, oracle):
+    """One coefficient+update pass against skiff's oracle_execute: the GPU
+    pipeline with niter=1 must reproduce the pinned C iteration."""
+    g = golden("srad_iter_10x13")
+    _exact(oracle.srad_iter(g["J"], float(g["q0sqr"]), float(g["lam"])), g["out"])
+
+
+# ------------------------------------------------------------------ CFD
+def _mesh(w=64, h=48, seed=0):
+    return W.euler_mesh(w, h, seed=seed)
+
+
+@pytest.mark.parametrize("wh,iters", [((64, 48), 1), ((37, 29), 3), ((256, 128), 2), ((1, 1), 1)])
+def test_euler_matches_oracle_bitwise(jb, oracle, wh, iters):
+    areas, nb, normals, ff, v = _mesh(*wh, seed=wh[0])
+    got = jb.euler(iters, areas, nb, normals, ff, v)
+    ref = oracle.euler(areas, nb, normals, ff, v, iters)
+    _exact(got, ref)
+    assert not np.array_equal(got, v)  # the state actually evolved
+
+
+def test_euler_stages_bitwise(jb, oracle):
+    areas, nb, normals, ff, v = _mesh(80, 60, seed=3)
+    _exact(jb.euler_step_factor(v, areas), oracle.euler_step_factor(v, areas))
+    _exact(jb.euler_flux(nb, normals, ff, v), oracle.euler_flux(nb, normals, ff, v))
+
+
+# ------------------------------------------------------------------ BFS
+@pytest.mark.parametrize("name", ["bfs_60", "bfs_200", "bfs_1000"])
+def test_bfs_matches_reference_interpreter(jb, name):
+    g = golden(name)
+    _exact(jb.bfs(g["starting"], g["no_of_edges"], g["edges"], int(g["source"])), g["cost"])
+
+
+@pytest.mark.parametrize("n,seed", [(1 << 16, 1), (100_003, 2), (1 << 20, 3)])
+def test_bfs_random_graph_bitwise(jb, oracle, n, seed):
+    s, d, e = W.bfs_graph(n, seed=seed)
+    src = seed * 7 % n
+    _exact(jb.bfs(s, d, e, src), oracle.bfs(s, d, e, src))
+
+
+def test_bfs_edge_cases(jb, oracle):
+    # isolated source, self loops, unreachable tail, zero-degree nodes
+    s = np.array([0, 0, 1, 3, 3], np.uint32)
+    d = np.array([0, 1, 2, 0, 1], np.uint32)
+    e = np.array([2, 2, 3, 4], np.uint32)
+    for src in range(5):
+        _exact(jb.bfs(s, d, e, src), oracle.bfs(s, d, e, src))
+    one = jb.bfs(np.zeros(1, np.uint32), np.zeros(1, np.uint32), np.zeros(0, np.uint32), 0)
+    assert one.tolist() == [0]
+
+
+# ------------------------------------------------------------------ backprop
+@pytest.mark.parametrize("n_in,n_hid", [(1000, 16), (65536, 16), (4097, 8), (333, 32)])
+def test_backprop_matches_oracle(jb, oracle, n_in, n_hid):
+    x, iw, hw, t, ipw, hpw = W.bp_inputs(n_in, n_hid, 1, seed=n_in)
+    # non-saturated variant: small weights so squash is not flat
+    iw = (iw - 0.5) * np.float32(4.0 / np.sqrt(n_in))
+    iw = iw.astype(np.float32)
+    eo, eh, iw2, hw2, ipw2, hpw2 = jb.backprop(x, iw, hw, t, ipw, hpw)
+    ref = oracle.bp_train(x, iw, hw, t, ipw, hpw, acc64=True)
+    # f64-accumulated layer sums -> the same f32 with overwhelming probability
+    np.testing.assert_allclose(iw2, ref["input_weights"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(hw2, ref["hidden_weights"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(ipw2, ref["input_prev_weights"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(hpw2, ref["hidden_prev_weights"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose([eo, eh], [ref["out_err"], ref["hid_err"]], rtol=1e-6)
+    assert np.count_nonzero(_bits(iw2) != _bits(ref["input_weights"])) <= iw2.size // 1000
+
+
+def test_backprop_adjust_pinned(oracle):
+    g = golden("bp_33x5")
+    w, _ = oracle.bp_adjust_weights(g["delta"], g["ly"], g["w"], g["oldw"])
+    _exact(w[:, 1:], g["adjusted"][:, 1:])
