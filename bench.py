@@ -306,7 +306,329 @@ class MatmulWorkload:
         return bool(np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-5)
 
 
-WORKLOADS = {"edge": EdgeWorkload, "matmul": MatmulWorkload}
+class _DeviceCall:
+    """Shared plumbing for the single-call workloads below: host arrays are
+    uploaded once (value), or copied H2D + D2H around every call (e2e)."""
+    flush_l2 = False
+    scaling = "weak"
+    local = 1
+
+    def setup_device(self, torch):
+        from paper_2503_10855_b200 import _lib
+        self.torch = torch
+        self.lib = _lib.load()
+        self.stream = torch.cuda.current_stream()
+        self.dev = {}
+        self.pin = {}
+        for k, a in self.host.items():
+            t = torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a)
+            self.dev[k] = t.cuda()
+            self.pin[k] = t.pin_memory()
+        self.alloc_outputs(torch)
+
+    def check_rc(self, rc):
+        if rc:
+            from paper_2503_10855_b200 import _lib
+            raise RuntimeError(_lib.last_error())
+
+    def step_e2e(self):
+        for k in self.inputs_e2e:
+            self.dev[k].copy_(self.pin[k], non_blocking=True)
+        self.step_device()
+        for k, t in self.outputs_e2e():
+            self.pin_out[k].copy_(t, non_blocking=True)
+        self.stream.synchronize()
+
+    def e2e_bytes(self):
+        h2d = sum(self.host[k].nbytes for k in self.inputs_e2e)
+        d2h = sum(t.numel() * t.element_size() for _, t in self.outputs_e2e())
+        return h2d, d2h
+
+
+class SradWorkload(_DeviceCall):
+    """srad<16384,16384>(niter=10, lambda=0.5): one step = one call."""
+    name = "srad"
+    metric = "srad_16384x16384_ms_per_iteration"
+    unit = "ms"
+    higher_is_better = False
+    kernel = "srad_iter"
+    bound = "hbm"
+    niter = 10
+
+    def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import workloads as W
+        self.rows = self.cols = 4096 if args.small else 16384
+        self.host = {"image": W.srad_image(self.rows, self.cols)}
+        self.inputs_e2e = ["image"]
+
+    def alloc_outputs(self, torch):
+        self.out = torch.empty((self.rows, self.cols), dtype=torch.float32, device="cuda")
+        self.pin_out = {"out": torch.empty((self.rows, self.cols), dtype=torch.float32).pin_memory()}
+
+    def outputs_e2e(self):
+        return [("out", self.out)]
+
+    def config(self, world):
+        return {"workload": f"srad<{self.rows},{self.cols}> niter={self.niter} lambda=0.5 (Rodinia srad_v1)",
+                "parallelism": "single GPU", "l2": "1 GiB image >> 126 MB L2"}
+
+    def units_per_step(self):
+        return self.niter
+
+    def algorithmic_bytes_per_unit(self):
+        return 8 * self.rows * self.cols  # read J + write J' per iteration (SURVEY §8(d))
+
+    def step_device(self):
+        self.check_rc(self.lib.jb_srad_f32(self.rows, self.cols, self.niter, 0.5, self.dev["image"].data_ptr(),
+                                           self.out.data_ptr(), None, self.stream.cuda_stream))
+
+    def value_from(self, ms_per_step):
+        return ms_per_step / self.niter
+
+    def cpu_sample(self, oracle):
+        crop = self.host["image"][:2048, :2048]
+        t = time.perf_counter()
+        oracle.srad(crop, 2, 0.5)
+        dt = time.perf_counter() - t
+        scale = (self.rows * self.cols) / crop.size
+        return dt / 2 * scale * 1e3, "2048x2048 crop, 2 iterations, scaled to ms/iteration at full size"
+
+    def check(self, oracle):
+        crop = np.ascontiguousarray(self.host["image"][:512, :512])
+        import paper_2503_10855_b200 as jbp
+        got = jbp.srad(3, 0.5, crop)
+        ref = oracle.srad(crop, 3, 0.5)
+        return bool(np.allclose(got, ref, rtol=1e-5, atol=1e-5))
+
+
+class EulerWorkload(_DeviceCall):
+    """euler<2^22> on a 2048x2048 structured-synthetic mesh, 10 iterations
+    (3 RK stages each) per step."""
+    name = "euler"
+    metric = "cfd_euler_2048x2048_ms_per_iteration"
+    unit = "ms"
+    higher_is_better = False
+    kernel = "euler_rk"
+    bound = "hbm"
+    iters = 10
+
+    def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import workloads as W
+        self.w = self.h = 512 if args.small else 2048
+        areas, nb, normals, ff, v = W.euler_mesh(self.w, self.h)
+        self.nelr = areas.shape[0]
+        self.host = {"areas": areas, "nb": nb, "normals": normals, "ff": ff, "v": v}
+        self.inputs_e2e = ["areas", "nb", "normals", "ff", "v"]
+
+    def alloc_outputs(self, torch):
+        self.pin_out = {"v": torch.empty((5, self.nelr), dtype=torch.float32).pin_memory()}
+
+    def outputs_e2e(self):
+        return [("v", self.dev["v"])]
+
+    def config(self, world):
+        return {"workload": f"euler<{self.nelr}> {self.w}x{self.h} structured mesh, {self.iters} iterations x RK3",
+                "parallelism": "single GPU", "l2": f"{self.nelr * 128 / 1e6:.0f} MB streamed per stage > L2"}
+
+    def units_per_step(self):
+        return self.iters
+
+    def algorithmic_bytes_per_unit(self):
+        # per RK stage and element: own vars 20 + normals 48 + neighbour ids 16
+        # + old vars 20 + area 4 + new vars 20 = 128 B (neighbour vars cached)
+        return 3 * 128 * self.nelr  # per iteration = 3 RK-stage launches
+
+    def step_device(self):
+        d = self.dev
+        self.check_rc(self.lib.jb_euler_f32(self.nelr, self.iters, d["areas"].data_ptr(), d["nb"].data_ptr(),
+                                            d["normals"].data_ptr(), d["ff"].data_ptr(), d["v"].data_ptr(),
+                                            self.stream.cuda_stream))
+
+    def value_from(self, ms_per_step):
+        return ms_per_step / self.iters
+
+    def cpu_sample(self, oracle):
+        h = self.host
+        t = time.perf_counter()
+        oracle.euler(h["areas"], h["nb"], h["normals"], h["ff"], h["v"], 1)
+        return (time.perf_counter() - t) * 1e3, "1 iteration at full size, oracle/juno_oracle.c (OpenMP)"
+
+    def check(self, oracle):
+        from paper_2503_10855_b200 import workloads as W
+        import paper_2503_10855_b200 as jbp
+        m = W.euler_mesh(256, 128, seed=5)
+        return bool(np.array_equal(jbp.euler(2, *m), oracle.euler(*m, 2)))
+
+
+class BfsWorkload(_DeviceCall):
+    """bfs<2^24, ~6*2^24> from source 0; one step = one traversal."""
+    name = "bfs"
+    metric = "bfs_16M_gteps"
+    unit = "GTEPS"
+    higher_is_better = True
+    kernel = "bfs_levels"
+    bound = "hbm"
+
+    def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import workloads as W
+        self.n = 1 << (20 if args.small else 24)
+        s, d, e = W.bfs_graph(self.n)
+        self.m = e.shape[0]
+        self.host = {"s": s, "d": d, "e": e}
+        self.inputs_e2e = ["s", "d", "e"]
+
+    def alloc_outputs(self, torch):
+        self.cost = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        self.pin_out = {"cost": torch.empty(self.n, dtype=torch.int32).pin_memory()}
+
+    def outputs_e2e(self):
+        return [("cost", self.cost)]
+
+    def config(self, world):
+        return {"workload": f"bfs n={self.n} m={self.m} (degree U{{1..11}}, seed 42), source 0",
+                "parallelism": "replicas" if world > 1 else "single GPU",
+                "l2": "CSR 0.5 GB > L2; visited bitmap (2 MiB) L2-resident by design"}
+
+    def units_per_step(self):
+        return self.m / 1e9  # giga-edges
+
+    def algorithmic_bytes_per_unit(self):
+        # 8n + 8m bytes per traversal (SURVEY §8(d)) per giga-edge unit
+        return (8 * self.n + 8 * self.m) / (self.m / 1e9)
+
+    def step_device(self):
+        d = self.dev
+        self.check_rc(self.lib.jb_bfs(self.n, self.m, d["s"].data_ptr(), d["d"].data_ptr(), d["e"].data_ptr(), 0,
+                                      self.cost.data_ptr(), self.stream.cuda_stream))
+
+    def cpu_sample(self, oracle):
+        h = self.host
+        t = time.perf_counter()
+        oracle.bfs(h["s"], h["d"], h["e"], 0)
+        return self.m / 1e9 / (time.perf_counter() - t), "full traversal, oracle/juno_oracle.c (1 thread)"
+
+    def check(self, oracle):
+        h = self.host
+        return bool(np.array_equal(self.cost.cpu().numpy(), oracle.bfs(h["s"], h["d"], h["e"], 0)))
+
+
+class BackpropWorkload(_DeviceCall):
+    """backprop<2^24,16,1>: one bpnn_train step per step."""
+    name = "backprop"
+    metric = "backprop_16M_train_step_ms"
+    unit = "ms"
+    higher_is_better = False
+    kernel = "bp_adjust"
+    bound = "hbm"
+
+    def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import workloads as W
+        self.n_in = 1 << (20 if args.small else 24)
+        x, iw, hw, t, ipw, hpw = W.bp_inputs(self.n_in, 16, 1)
+        self.host = {"x": x, "iw": iw, "hw": hw, "t": t, "ipw": ipw, "hpw": hpw}
+        self.inputs_e2e = ["x", "iw", "hw", "t", "ipw", "hpw"]
+
+    def alloc_outputs(self, torch):
+        self.hidden = torch.empty(17, dtype=torch.float32, device="cuda")
+        self.output = torch.empty(2, dtype=torch.float32, device="cuda")
+        self.errs = torch.empty(2, dtype=torch.float32, device="cuda")
+        self.pin_out = {k: torch.empty(self.host[k].shape, dtype=torch.float32).pin_memory()
+                        for k in ("iw", "hw", "ipw", "hpw")}
+        self.pin_out["errs"] = torch.empty(2, dtype=torch.float32).pin_memory()
+
+    def outputs_e2e(self):
+        return [(k, self.dev[k]) for k in ("iw", "hw", "ipw", "hpw")] + [("errs", self.errs)]
+
+    def config(self, world):
+        return {"workload": f"backprop<{self.n_in},16,1> one bpnn_train step (Rodinia init)",
+                "parallelism": "single GPU", "l2": "weights 2 x 1.07 GiB >> L2"}
+
+    def units_per_step(self):
+        return 1
+
+    def algorithmic_bytes_per_unit(self):
+        return 16 * (self.n_in + 1) * 17  # adjust_weights: read w, oldw; write w, oldw
+
+    def step_device(self):
+        d = self.dev
+        self.check_rc(self.lib.jb_bp_train_f32(self.n_in, 16, 1, d["x"].data_ptr(), d["iw"].data_ptr(),
+                                               d["hw"].data_ptr(), d["t"].data_ptr(), d["ipw"].data_ptr(),
+                                               d["hpw"].data_ptr(), self.hidden.data_ptr(), self.output.data_ptr(),
+                                               self.errs.data_ptr(), self.stream.cuda_stream))
+
+    def cpu_sample(self, oracle):
+        h = self.host
+        n = 1 << 20
+        t = time.perf_counter()
+        oracle.bp_train(h["x"][:n + 1], h["iw"][:n + 1], h["hw"], h["t"], h["ipw"][:n + 1], h["hpw"])
+        return (time.perf_counter() - t) * (self.n_in / n) * 1e3, "2^20-input slab, scaled to 2^24"
+
+    def check(self, oracle):
+        from paper_2503_10855_b200 import workloads as W
+        import paper_2503_10855_b200 as jbp
+        x, iw, hw, t, ipw, hpw = W.bp_inputs(4096, 16, 1, seed=9)
+        got = jbp.backprop(x, iw, hw, t, ipw, hpw)
+        ref = oracle.bp_train(x, iw, hw, t, ipw, hpw)
+        return bool(np.allclose(got[2], ref["input_weights"], rtol=1e-6))
+
+
+class CavaWorkload(_DeviceCall):
+    """cava on a batch of 16 synthetic 1080x1920 raw frames, P=16."""
+    name = "cava"
+    metric = "cava_frames_per_s"
+    unit = "frames/s"
+    higher_is_better = True
+    kernel = "cava_fused"
+    bound = "hbm"
+    scaling = "strong"
+
+    def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import workloads as W
+        self.batch = 4 if args.small else 16
+        self.r, self.c = (270, 480) if args.small else (1080, 1920)
+        self.P = 16
+        self.host = {"raw": W.cava_raw(self.batch, self.r, self.c)}
+        self.params = W.cava_params(self.P)
+        for k, v in zip(("tstw", "ctrl", "wts", "coefs", "tmap"), self.params):
+            self.host[k] = v
+        self.inputs_e2e = ["raw"]
+        self.local = self.batch
+
+    def alloc_outputs(self, torch):
+        self.out = torch.empty(self.host["raw"].shape, dtype=torch.uint8, device="cuda")
+        self.pin_out = {"out": torch.empty(self.host["raw"].shape, dtype=torch.uint8).pin_memory()}
+
+    def outputs_e2e(self):
+        return [("out", self.out)]
+
+    def config(self, world):
+        return {"workload": f"cava batch={self.batch} u8[3,{self.r},{self.c}] P={self.P} control points",
+                "parallelism": "frames", "l2": f"{self.batch * 6 * self.r * self.c / 1e6:.0f} MB in+out"}
+
+    def units_per_step(self):
+        return self.batch
+
+    def algorithmic_bytes_per_unit(self):
+        return 6 * self.r * self.c  # u8 x3 in + u8 x3 out (SURVEY §8(d))
+
+    def step_device(self):
+        d = self.dev
+        self.check_rc(self.lib.jb_cava_u8(self.batch, self.r, self.c, self.P, d["raw"].data_ptr(),
+                                          d["tstw"].data_ptr(), d["ctrl"].data_ptr(), d["wts"].data_ptr(),
+                                          d["coefs"].data_ptr(), d["tmap"].data_ptr(), self.out.data_ptr(),
+                                          self.stream.cuda_stream))
+
+    def cpu_sample(self, oracle):
+        t = time.perf_counter()
+        oracle.cava(self.host["raw"][:1], *self.params)
+        return 1.0 / (time.perf_counter() - t), "1 frame, oracle/juno_oracle.c (OpenMP)"
+
+    def check(self, oracle):
+        return bool(np.array_equal(self.out[:1].cpu().numpy(), oracle.cava(self.host["raw"][:1], *self.params)))
+
+
+WORKLOADS = {"edge": EdgeWorkload, "matmul": MatmulWorkload, "srad": SradWorkload, "euler": EulerWorkload,
+             "bfs": BfsWorkload, "backprop": BackpropWorkload, "cava": CavaWorkload}
 
 
 # ------------------------------------------------------------------ arms
@@ -373,14 +695,15 @@ def run_ours(args):
     if hib:
         value = units * args.steps / (ms_max / 1e3)
         e2e_value = units * args.e2e_steps / (e2e_ms / 1e3)
-    else:  # time-like metric: ms per step
-        value = ms_max / args.steps
-        e2e_value = e2e_ms / args.e2e_steps
+    else:  # time-like metric: ms per step (or per unit via value_from)
+        vf = getattr(wl, "value_from", lambda x: x)
+        value = vf(ms_max / args.steps)
+        e2e_value = vf(e2e_ms / args.e2e_steps)
     peaks = load_peaks()
     roofline = None
     if kcount:
         avg_ms = kms / kcount
-        local_units = getattr(wl, "local", 1) * args.steps
+        local_units = (wl.local if isinstance(wl, EdgeWorkload) else units) * args.steps
         per_launch_units = local_units / kcount
         if getattr(wl, "bound", "hbm") == "tensor":
             alg = wl.flops_per_unit() * per_launch_units

@@ -118,9 +118,29 @@ struct Smem {
   float c[CR][JP];
 };
 
+// c at image position (gy, gx) from the replicated J tile (tile origin y0,x0).
+// The replicated halo reproduces the oracle's clamped neighbour indices
+// (iN[0] = 0, iS[rows-1] = rows-1, ...): a clamped neighbour equals the centre.
+__device__ __forceinline__ float coef(const Smem &S, int jr, int jc, float q0, float q0den) {
+  const float Jc = S.J[jr][jc];
+  const float n_ = sub_rn(S.J[jr - 1][jc], Jc);
+  const float s_ = sub_rn(S.J[jr + 1][jc], Jc);
+  const float w_ = sub_rn(S.J[jr][jc - 1], Jc);
+  const float e_ = sub_rn(S.J[jr][jc + 1], Jc);
+  const float G2 =
+      div_rn(add_rn(add_rn(add_rn(mul_rn(n_, n_), mul_rn(s_, s_)), mul_rn(w_, w_)), mul_rn(e_, e_)), mul_rn(Jc, Jc));
+  const float L = div_rn(add_rn(add_rn(add_rn(n_, s_), w_), e_), Jc);
+  const float num = sub_rn(mul_rn(0.5f, G2), mul_rn(0.0625f, mul_rn(L, L)));
+  const float den = add_rn(1.0f, mul_rn(0.25f, L));
+  const float qsqr = div_rn(num, mul_rn(den, den));
+  const float den2 = div_rn(sub_rn(qsqr, q0), q0den);
+  const float cv = div_rn(1.0f, add_rn(1.0f, den2));
+  return cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
+}
+
 __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
   __shared__ Smem S;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rows = a.rows, cols = a.cols;
   const float q0 = *a.q0;
   const float q0den = mul_rn(q0, add_rn(1.0f, q0));
@@ -129,68 +149,79 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
     const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
     const int y0 = ty * TH, x0 = tx * TW;
-    // ---- J tile with clamped (replicated) halo: rows y0-1..y0+TH+1, cols x0-1..x0+TW+1
-    for (int idx = tid; idx < JR * JC; idx += THREADS) {
-      const int r = idx / JC, cc = idx - r * JC;
-      const int gy = min(max(y0 - 1 + r, 0), rows - 1);
-      const int gx = min(max(x0 - 1 + cc, 0), cols - 1);
-      S.J[r][cc] = __ldg(a.src + (size_t)gy * cols + gx);
+    // ---- J tile with replicated halo: rows y0-1..y0+TH+1, cols x0-1..x0+TW+1.
+    // warp w loads rows w, w+8, ...; lane l loads cols l, l+32, ... (loads first)
+    {
+      constexpr int RPW = (JR + 7) / 8;  // 5
+      float v[RPW][5];
+#pragma unroll
+      for (int i = 0; i < RPW; i++) {
+        const int r = min(warp + 8 * i, JR - 1);
+        const float *row = a.src + (size_t)min(max(y0 - 1 + r, 0), rows - 1) * cols;
+#pragma unroll
+        for (int q = 0; q < 5; q++) {
+          const int cc = min(32 * q + lane, JC - 1);
+          v[i][q] = __ldg(row + min(max(x0 - 1 + cc, 0), cols - 1));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RPW; i++) {
+        const int r = warp + 8 * i;
+#pragma unroll
+        for (int q = 0; q < 5; q++) {
+          const int cc = 32 * q + lane;
+          if (r < JR && cc < JC) S.J[r][cc] = v[i][q];
+        }
+      }
     }
     __syncthreads();
-    // ---- diffusion coefficient on rows y0..y0+TH, cols x0..x0+TW (clamped
-    // to the image: an out-of-range position is never read, see stage C)
-    for (int idx = tid; idx < CR * CC; idx += THREADS) {
-      const int r = idx / CC, cc = idx - r * CC;
-      const int gy = y0 + r, gx = x0 + cc;
-      if (gy >= rows || gx >= cols) continue;
-      // neighbours with the oracle's clamped indices, expressed in the
-      // replicated tile: row gy -> r+1, iN -> r (or r+1 at the top edge) ...
-      const int jr = r + 1, jc = cc + 1;
-      const float Jc = S.J[jr][jc];
-      const float n_ = sub_rn(S.J[gy > 0 ? jr - 1 : jr][jc], Jc);
-      const float s_ = sub_rn(S.J[gy < rows - 1 ? jr + 1 : jr][jc], Jc);
-      const float w_ = sub_rn(S.J[jr][gx > 0 ? jc - 1 : jc], Jc);
-      const float e_ = sub_rn(S.J[jr][gx < cols - 1 ? jc + 1 : jc], Jc);
-      const float G2 = div_rn(add_rn(add_rn(add_rn(mul_rn(n_, n_), mul_rn(s_, s_)), mul_rn(w_, w_)), mul_rn(e_, e_)),
-                              mul_rn(Jc, Jc));
-      const float L = div_rn(add_rn(add_rn(add_rn(n_, s_), w_), e_), Jc);
-      const float num = sub_rn(mul_rn(0.5f, G2), mul_rn(0.0625f, mul_rn(L, L)));
-      const float den = add_rn(1.0f, mul_rn(0.25f, L));
-      const float qsqr = div_rn(num, mul_rn(den, den));
-      const float den2 = div_rn(sub_rn(qsqr, q0), q0den);
-      float cv = div_rn(1.0f, add_rn(1.0f, den2));
-      cv = cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
-      S.c[r][cc] = cv;
+    // ---- diffusion coefficient on rows y0..y0+TH, cols x0..x0+TW.  A
+    // position past the image edge gets the coefficient of the clamped
+    // position, which is exactly what the oracle's c[iS[i]] / c[jE[j]] read.
+#pragma unroll 1
+    for (int r = warp; r < CR; r += 8) {
+      const int jr = min(y0 + r, rows - 1) - y0 + 1;
+#pragma unroll
+      for (int q = 0; q < TW / 32; q++) {  // the tile's own 128 columns
+        const int cc = 32 * q + lane;
+        const int jc = min(x0 + cc, cols - 1) - x0 + 1;
+        S.c[r][cc] = coef(S, jr, jc, q0, q0den);
+      }
+    }
+    if (tid < CR) {  // the east halo column (cc = TW), one row per thread
+      const int r = tid;
+      const int jr = min(y0 + r, rows - 1) - y0 + 1;
+      const int jc = min(x0 + TW, cols - 1) - x0 + 1;
+      S.c[r][TW] = coef(S, jr, jc, q0, q0den);
     }
     __syncthreads();
-    // ---- update J' = J + ql * D on the tile
-    const int cc = tid & (TW - 1);
-    const int rbase = (tid >> 7) * (TH / 2);
-    const int gx = x0 + cc;
-    if (gx < cols) {
-      const int jc = cc + 1;
-      const int ce = gx < cols - 1 ? cc + 1 : cc;  // clamped east column in c
-#pragma unroll 4
-      for (int k = 0; k < TH / 2; k++) {
-        const int r = rbase + k, gy = y0 + r;
-        if (gy >= rows) break;
-        const int jr = r + 1;
-        const float Jc = S.J[jr][jc];
-        const float n_ = sub_rn(S.J[gy > 0 ? jr - 1 : jr][jc], Jc);
-        const float s_ = sub_rn(S.J[gy < rows - 1 ? jr + 1 : jr][jc], Jc);
-        const float w_ = sub_rn(S.J[jr][gx > 0 ? jc - 1 : jc], Jc);
-        const float e_ = sub_rn(S.J[jr][gx < cols - 1 ? jc + 1 : jc], Jc);
-        const float cN = S.c[r][cc];
-        const float cS = S.c[gy < rows - 1 ? r + 1 : r][cc];
-        const float cE = S.c[r][ce];
-        const float D = add_rn(add_rn(add_rn(mul_rn(cN, n_), mul_rn(cS, s_)), mul_rn(cN, w_)), mul_rn(cE, e_));
-        const float jn = add_rn(Jc, mul_rn(a.ql, D));
-        if (a.compress) {
-          a.dst[(size_t)gy * cols + gx] = mul_rn(log_ref(jn), 255.0f);
-        } else {
-          a.dst[(size_t)gy * cols + gx] = jn;
-          s += (double)jn;
-          s2 += (double)jn * (double)jn;
+    // ---- update J' = J + ql * D on the tile: warp w rows 4w..4w+3, lane
+    // columns l, l+32, l+64, l+96
+#pragma unroll
+    for (int k = 0; k < TH / 8; k++) {
+      const int r = warp * (TH / 8) + k, gy = y0 + r;
+      if (gy >= rows) break;
+      const int jr = r + 1;
+#pragma unroll
+      for (int q = 0; q < TW / 32; q++) {
+        const int cc = 32 * q + lane, gx = x0 + cc;
+        if (gx < cols) {
+          const int jc = cc + 1;
+          const float Jc = S.J[jr][jc];
+          const float n_ = sub_rn(S.J[jr - 1][jc], Jc);
+          const float s_ = sub_rn(S.J[jr + 1][jc], Jc);
+          const float w_ = sub_rn(S.J[jr][jc - 1], Jc);
+          const float e_ = sub_rn(S.J[jr][jc + 1], Jc);
+          const float cN = S.c[r][cc], cS = S.c[r + 1][cc], cE = S.c[r][cc + 1];
+          const float D = add_rn(add_rn(add_rn(mul_rn(cN, n_), mul_rn(cS, s_)), mul_rn(cN, w_)), mul_rn(cE, e_));
+          const float jn = add_rn(Jc, mul_rn(a.ql, D));
+          if (a.compress) {
+            a.dst[(size_t)gy * cols + gx] = mul_rn(log_ref(jn), 255.0f);
+          } else {
+            a.dst[(size_t)gy * cols + gx] = jn;
+            s += (double)jn;
+            s2 += (double)jn * (double)jn;
+          }
         }
       }
     }
