@@ -6,18 +6,20 @@
 // (monoid-reassociate), so the contract is fp32 tolerance:
 //     |C - C_ref| <= (2*gamma_m + 8u) * (|A| |B|)   elementwise, u = 2^-24.
 //
-// B200 design: 3xTF32 on the 5th-gen tensor cores.
-//   split kernels  : A -> (A_hi, A_lo), B -> (Bt_hi, Bt_lo) with x_hi =
-//                    rna_tf32(x), x_lo = rna_tf32(x - x_hi); B is transposed
-//                    on the way (tiled through shared memory) so both MMA
-//                    operands are K-major (an MN-major tf32 B descriptor
-//                    produced no result on this part, tools/mma_probe.cu).
-//   gemm kernel    : one 128x64 output tile per CTA; warp 0 = TMA producer
-//                    (4 operand tiles per 32-wide k-block, 128B swizzle,
-//                    4-stage mbarrier ring), warp 1 = TMEM allocator + single
-//                    thread tcgen05.mma issuer (D += Ahi*Bhi + Ahi*Blo +
-//                    Alo*Bhi, f32 accumulators in 64 TMEM columns), warps 2-5
-//                    = epilogue (tcgen05.ld -> registers -> global).
+// B200 design: 3xTF32 on the 5th-gen tensor cores,
+//   x_hi = x rounded to tf32, x_lo = x - x_hi (exact in f32),
+//   D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi   (f32 accumulators in TMEM).
+// One kernel, one 128x64 output tile per CTA, 320 threads:
+//   warp 0     TMA producer: raw fp32 A tile (K-major, 128B swizzle) and raw
+//              B tile ([32 k][64 n], unswizzled) per 32-wide k-block into a
+//              4-stage mbarrier ring.  Only raw operands cross L2 -> SMEM
+//              (the split is never materialised in HBM/L2).
+//   warps 2-9  converters: split the staged tile into tf32 hi/lo operands in
+//              shared memory -- A in place (same swizzled layout), B with a
+//              transpose into the K-major 128B-swizzle layout (B's MN-major
+//              tf32 descriptor gave no result on this part, see
+//              tools/mma_probe.cu); then the epilogue (tcgen05.ld -> global).
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer.
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
 #include <cudaTypedefs.h>
@@ -33,72 +35,43 @@ namespace mm {
 constexpr int BM = 128, BN = 64, BK = 32;  // BK fp32 = one 128-byte swizzle row
 constexpr int STAGES = 4;
 constexpr int A_TILE = BM * BK * 4;        // 16 KiB
-constexpr int B_TILE = BK * BN * 4;        // 8 KiB (64 K-major rows of 128 B)
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int THREADS = 192;
+constexpr int B_TILE = BK * BN * 4;        // 8 KiB
+constexpr int THREADS = 320;
+constexpr int CONVERTERS = 256;            // warps 2..9 (warps 2..5 also run the epilogue)
 constexpr uint32_t TMEM_COLS = 64;
 
 struct Smem {
-  uint8_t a_hi[STAGES][A_TILE];
+  uint8_t a_hi[STAGES][A_TILE];  // raw A, converted in place to A_hi
   uint8_t a_lo[STAGES][A_TILE];
-  uint8_t b_hi[STAGES][B_TILE];
-  uint8_t b_lo[STAGES][B_TILE];
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  uint8_t bt_hi[STAGES][B_TILE]; // K-major [64 n][32 k], 128B swizzle
+  uint8_t bt_lo[STAGES][B_TILE];
+  uint8_t b_raw[STAGES][B_TILE]; // [32 k][64 n] as loaded
+  uint64_t full[STAGES];         // TMA -> converters
+  uint64_t conv[STAGES];         // converters -> MMA
+  uint64_t empty[STAGES];        // MMA -> TMA
   uint64_t tmem_full;
   uint32_t tmem_base;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + manual 1 KiB alignment
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-__global__ void split_tf32_kernel(const float4 *__restrict__ x, float4 *__restrict__ hi, float4 *__restrict__ lo,
-                                  long long n4) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 v = __ldg(x + i);
-    float4 h, l;
-    h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
-    h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
-    h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
-    h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
-    hi[i] = h;
-    lo[i] = l;
-  }
-}
-
-// B [K][N] -> Bt_hi, Bt_lo [N][K] (32x32 tiles through shared memory)
-__global__ void split_tf32_transpose_kernel(const float *__restrict__ b, float *__restrict__ bt_hi,
-                                            float *__restrict__ bt_lo, int K, int N) {
-  __shared__ float t[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
-  for (int r = ty; r < 32; r += 8) {
-    const int k = k0 + r, nn = n0 + tx;
-    t[r][tx] = (k < K && nn < N) ? __ldg(b + (size_t)k * N + nn) : 0.f;
-  }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int nn = n0 + r, k = k0 + tx;
-    if (nn < N && k < K) {
-      const float v = t[tx][r];
-      const float h = tf32_rna(v);
-      bt_hi[(size_t)nn * K + k] = h;
-      bt_lo[(size_t)nn * K + k] = tf32_rna(v - h);
-    }
-  }
+// x_hi = x rounded to the nearest tf32 (ties away from zero: add half an
+// ulp of tf32 to the magnitude bits, clear the 13 low bits -- two integer
+// ops instead of cvt.rna.tf32.f32, which ptxas expands to ~8); x_lo = x - x_hi
+// is exact in f32 and the tensor core reads its leading 11 bits.
+__device__ __forceinline__ void split(float x, float &h, float &l) {
+  h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  l = x - h;
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-                   const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    float *__restrict__ c, int M, int N, int K) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1 KiB alignment by offsetting within the __shared__ array, so the compiler
+  // keeps the shared address space (LDS/STS, not generic LD/ST)
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int kblocks = (K + BK - 1) / BK;
@@ -106,12 +79,13 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; s++) {
       tc::mbar_init(&S.full[s], 1);
+      tc::mbar_init(&S.conv[s], CONVERTERS);
       tc::mbar_init(&S.empty[s], 1);
     }
     tc::mbar_init(&S.tmem_full, 1);
     tc::fence_mbar_init();
-    tc::tma_prefetch(&tm_ahi); tc::tma_prefetch(&tm_alo);
-    tc::tma_prefetch(&tm_bhi); tc::tma_prefetch(&tm_blo);
+    tc::tma_prefetch(&tm_a);
+    tc::tma_prefetch(&tm_b);
   }
   if (warp == 1) tc::tmem_alloc<TMEM_COLS>(&S.tmem_base);
   tc::tc_fence_before();
@@ -125,12 +99,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
       for (int kb = 0; kb < kblocks; kb++) {
         const int s = kb % STAGES;
         if (kb >= STAGES) tc::mbar_wait(&S.empty[s], ((kb / STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&S.full[s], STAGE_BYTES);
+        tc::mbar_arrive_expect_tx(&S.full[s], A_TILE + B_TILE);
         const int k0 = kb * BK;
-        tc::tma_load_2d(S.a_hi[s], &tm_ahi, &S.full[s], k0, m0);
-        tc::tma_load_2d(S.a_lo[s], &tm_alo, &S.full[s], k0, m0);
-        tc::tma_load_2d(S.b_hi[s], &tm_bhi, &S.full[s], k0, n0);
-        tc::tma_load_2d(S.b_lo[s], &tm_blo, &S.full[s], k0, n0);
+        tc::tma_load_2d(S.a_hi[s], &tm_a, &S.full[s], k0, m0);
+        tc::tma_load_2d(S.b_raw[s], &tm_b, &S.full[s], n0, k0);
       }
     }
   } else if (warp == 1) {
@@ -138,15 +110,15 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
     constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 0);
     for (int kb = 0; kb < kblocks; kb++) {
       const int s = kb % STAGES;
-      tc::mbar_wait(&S.full[s], (kb / STAGES) & 1);
+      tc::mbar_wait(&S.conv[s], (kb / STAGES) & 1);
       tc::tc_fence_after();
       if (lane == 0) {
         const uint32_t ahi = tc::smem_u32(S.a_hi[s]), alo = tc::smem_u32(S.a_lo[s]);
-        const uint32_t bhi = tc::smem_u32(S.b_hi[s]), blo = tc::smem_u32(S.b_lo[s]);
+        const uint32_t bhi = tc::smem_u32(S.bt_hi[s]), blo = tc::smem_u32(S.bt_lo[s]);
 #pragma unroll
         for (int k = 0; k < BK / 8; k++) {
-          // A and Bt: K-major, 128B rows, 8-row atoms of 1 KiB -> SBO = 1024;
-          // one MMA consumes 8 fp32 of K = 32 bytes of each row.
+          // K-major, 128B rows, 8-row atoms of 1 KiB -> SBO = 1024; one MMA
+          // consumes 8 fp32 of K = 32 bytes of each row.
           const uint64_t da_hi = tc::smem_desc_sw128(ahi + k * 32, 16, 1024);
           const uint64_t da_lo = tc::smem_desc_sw128(alo + k * 32, 16, 1024);
           const uint64_t db_hi = tc::smem_desc_sw128(bhi + k * 32, 16, 1024);
@@ -156,16 +128,52 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
           tc::mma_tf32(tmem_d, da_hi, db_lo, idesc, 1);
           tc::mma_tf32(tmem_d, da_lo, db_hi, idesc, 1);
         }
-        tc::mma_commit(&S.empty[s]);               // smem stage may be refilled
+        tc::mma_commit(&S.empty[s]);  // stage s may be refilled
         if (kb == kblocks - 1) tc::mma_commit(&S.tmem_full);
       }
       __syncwarp();
     }
   } else {
+    // ------------------------------------------------------ converters
+    const int ct = threadIdx.x - 64;  // 0..255
+    for (int kb = 0; kb < kblocks; kb++) {
+      const int s = kb % STAGES;
+      tc::mbar_wait(&S.full[s], (kb / STAGES) & 1);
+      // A: 1024 16-byte chunks, layout-preserving (hi in place, lo alongside)
+      float4 *ah = reinterpret_cast<float4 *>(S.a_hi[s]);
+      float4 *al = reinterpret_cast<float4 *>(S.a_lo[s]);
+#pragma unroll
+      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++) {
+        const int q = ct + i * CONVERTERS;
+        float4 v = ah[q], h, l;
+        split(v.x, h.x, l.x); split(v.y, h.y, l.y); split(v.z, h.z, l.z); split(v.w, h.w, l.w);
+        ah[q] = h;
+        al[q] = l;
+      }
+      // B: raw [32 k][64 n] -> Bt [64 n][32 k], K-major with the 128B swizzle
+      // (16-byte chunk c of row n stored at chunk c ^ (n & 7))
+      const float *br = reinterpret_cast<const float *>(S.b_raw[s]);
+      const int nn = ct & 63, cg = ct >> 6;  // 4 groups of 2 k-chunks
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const int cch = cg * 2 + i;  // k chunk: k = 4*cch .. 4*cch+3
+        float4 h, l;
+        split(br[(4 * cch + 0) * BN + nn], h.x, l.x);
+        split(br[(4 * cch + 1) * BN + nn], h.y, l.y);
+        split(br[(4 * cch + 2) * BN + nn], h.z, l.z);
+        split(br[(4 * cch + 3) * BN + nn], h.w, l.w);
+        const int off = nn * 128 + ((cch ^ (nn & 7)) << 4);
+        *reinterpret_cast<float4 *>(S.bt_hi[s] + off) = h;
+        *reinterpret_cast<float4 *>(S.bt_lo[s] + off) = l;
+      }
+      tc::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
+      tc::mbar_arrive(&S.conv[s]);
+    }
     // ------------------------------------------------------ epilogue
+    if (warp >= 6) goto done;  // four warps cover the 128 TMEM lanes
     tc::mbar_wait(&S.tmem_full, 0);
     tc::tc_fence_after();
-    const int q = warp & 3;                 // TMEM lane quarter this warp may read
+    const int q = warp & 3;  // TMEM lane quarter this warp may read
     const int row = m0 + q * 32 + lane;
 #pragma unroll
     for (int cb = 0; cb < BN; cb += 16) {
@@ -188,6 +196,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_cons
     }
     tc::tc_fence_before();
   }
+done:
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
@@ -238,16 +247,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor [rows][cols] (row pitch = cols), box {32 cols, box_rows}
-static bool make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// 2-D fp32 tensor [rows][cols] (row pitch = cols), box {box_cols, box_rows}
+static bool make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                     uint32_t box_rows, CUtensorMapSwizzle swz) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 4};
-  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -257,6 +267,17 @@ static bool make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t
 
 using namespace jb;
 using namespace jb::mm;
+
+extern "C" jb_status jb_matmul_exact_f32(uint64_t n, uint64_t m, uint64_t l, const float *a, const float *b,
+                                         float *res, void *stream) {
+  JB_REQUIRE(n < (1ull << 31) && m < (1ull << 31) && l < (1ull << 31), "matmul: extents too large");
+  if (n == 0 || l == 0) return JB_OK;
+  JB_REQUIRE(res && (m == 0 || (a && b)), "matmul: null pointer");
+  dim3 grid((unsigned)((l + 31) / 32), (unsigned)((n + 31) / 32));
+  matmul_exact_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, b, res, (int)n, (int)l, (int)m);
+  JB_LAUNCHED("matmul_exact");
+  return JB_OK;
+}
 
 extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const float *a, const float *b,
                                    float *res, void *stream) {
@@ -270,27 +291,12 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   JB_REQUIRE(a && b, "matmul: null pointer");
   const bool tma_ok = (m % 4 == 0) && (l % 4 == 0) && ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
-                      n >= 1 && mm::encode_fn() != nullptr;
-  if (!tma_ok) {
-    dim3 grid((unsigned)((l + 31) / 32), (unsigned)((n + 31) / 32));
-    matmul_exact_kernel<<<grid, 256, 0, s>>>(a, b, res, (int)n, (int)l, (int)m);
-    JB_LAUNCHED("matmul_exact");
-    return JB_OK;
-  }
-  const size_t asz = n * m, bsz = m * l;
-  char *ws = (char *)workspace((2 * asz + 2 * bsz) * 4 + 1024, s);
-  if (!ws) return JB_ECUDA;
-  float *a_hi = (float *)ws, *a_lo = a_hi + asz, *b_hi = a_lo + asz, *b_lo = b_hi + bsz;
-  split_tf32_kernel<<<sm_count() * 4, 256, 0, s>>>((const float4 *)a, (float4 *)a_hi, (float4 *)a_lo,
-                                                   (long long)(asz / 4));
-  JB_LAUNCHED("matmul_split_a");
-  split_tf32_transpose_kernel<<<dim3((unsigned)((l + 31) / 32), (unsigned)((m + 31) / 32)), 256, 0, s>>>(
-      b, b_hi, b_lo, (int)m, (int)l);
-  JB_LAUNCHED("matmul_split_b");
+                      mm::encode_fn() != nullptr;
+  if (!tma_ok) return jb_matmul_exact_f32(n, m, l, a, b, res, stream);
 
-  CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
-  if (!make_map(&m_ahi, a_hi, n, m, BM) || !make_map(&m_alo, a_lo, n, m, BM) ||
-      !make_map(&m_bhi, b_hi, l, m, BN) || !make_map(&m_blo, b_lo, l, m, BN)) {
+  CUtensorMap m_a, m_b;
+  if (!make_map(&m_a, a, n, m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&m_b, b, m, l, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE)) {
     set_error("matmul: cuTensorMapEncodeTiled failed");
     return JB_ECUDA;
   }
@@ -304,19 +310,8 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   dim3 grid((unsigned)((l + BN - 1) / BN), (unsigned)((n + BM - 1) / BM));
   void *tok = prof_begin("matmul_tcgen05", s);
-  gemm_3xtf32_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(m_ahi, m_alo, m_bhi, m_blo, res, (int)n, (int)l, (int)m);
+  gemm_3xtf32_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(m_a, m_b, res, (int)n, (int)l, (int)m);
   prof_end(tok, s);
   JB_LAUNCHED("matmul_tcgen05");
-  return JB_OK;
-}
-
-// exact path exposed for tests and the bit-exact mode of the host API
-extern "C" JB_API jb_status jb_matmul_exact_f32(uint64_t n, uint64_t m, uint64_t l, const float *a,
-                                                const float *b, float *res, void *stream) {
-  JB_REQUIRE(n < (1ull << 31) && m < (1ull << 31) && l < (1ull << 31), "matmul: extents too large");
-  if (n == 0 || l == 0) return JB_OK;
-  dim3 grid((unsigned)((l + 31) / 32), (unsigned)((n + 31) / 32));
-  matmul_exact_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, b, res, (int)n, (int)l, (int)m);
-  JB_LAUNCHED("matmul_exact");
   return JB_OK;
 }
