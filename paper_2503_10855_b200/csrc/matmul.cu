@@ -9,13 +9,15 @@
 // B200 design: 3xTF32 on the 5th-gen tensor cores,
 //   x_hi = x rounded to tf32, x_lo = x - x_hi (exact in f32),
 //   D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi   (f32 accumulators in TMEM).
-// One kernel, one 128x64 output tile per CTA, 320 threads:
+// One kernel, one 128x128 output tile per CTA (split-K 2 when the tile
+// count is below one wave: the two partials meet in C through f32 vector
+// reductions, order independent), 320 threads:
 //   warp 0     TMA producer: raw fp32 A tile (K-major, 128B swizzle) and raw
-//              B tile ([32 k][64 n], unswizzled) per 32-wide k-block into a
-//              4-stage mbarrier ring.  Only raw operands cross L2 -> SMEM
+//              B tile ([32 k][128 n], unswizzled) per 32-wide k-block into a
+//              3-stage mbarrier ring.  Only raw operands cross L2 -> SMEM
 //              (the split is never materialised in HBM/L2).
-//   warps 2-9  converters: split the staged tile into tf32 hi/lo operands in
-//              shared memory -- A in place (same swizzled layout), B with a
+//   warps 2-9  converters: split the staged tile into a 2-stage ring of tf32
+//              hi/lo operands -- A layout-preserving, B with a
 //              transpose into the K-major 128B-swizzle layout (B's MN-major
 //              tf32 descriptor gave no result on this part, see
 //              tools/mma_probe.cu); then the epilogue (tcgen05.ld -> global).
@@ -32,23 +34,26 @@
 namespace jb {
 namespace mm {
 
-constexpr int BM = 128, BN = 64, BK = 32;  // BK fp32 = one 128-byte swizzle row
-constexpr int STAGES = 4;
-constexpr int A_TILE = BM * BK * 4;        // 16 KiB
-constexpr int B_TILE = BK * BN * 4;        // 8 KiB
+constexpr int BM = 128, BN = 128, BK = 32;  // BK fp32 = one 128-byte swizzle row
+constexpr int RAW_STAGES = 3;               // TMA ring of raw fp32 tiles
+constexpr int OP_STAGES = 2;                // converted tf32 hi/lo operand ring
+constexpr int A_TILE = BM * BK * 4;         // 16 KiB
+constexpr int B_TILE = BK * BN * 4;         // 16 KiB
 constexpr int THREADS = 320;
-constexpr int CONVERTERS = 256;            // warps 2..9 (warps 2..5 also run the epilogue)
-constexpr uint32_t TMEM_COLS = 64;
+constexpr int CONVERTERS = 256;             // warps 2..9 (warps 2..5 also run the epilogue)
+constexpr uint32_t TMEM_COLS = 128;
 
 struct Smem {
-  uint8_t a_hi[STAGES][A_TILE];  // raw A, converted in place to A_hi
-  uint8_t a_lo[STAGES][A_TILE];
-  uint8_t bt_hi[STAGES][B_TILE]; // K-major [64 n][32 k], 128B swizzle
-  uint8_t bt_lo[STAGES][B_TILE];
-  uint8_t b_raw[STAGES][B_TILE]; // [32 k][64 n] as loaded
-  uint64_t full[STAGES];         // TMA -> converters
-  uint64_t conv[STAGES];         // converters -> MMA
-  uint64_t empty[STAGES];        // MMA -> TMA
+  uint8_t a_raw[RAW_STAGES][A_TILE];  // [128 m][32 k] K-major, 128B swizzle (TMA)
+  uint8_t b_raw[RAW_STAGES][B_TILE];  // [32 k][128 n] unswizzled (TMA)
+  uint8_t a_hi[OP_STAGES][A_TILE];    // same layout as a_raw
+  uint8_t a_lo[OP_STAGES][A_TILE];
+  uint8_t bt_hi[OP_STAGES][B_TILE];   // [128 n][32 k] K-major, 128B swizzle
+  uint8_t bt_lo[OP_STAGES][B_TILE];
+  uint64_t raw_full[RAW_STAGES];      // TMA -> converters
+  uint64_t raw_empty[RAW_STAGES];     // converters -> TMA
+  uint64_t op_full[OP_STAGES];        // converters -> MMA
+  uint64_t op_empty[OP_STAGES];       // MMA -> converters
   uint64_t tmem_full;
   uint32_t tmem_base;
 };
@@ -64,6 +69,12 @@ __device__ __forceinline__ void split(float x, float &h, float &l) {
   l = x - h;
 }
 
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// grid (N/128, M/128, splitk); blockIdx.z takes k-blocks [kb0, kb1)
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    float *__restrict__ c, int M, int N, int K) {
@@ -75,12 +86,19 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int kblocks = (K + BK - 1) / BK;
+  const int splitk = gridDim.z;
+  const int kb0 = (int)((long long)kblocks * blockIdx.z / splitk);
+  const int kb1 = (int)((long long)kblocks * (blockIdx.z + 1) / splitk);
+  const int nkb = kb1 - kb0;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      tc::mbar_init(&S.full[s], 1);
-      tc::mbar_init(&S.conv[s], CONVERTERS);
-      tc::mbar_init(&S.empty[s], 1);
+    for (int s = 0; s < RAW_STAGES; s++) {
+      tc::mbar_init(&S.raw_full[s], 1);
+      tc::mbar_init(&S.raw_empty[s], CONVERTERS);
+    }
+    for (int s = 0; s < OP_STAGES; s++) {
+      tc::mbar_init(&S.op_full[s], CONVERTERS);
+      tc::mbar_init(&S.op_empty[s], 1);
     }
     tc::mbar_init(&S.tmem_full, 1);
     tc::fence_mbar_init();
@@ -96,21 +114,21 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; kb++) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) tc::mbar_wait(&S.empty[s], ((kb / STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&S.full[s], A_TILE + B_TILE);
-        const int k0 = kb * BK;
-        tc::tma_load_2d(S.a_hi[s], &tm_a, &S.full[s], k0, m0);
-        tc::tma_load_2d(S.b_raw[s], &tm_b, &S.full[s], n0, k0);
+      for (int j = 0; j < nkb; j++) {
+        const int s = j % RAW_STAGES;
+        if (j >= RAW_STAGES) tc::mbar_wait(&S.raw_empty[s], ((j / RAW_STAGES) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&S.raw_full[s], A_TILE + B_TILE);
+        const int k0 = (kb0 + j) * BK;
+        tc::tma_load_2d(S.a_raw[s], &tm_a, &S.raw_full[s], k0, m0);
+        tc::tma_load_2d(S.b_raw[s], &tm_b, &S.raw_full[s], n0, k0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 0);
-    for (int kb = 0; kb < kblocks; kb++) {
-      const int s = kb % STAGES;
-      tc::mbar_wait(&S.conv[s], (kb / STAGES) & 1);
+    for (int j = 0; j < nkb; j++) {
+      const int s = j % OP_STAGES;
+      tc::mbar_wait(&S.op_full[s], (j / OP_STAGES) & 1);
       tc::tc_fence_after();
       if (lane == 0) {
         const uint32_t ahi = tc::smem_u32(S.a_hi[s]), alo = tc::smem_u32(S.a_lo[s]);
@@ -123,74 +141,90 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
           const uint64_t da_lo = tc::smem_desc_sw128(alo + k * 32, 16, 1024);
           const uint64_t db_hi = tc::smem_desc_sw128(bhi + k * 32, 16, 1024);
           const uint64_t db_lo = tc::smem_desc_sw128(blo + k * 32, 16, 1024);
-          const uint32_t acc0 = (kb | k) != 0;
+          const uint32_t acc0 = (j | k) != 0;
           tc::mma_tf32(tmem_d, da_hi, db_hi, idesc, acc0);
           tc::mma_tf32(tmem_d, da_hi, db_lo, idesc, 1);
           tc::mma_tf32(tmem_d, da_lo, db_hi, idesc, 1);
         }
-        tc::mma_commit(&S.empty[s]);  // stage s may be refilled
-        if (kb == kblocks - 1) tc::mma_commit(&S.tmem_full);
+        tc::mma_commit(&S.op_empty[s]);  // operand slot may be rewritten
+        if (j == nkb - 1) tc::mma_commit(&S.tmem_full);
       }
       __syncwarp();
     }
   } else {
     // ------------------------------------------------------ converters
     const int ct = threadIdx.x - 64;  // 0..255
-    for (int kb = 0; kb < kblocks; kb++) {
-      const int s = kb % STAGES;
-      tc::mbar_wait(&S.full[s], (kb / STAGES) & 1);
-      // A: 1024 16-byte chunks, layout-preserving (hi in place, lo alongside)
-      float4 *ah = reinterpret_cast<float4 *>(S.a_hi[s]);
-      float4 *al = reinterpret_cast<float4 *>(S.a_lo[s]);
+    const int nn = ct & 127, cg = ct >> 7;
+    for (int j = 0; j < nkb; j++) {
+      const int rs = j % RAW_STAGES, os = j % OP_STAGES;
+      tc::mbar_wait(&S.raw_full[rs], (j / RAW_STAGES) & 1);
+      if (j >= OP_STAGES) tc::mbar_wait(&S.op_empty[os], ((j / OP_STAGES) - 1) & 1);
+      // A: 1024 16-byte chunks, layout-preserving copy into hi / lo
+      const float4 *ar = reinterpret_cast<const float4 *>(S.a_raw[rs]);
+      float4 *ah = reinterpret_cast<float4 *>(S.a_hi[os]);
+      float4 *al = reinterpret_cast<float4 *>(S.a_lo[os]);
 #pragma unroll
       for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++) {
         const int q = ct + i * CONVERTERS;
-        float4 v = ah[q], h, l;
+        const float4 v = ar[q];
+        float4 h, l;
         split(v.x, h.x, l.x); split(v.y, h.y, l.y); split(v.z, h.z, l.z); split(v.w, h.w, l.w);
         ah[q] = h;
         al[q] = l;
       }
-      // B: raw [32 k][64 n] -> Bt [64 n][32 k], K-major with the 128B swizzle
+      // B: raw [32 k][128 n] -> Bt [128 n][32 k], K-major with the 128B swizzle
       // (16-byte chunk c of row n stored at chunk c ^ (n & 7))
-      const float *br = reinterpret_cast<const float *>(S.b_raw[s]);
-      const int nn = ct & 63, cg = ct >> 6;  // 4 groups of 2 k-chunks
+      const float *br = reinterpret_cast<const float *>(S.b_raw[rs]);
 #pragma unroll
-      for (int i = 0; i < 2; i++) {
-        const int cch = cg * 2 + i;  // k chunk: k = 4*cch .. 4*cch+3
+      for (int i = 0; i < 4; i++) {
+        const int cch = cg * 4 + i;  // k chunk: k = 4*cch .. 4*cch+3
         float4 h, l;
         split(br[(4 * cch + 0) * BN + nn], h.x, l.x);
         split(br[(4 * cch + 1) * BN + nn], h.y, l.y);
         split(br[(4 * cch + 2) * BN + nn], h.z, l.z);
         split(br[(4 * cch + 3) * BN + nn], h.w, l.w);
         const int off = nn * 128 + ((cch ^ (nn & 7)) << 4);
-        *reinterpret_cast<float4 *>(S.bt_hi[s] + off) = h;
-        *reinterpret_cast<float4 *>(S.bt_lo[s] + off) = l;
+        *reinterpret_cast<float4 *>(S.bt_hi[os] + off) = h;
+        *reinterpret_cast<float4 *>(S.bt_lo[os] + off) = l;
       }
       tc::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
-      tc::mbar_arrive(&S.conv[s]);
+      tc::mbar_arrive(&S.raw_empty[rs]);
+      tc::mbar_arrive(&S.op_full[os]);
     }
     // ------------------------------------------------------ epilogue
-    if (warp >= 6) goto done;  // four warps cover the 128 TMEM lanes
+    if (warp >= 6 || nkb == 0) goto done;  // four warps cover the 128 TMEM lanes
     tc::mbar_wait(&S.tmem_full, 0);
     tc::tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may read
-    const int row = m0 + q * 32 + lane;
+    {
+      const int q = warp & 3;  // TMEM lane quarter this warp may read
+      const int row = m0 + q * 32 + lane;
+      const bool vec = (N & 3) == 0;
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 16) {
+        uint32_t r[16];
+        tc::tmem_ld_32x32b_x16(tmem_d + ((uint32_t)(q * 32) << 16) + cb, r);
+        tc::tmem_ld_wait();
+        if (row < M) {
+          float *dst = c + (size_t)row * N + n0 + cb;
+          if (n0 + cb + 16 <= N && vec) {
 #pragma unroll
-    for (int cb = 0; cb < BN; cb += 16) {
-      uint32_t r[16];
-      tc::tmem_ld_32x32b_x16(tmem_d + ((uint32_t)(q * 32) << 16) + cb, r);
-      tc::tmem_ld_wait();
-      if (row < M) {
-        float *dst = c + (size_t)row * N + n0 + cb;
-        if (n0 + cb + 16 <= N && (N & 3) == 0) {
-#pragma unroll
-          for (int v = 0; v < 4; v++)
-            reinterpret_cast<float4 *>(dst)[v] =
-                make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                            __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-        } else {
-          for (int v = 0; v < 16; v++)
-            if (n0 + cb + v < N) dst[v] = __uint_as_float(r[v]);
+            for (int v = 0; v < 4; v++) {
+              const float a0 = __uint_as_float(r[4 * v]), a1 = __uint_as_float(r[4 * v + 1]);
+              const float a2 = __uint_as_float(r[4 * v + 2]), a3 = __uint_as_float(r[4 * v + 3]);
+              if (splitk > 1)
+                red_add_v4(dst + 4 * v, a0, a1, a2, a3);
+              else
+                reinterpret_cast<float4 *>(dst)[v] = make_float4(a0, a1, a2, a3);
+            }
+          } else {
+            for (int v = 0; v < 16; v++)
+              if (n0 + cb + v < N) {
+                if (splitk > 1)
+                  atomicAdd(dst + v, __uint_as_float(r[v]));
+                else
+                  dst[v] = __uint_as_float(r[v]);
+              }
+          }
         }
       }
     }
@@ -308,7 +342,14 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
                                        (int)SMEM_BYTES));
     attr_set[dev] = true;
   }
-  dim3 grid((unsigned)((l + BN - 1) / BN), (unsigned)((n + BM - 1) / BM));
+  const long long tiles = (long long)((l + BN - 1) / BN) * (long long)((n + BM - 1) / BM);
+  const int kblocks = (int)((m + BK - 1) / BK);
+  // split K so that at least ~one CTA per SM runs; the partial tiles meet in
+  // C through f32 vector reductions (2 addends: order independent)
+  int splitk = 1;
+  while (splitk < 4 && tiles * splitk * 2 <= sm_count() && kblocks >= splitk * 2 * 4) splitk *= 2;
+  if (splitk > 1) JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
+  dim3 grid((unsigned)((l + BN - 1) / BN), (unsigned)((n + BM - 1) / BM), (unsigned)splitk);
   void *tok = prof_begin("matmul_tcgen05", s);
   gemm_3xtf32_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(m_a, m_b, res, (int)n, (int)l, (int)m);
   prof_end(tok, s);
