@@ -7,20 +7,21 @@
 //     |C - C_ref| <= (2*gamma_m + 8u) * (|A| |B|)   elementwise, u = 2^-24.
 //
 // B200 design: 3xTF32 on the 5th-gen tensor cores,
-//   x_hi = x rounded to tf32, x_lo = x - x_hi (exact in f32),
+//   x_hi = trunc_tf32(x) (what kind::tf32 reads from an f32 container),
+//   x_lo = x - x_hi (exact in f32),
 //   D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi   (f32 accumulators in TMEM).
 // One kernel, one 128x128 output tile per CTA (split-K 2 when the tile
 // count is below one wave: the two partials meet in C through f32 vector
 // reductions, order independent), 320 threads:
 //   warp 0     TMA producer: raw fp32 A tile (K-major, 128B swizzle) and raw
-//              B tile ([32 k][128 n], unswizzled) per 32-wide k-block into a
-//              3-stage mbarrier ring.  Only raw operands cross L2 -> SMEM
-//              (the split is never materialised in HBM/L2).
-//   warps 2-9  converters: split the staged tile into a 2-stage ring of tf32
-//              hi/lo operands -- A layout-preserving, B with a
-//              transpose into the K-major 128B-swizzle layout (B's MN-major
-//              tf32 descriptor gave no result on this part, see
-//              tools/mma_probe.cu); then the epilogue (tcgen05.ld -> global).
+//              B tile (MN-major, 128B swizzle with 32-byte atoms = UMMA
+//              layout SWIZZLE_128B_BASE32B) per 32-wide k-block into a
+//              4-stage mbarrier ring.  Only raw operands cross L2 -> SMEM;
+//              the raw tiles ARE the hi operands (the tensor core truncates
+//              the 13 low bits, verified by tools/mma_probe.cu).
+//   warps 2-9  converters: lo = x - trunc(x) into a 2-slot ring, elementwise in the same
+//              swizzled layouts (no transpose), then the epilogue
+//              (tcgen05.ld -> global, f32x4 reductions under split-K).
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer.
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
@@ -35,8 +36,8 @@ namespace jb {
 namespace mm {
 
 constexpr int BM = 128, BN = 128, BK = 32;  // BK fp32 = one 128-byte swizzle row
-constexpr int RAW_STAGES = 3;               // TMA ring of raw fp32 tiles
-constexpr int OP_STAGES = 2;                // converted tf32 hi/lo operand ring
+constexpr int STAGES = 4;                   // raw tiles (TMA ring, also the hi operands)
+constexpr int LO_STAGES = 2;                // converted lo operands
 constexpr int A_TILE = BM * BK * 4;         // 16 KiB
 constexpr int B_TILE = BK * BN * 4;         // 16 KiB
 constexpr int THREADS = 320;
@@ -44,34 +45,37 @@ constexpr int CONVERTERS = 256;             // warps 2..9 (warps 2..5 also run t
 constexpr uint32_t TMEM_COLS = 128;
 
 struct Smem {
-  uint8_t a_raw[RAW_STAGES][A_TILE];  // [128 m][32 k] K-major, 128B swizzle (TMA)
-  uint8_t b_raw[RAW_STAGES][B_TILE];  // [32 k][128 n] unswizzled (TMA)
-  uint8_t a_hi[OP_STAGES][A_TILE];    // same layout as a_raw
-  uint8_t a_lo[OP_STAGES][A_TILE];
-  uint8_t bt_hi[OP_STAGES][B_TILE];   // [128 n][32 k] K-major, 128B swizzle
-  uint8_t bt_lo[OP_STAGES][B_TILE];
-  uint64_t raw_full[RAW_STAGES];      // TMA -> converters
-  uint64_t raw_empty[RAW_STAGES];     // converters -> TMA
-  uint64_t op_full[OP_STAGES];        // converters -> MMA
-  uint64_t op_empty[OP_STAGES];       // MMA -> converters
+  // raw fp32 tiles straight from TMA; the tensor core reads them as the tf32
+  // "hi" operands (it ignores the 13 low mantissa bits, tools/mma_probe.cu)
+  uint8_t a_raw[STAGES][A_TILE];  // [128 m][32 k] K-major, 128B swizzle
+  uint8_t b_raw[STAGES][B_TILE];  // 4 MN atoms x [32 k][32 n], 128B swizzle / 32B atoms
+  uint8_t a_lo[LO_STAGES][A_TILE];  // x - trunc_tf32(x), same layouts
+  uint8_t b_lo[LO_STAGES][B_TILE];
+  uint64_t full[STAGES];            // TMA -> converters
+  uint64_t empty[STAGES];           // MMA -> TMA (raw slot free)
+  uint64_t conv[LO_STAGES];         // converters -> MMA
+  uint64_t lo_empty[LO_STAGES];     // MMA -> converters (lo slot free)
   uint64_t tmem_full;
   uint32_t tmem_base;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + manual 1 KiB alignment
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
-// x_hi = x rounded to the nearest tf32 (ties away from zero: add half an
-// ulp of tf32 to the magnitude bits, clear the 13 low bits -- two integer
-// ops instead of cvt.rna.tf32.f32, which ptxas expands to ~8); x_lo = x - x_hi
-// is exact in f32 and the tensor core reads its leading 11 bits.
-__device__ __forceinline__ void split(float x, float &h, float &l) {
-  h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-  l = x - h;
+// residual of the tensor core's tf32 truncation: exact in f32
+__device__ __forceinline__ float tf32_residual(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
+}
+
+// MN-major B descriptor: 128B swizzle with 32-byte atoms (layout type 1),
+// 32-column MN atoms B_TILE/4 apart (LBO), 4-row K groups 512 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_b_mn(uint32_t saddr) {
+  const uint64_t d = tc::smem_desc_sw128(saddr, B_TILE / 4, 512);
+  return (d & ~(7ull << 61)) | (1ull << 61);
 }
 
 // grid (N/128, M/128, splitk); blockIdx.z takes k-blocks [kb0, kb1)
@@ -92,13 +96,13 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   const int nkb = kb1 - kb0;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < RAW_STAGES; s++) {
-      tc::mbar_init(&S.raw_full[s], 1);
-      tc::mbar_init(&S.raw_empty[s], CONVERTERS);
+    for (int s = 0; s < STAGES; s++) {
+      tc::mbar_init(&S.full[s], 1);
+      tc::mbar_init(&S.empty[s], 1);
     }
-    for (int s = 0; s < OP_STAGES; s++) {
-      tc::mbar_init(&S.op_full[s], CONVERTERS);
-      tc::mbar_init(&S.op_empty[s], 1);
+    for (int s = 0; s < LO_STAGES; s++) {
+      tc::mbar_init(&S.conv[s], CONVERTERS);
+      tc::mbar_init(&S.lo_empty[s], 1);
     }
     tc::mbar_init(&S.tmem_full, 1);
     tc::fence_mbar_init();
@@ -115,38 +119,42 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
       for (int j = 0; j < nkb; j++) {
-        const int s = j % RAW_STAGES;
-        if (j >= RAW_STAGES) tc::mbar_wait(&S.raw_empty[s], ((j / RAW_STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&S.raw_full[s], A_TILE + B_TILE);
+        const int s = j % STAGES;
+        if (j >= STAGES) tc::mbar_wait(&S.empty[s], ((j / STAGES) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&S.full[s], A_TILE + B_TILE);
         const int k0 = (kb0 + j) * BK;
-        tc::tma_load_2d(S.a_raw[s], &tm_a, &S.raw_full[s], k0, m0);
-        tc::tma_load_2d(S.b_raw[s], &tm_b, &S.raw_full[s], n0, k0);
+        tc::tma_load_2d(S.a_raw[s], &tm_a, &S.full[s], k0, m0);
+#pragma unroll
+        for (int at = 0; at < BN / 32; at++)
+          tc::tma_load_2d(S.b_raw[s] + at * (B_TILE / 4), &tm_b, &S.full[s], n0 + 32 * at, k0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 0);
+    constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 1);
     for (int j = 0; j < nkb; j++) {
-      const int s = j % OP_STAGES;
-      tc::mbar_wait(&S.op_full[s], (j / OP_STAGES) & 1);
+      const int s = j % STAGES, ls = j % LO_STAGES;
+      tc::mbar_wait(&S.conv[ls], (j / LO_STAGES) & 1);
       tc::tc_fence_after();
       if (lane == 0) {
-        const uint32_t ahi = tc::smem_u32(S.a_hi[s]), alo = tc::smem_u32(S.a_lo[s]);
-        const uint32_t bhi = tc::smem_u32(S.bt_hi[s]), blo = tc::smem_u32(S.bt_lo[s]);
+        const uint32_t ahi = tc::smem_u32(S.a_raw[s]), alo = tc::smem_u32(S.a_lo[ls]);
+        const uint32_t bhi = tc::smem_u32(S.b_raw[s]), blo = tc::smem_u32(S.b_lo[ls]);
 #pragma unroll
         for (int k = 0; k < BK / 8; k++) {
-          // K-major, 128B rows, 8-row atoms of 1 KiB -> SBO = 1024; one MMA
-          // consumes 8 fp32 of K = 32 bytes of each row.
+          // A: K-major, 128B rows in 1 KiB 8-row atoms (SBO 1024), one MMA
+          //    consumes 32 bytes of each row.  B: MN-major, one MMA consumes
+          //    8 K-rows = 1 KiB of every MN atom.
           const uint64_t da_hi = tc::smem_desc_sw128(ahi + k * 32, 16, 1024);
           const uint64_t da_lo = tc::smem_desc_sw128(alo + k * 32, 16, 1024);
-          const uint64_t db_hi = tc::smem_desc_sw128(bhi + k * 32, 16, 1024);
-          const uint64_t db_lo = tc::smem_desc_sw128(blo + k * 32, 16, 1024);
+          const uint64_t db_hi = desc_b_mn(bhi + k * 1024);
+          const uint64_t db_lo = desc_b_mn(blo + k * 1024);
           const uint32_t acc0 = (j | k) != 0;
           tc::mma_tf32(tmem_d, da_hi, db_hi, idesc, acc0);
           tc::mma_tf32(tmem_d, da_hi, db_lo, idesc, 1);
           tc::mma_tf32(tmem_d, da_lo, db_hi, idesc, 1);
         }
-        tc::mma_commit(&S.op_empty[s]);  // operand slot may be rewritten
+        tc::mma_commit(&S.empty[s]);      // raw slot may be refilled by TMA
+        tc::mma_commit(&S.lo_empty[ls]);  // lo slot may be rewritten
         if (j == nkb - 1) tc::mma_commit(&S.tmem_full);
       }
       __syncwarp();
@@ -154,42 +162,30 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   } else {
     // ------------------------------------------------------ converters
     const int ct = threadIdx.x - 64;  // 0..255
-    const int nn = ct & 127, cg = ct >> 7;
     for (int j = 0; j < nkb; j++) {
-      const int rs = j % RAW_STAGES, os = j % OP_STAGES;
-      tc::mbar_wait(&S.raw_full[rs], (j / RAW_STAGES) & 1);
-      if (j >= OP_STAGES) tc::mbar_wait(&S.op_empty[os], ((j / OP_STAGES) - 1) & 1);
-      // A: 1024 16-byte chunks, layout-preserving copy into hi / lo
-      const float4 *ar = reinterpret_cast<const float4 *>(S.a_raw[rs]);
-      float4 *ah = reinterpret_cast<float4 *>(S.a_hi[os]);
-      float4 *al = reinterpret_cast<float4 *>(S.a_lo[os]);
+      const int s = j % STAGES, ls = j % LO_STAGES;
+      tc::mbar_wait(&S.full[s], (j / STAGES) & 1);
+      if (j >= LO_STAGES) tc::mbar_wait(&S.lo_empty[ls], ((j / LO_STAGES) - 1) & 1);
+      // elementwise, layout preserving: lo = x - trunc_tf32(x) for A and B
+      const float4 *ar = reinterpret_cast<const float4 *>(S.a_raw[s]);
+      const float4 *br = reinterpret_cast<const float4 *>(S.b_raw[s]);
+      float4 *al = reinterpret_cast<float4 *>(S.a_lo[ls]);
+      float4 *bl = reinterpret_cast<float4 *>(S.b_lo[ls]);
+      float4 va[A_TILE / 16 / CONVERTERS], vb[B_TILE / 16 / CONVERTERS];
 #pragma unroll
-      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++) {
-        const int q = ct + i * CONVERTERS;
-        const float4 v = ar[q];
-        float4 h, l;
-        split(v.x, h.x, l.x); split(v.y, h.y, l.y); split(v.z, h.z, l.z); split(v.w, h.w, l.w);
-        ah[q] = h;
-        al[q] = l;
-      }
-      // B: raw [32 k][128 n] -> Bt [128 n][32 k], K-major with the 128B swizzle
-      // (16-byte chunk c of row n stored at chunk c ^ (n & 7))
-      const float *br = reinterpret_cast<const float *>(S.b_raw[rs]);
+      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++) va[i] = ar[ct + i * CONVERTERS];
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int cch = cg * 4 + i;  // k chunk: k = 4*cch .. 4*cch+3
-        float4 h, l;
-        split(br[(4 * cch + 0) * BN + nn], h.x, l.x);
-        split(br[(4 * cch + 1) * BN + nn], h.y, l.y);
-        split(br[(4 * cch + 2) * BN + nn], h.z, l.z);
-        split(br[(4 * cch + 3) * BN + nn], h.w, l.w);
-        const int off = nn * 128 + ((cch ^ (nn & 7)) << 4);
-        *reinterpret_cast<float4 *>(S.bt_hi[os] + off) = h;
-        *reinterpret_cast<float4 *>(S.bt_lo[os] + off) = l;
-      }
+      for (int i = 0; i < B_TILE / 16 / CONVERTERS; i++) vb[i] = br[ct + i * CONVERTERS];
+#pragma unroll
+      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++)
+        al[ct + i * CONVERTERS] = make_float4(tf32_residual(va[i].x), tf32_residual(va[i].y),
+                                              tf32_residual(va[i].z), tf32_residual(va[i].w));
+#pragma unroll
+      for (int i = 0; i < B_TILE / 16 / CONVERTERS; i++)
+        bl[ct + i * CONVERTERS] = make_float4(tf32_residual(vb[i].x), tf32_residual(vb[i].y),
+                                              tf32_residual(vb[i].z), tf32_residual(vb[i].w));
       tc::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
-      tc::mbar_arrive(&S.raw_empty[rs]);
-      tc::mbar_arrive(&S.op_full[os]);
+      tc::mbar_arrive(&S.conv[ls]);
     }
     // ------------------------------------------------------ epilogue
     if (warp >= 6 || nkb == 0) goto done;  // four warps cover the 128 TMEM lanes
@@ -330,7 +326,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
 
   CUtensorMap m_a, m_b;
   if (!make_map(&m_a, a, n, m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&m_b, b, m, l, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      !make_map(&m_b, b, m, l, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
     set_error("matmul: cuTensorMapEncodeTiled failed");
     return JB_ECUDA;
   }

@@ -5,6 +5,8 @@
 using namespace jb;
 
 // mode bit0: B K-major (else MN-major); bit1: use 4 k-steps (K=32) else 1 (K=8)
+// bit2: swap LBO/SBO for MN-major; bit3: MN-major with SWIZZLE_128B_BASE32B
+// (layout type 1: 32-byte chunks XOR (row & 3), 4-row K groups)
 __global__ void probe(const float* A, const float* B, float* C, float* dbg, int mode) {
   __shared__ __align__(1024) uint8_t sa[128 * 128];
   __shared__ __align__(1024) uint8_t sb[64 * 128];
@@ -24,6 +26,9 @@ __global__ void probe(const float* A, const float* B, float* C, float* dbg, int 
     int off;
     if (bk) {  // K-major: row = n (64 rows of 128B), chunk by k
       off = nn * 128 + (((k >> 2) ^ (nn & 7)) << 4) + (k & 3) * 4;
+    } else if (mode & 8) {  // MN-major BASE32B: 32B chunk (c>>3) ^ (k&3)
+      int a = nn >> 5, c = nn & 31;
+      off = a * 4096 + k * 128 + (((c >> 3) ^ (k & 3)) << 5) + (c & 7) * 4;
     } else {   // MN-major: atom = nn/32 at 4096*atom, row = k
       int a = nn >> 5, c = nn & 31;
       off = a * 4096 + k * 128 + (((c >> 2) ^ (k & 7)) << 4) + (c & 3) * 4;
@@ -45,6 +50,11 @@ __global__ void probe(const float* A, const float* B, float* C, float* dbg, int 
       uint64_t db = bk ? tc::smem_desc_sw128(tc::smem_u32(sb) + k * 32, 16, 1024)
                        : ((mode & 4) ? tc::smem_desc_sw128(tc::smem_u32(sb) + k * 1024, 1024, 4096)
                                      : tc::smem_desc_sw128(tc::smem_u32(sb) + k * 1024, 4096, 1024));
+      if (!bk && (mode & 8)) {
+        db = (mode & 4) ? tc::smem_desc_sw128(tc::smem_u32(sb) + k * 1024, 512, 4096)
+                        : tc::smem_desc_sw128(tc::smem_u32(sb) + k * 1024, 4096, 512);
+        db = (db & ~(7ull << 61)) | (1ull << 61);  // layout type 1 = SWIZZLE_128B_BASE32B
+      }
       if (k == 0) { dbg[0] = __uint_as_float((uint32_t)da); dbg[1] = __uint_as_float((uint32_t)(da >> 32));
                     dbg[2] = __uint_as_float((uint32_t)db); dbg[3] = __uint_as_float((uint32_t)(db >> 32));
                     dbg[4] = __uint_as_float(idesc); dbg[5] = __uint_as_float(td); }
