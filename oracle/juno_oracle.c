@@ -735,3 +735,28 @@ EXPORT void jo_bp_train(int64_t n_in, int64_t n_hid, int64_t n_out,
   jo_bp_adjust_weights(delta_o, n_out, hidden, n_hid, hid_w, hid_prev_w);
   jo_bp_adjust_weights(delta_h, n_hid, input, n_in, in_w, in_prev_w);
 }
+
+/* ---- SRAD row-slab helpers (multi-rank tests of dist.py) ---------------- */
+EXPORT void jo_srad_extract(int64_t n, const float *image, float *J, int compress) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < n; k++) {
+    const float j = exp_ref(image[k] / 255.0f);
+    J[k] = compress ? log_ref(j) * 255.0f : j;
+  }
+}
+
+EXPORT void jo_srad_sums(int64_t n, const float *J, double *out) {
+  double sum = 0.0, sum2 = 0.0;
+  for (int64_t k = 0; k < n; k++) {
+    const double t = (double)J[k];
+    sum += t;
+    sum2 += t * t;
+  }
+  out[0] = sum;
+  out[1] = sum2;
+}
+
+EXPORT void jo_srad_compress(int64_t n, const float *J, float *out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < n; k++) out[k] = log_ref(J[k]) * 255.0f;
+}

@@ -289,3 +289,25 @@ def cava_stage(name: str, *arrays, P: int = 0):
         L.jo_cava_tonemap_descale(_i64(N), _p(x, _f32p), _p(tm, _f32p), _p(out, _u8p))
         return out
     raise ValueError(name)
+
+
+# -- SRAD slab helpers (tests of paper_2503_10855_b200.dist) -------------------
+def srad_extract(image, compress=False) -> np.ndarray:
+    img = _f32(image)
+    out = np.empty_like(img)
+    lib().jo_srad_extract(_i64(img.size), _p(img, _f32p), _p(out, _f32p), ctypes.c_int(int(compress)))
+    return out
+
+
+def srad_sums(J) -> np.ndarray:
+    J = _f32(J)
+    out = np.zeros(2, np.float64)
+    lib().jo_srad_sums(_i64(J.size), _p(J, _f32p), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+def srad_compress(J) -> np.ndarray:
+    J = _f32(J)
+    out = np.empty_like(J)
+    lib().jo_srad_compress(_i64(J.size), _p(J, _f32p), _p(out, _f32p))
+    return out

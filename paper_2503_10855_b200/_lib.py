@@ -37,6 +37,9 @@ SIGNATURES = {
                            _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_cava_u8": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_srad_f32": [_u64, _u64, _u64, _f32, _vp, _vp, _vp, _vp],
+    "jb_srad_extract_f32": [_u64, _vp, _vp, _vp, ctypes.c_int, _vp],
+    "jb_srad_slab_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, _vp, ctypes.c_int, _vp],
+    "jb_srad_q0_f32": [_vp, _u64, _vp, _vp],
     "jb_euler_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_euler_step_factor_f32": [_u64, _vp, _vp, _vp, _vp],
     "jb_euler_flux_f32": [_u64, _vp, _vp, _vp, _vp, _vp, _vp],

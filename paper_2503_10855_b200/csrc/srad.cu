@@ -49,8 +49,10 @@ struct Args {
   Stats *partials;    // [gridDim.x]
   unsigned *ticket;
   int rows, cols, tiles_x, tiles;
+  int row_lo, row_hi; // output rows [row_lo, row_hi) of src (slab mode: the rest is halo)
   float ql;           // 0.25f * lambda
   int compress;       // write log(J')*255 instead of J'
+  double *sums_out;   // slab mode: the last CTA writes (sum, sum2) here instead of q0
 };
 
 __device__ __forceinline__ void block_stats(double s, double s2, Stats *out) {
@@ -87,9 +89,14 @@ __device__ void finish_stats(const Args &a, long long npx) {
     s = warp_sum(s);
     s2 = warp_sum(s2);
     if (threadIdx.x == 0) {
-      const double mean = s / (double)npx;
-      const double var = s2 / (double)npx - mean * mean;
-      *a.q0_next = (float)(var / (mean * mean));
+      if (a.sums_out) {  // multi-GPU slab: the q0 comes after the allreduce
+        a.sums_out[0] = s;
+        a.sums_out[1] = s2;
+      } else {
+        const double mean = s / (double)npx;
+        const double var = s2 / (double)npx - mean * mean;
+        *a.q0_next = (float)(var / (mean * mean));
+      }
       *a.ticket = 0;  // ready for the next launch (stream order)
     }
   }
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
 
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
     const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
-    const int y0 = ty * TH, x0 = tx * TW;
+    const int y0 = a.row_lo + ty * TH, x0 = tx * TW;
     // ---- J tile with replicated halo: rows y0-1..y0+TH+1, cols x0-1..x0+TW+1.
     // warp w loads rows w, w+8, ...; lane l loads cols l, l+32, ... (loads first)
     {
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
 #pragma unroll
     for (int k = 0; k < TH / 8; k++) {
       const int r = warp * (TH / 8) + k, gy = y0 + r;
-      if (gy >= rows) break;
+      if (gy >= a.row_hi) break;
       const int jr = r + 1;
 #pragma unroll
       for (int q = 0; q < TW / 32; q++) {
@@ -215,10 +222,11 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
           const float cN = S.c[r][cc], cS = S.c[r + 1][cc], cE = S.c[r][cc + 1];
           const float D = add_rn(add_rn(add_rn(mul_rn(cN, n_), mul_rn(cS, s_)), mul_rn(cN, w_)), mul_rn(cE, e_));
           const float jn = add_rn(Jc, mul_rn(a.ql, D));
+          const size_t o = (size_t)(gy - a.row_lo) * cols + gx;
           if (a.compress) {
-            a.dst[(size_t)gy * cols + gx] = mul_rn(log_ref(jn), 255.0f);
+            a.dst[o] = mul_rn(log_ref(jn), 255.0f);
           } else {
-            a.dst[(size_t)gy * cols + gx] = jn;
+            a.dst[o] = jn;
             s += (double)jn;
             s2 += (double)jn * (double)jn;
           }
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
   }
   if (a.compress) return;
   block_stats(s, s2, a.partials + blockIdx.x);
-  finish_stats(a, (long long)rows * cols);
+  finish_stats(a, (long long)(a.row_hi - a.row_lo) * cols);
 }
 
 __global__ void copy_q0_kernel(const float *q0, float *out, int n) {
@@ -272,6 +280,7 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
 
   Args a{};
   a.rows = (int)rows; a.cols = (int)cols; a.tiles_x = tiles_x; a.tiles = tiles;
+  a.row_lo = 0; a.row_hi = (int)rows; a.sums_out = nullptr;
   a.ql = 0.25f * lambda;  // one IEEE multiply, as in the oracle
   a.partials = parts; a.ticket = ticket;
   // extract (+ stats of J0), or extract+compress when niter == 0
@@ -298,5 +307,78 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
     copy_q0_kernel<<<1, 256, 0, s>>>(q0, q0sqr, (int)niter);
     JB_LAUNCHED("srad_q0_copy");
   }
+  return JB_OK;
+}
+
+// ------------------------------------------------------------ slab entries
+// Multi-GPU row slabs (paper_2503_10855_b200/dist.py): each rank owns rows
+// [own_lo, own_hi) of an extended slab that carries 1 halo row above and 2
+// below (fewer at the image edges); the host exchanges halos and allreduces
+// the f64 sums between iterations, then jb_srad_q0_f32 turns them into q0^2.
+
+__global__ void srad_q0_kernel(const double *sums, double npx, float *q0) {
+  const double mean = sums[0] / npx;
+  const double var = sums[1] / npx - mean * mean;
+  *q0 = (float)(var / (mean * mean));
+}
+
+extern "C" jb_status jb_srad_extract_f32(uint64_t n, const float *image, float *J, double *sums,
+                                         int compress, void *stream) {
+  JB_REQUIRE(n >= 1 && n < (1ull << 40), "srad_extract: bad size");
+  JB_REQUIRE(image && J, "srad_extract: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = sm_count() * 8;
+  char *ws = (char *)workspace(((grid * sizeof(Stats) + 255) / 256) * 256 + 256, s);
+  if (!ws) return JB_ECUDA;
+  Args a{};
+  a.src = image; a.dst = J; a.rows = 1; a.cols = (int)n;
+  a.partials = (Stats *)ws;
+  a.ticket = (unsigned *)(ws + ((grid * sizeof(Stats) + 255) / 256) * 256);
+  a.compress = compress;
+  a.sums_out = sums;
+  a.q0_next = nullptr;
+  JB_CHECK_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s));
+  // extract kernel indexes rows*cols elements as a flat array
+  a.rows = 1;
+  srad_extract_kernel<<<grid, THREADS, 0, s>>>(a);
+  JB_LAUNCHED("srad_extract");
+  return JB_OK;
+}
+
+extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uint64_t own_lo, uint64_t own_hi,
+                                           const float *J_ext, float *out_own, const float *q0, float lambda,
+                                           double *sums, int compress, void *stream) {
+  JB_REQUIRE(rows_ext >= 1 && cols >= 1 && own_lo < own_hi && own_hi <= rows_ext, "srad_slab: bad slab");
+  JB_REQUIRE(J_ext && out_own && q0, "srad_slab: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int tiles_x = (int)((cols + TW - 1) / TW), tiles_y = (int)((own_hi - own_lo + TH - 1) / TH);
+  const int tiles = tiles_x * tiles_y;
+  int per_sm = 0;
+  JB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_iter_kernel, THREADS, 0));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = tiles < sm_count() * per_sm ? tiles : sm_count() * per_sm;
+  const size_t pb = ((grid * sizeof(Stats) + 255) / 256) * 256;
+  char *ws = (char *)workspace(pb + 256, s);
+  if (!ws) return JB_ECUDA;
+  Args a{};
+  a.src = J_ext; a.dst = out_own; a.q0 = q0; a.q0_next = nullptr;
+  a.partials = (Stats *)ws; a.ticket = (unsigned *)(ws + pb);
+  a.rows = (int)rows_ext; a.cols = (int)cols; a.tiles_x = tiles_x; a.tiles = tiles;
+  a.row_lo = (int)own_lo; a.row_hi = (int)own_hi;
+  a.ql = 0.25f * lambda;
+  a.compress = compress;
+  a.sums_out = sums;
+  JB_CHECK_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s));
+  void *tok = prof_begin("srad_iter", s);
+  srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
+  prof_end(tok, s);
+  JB_LAUNCHED("srad_slab_step");
+  return JB_OK;
+}
+
+extern "C" jb_status jb_srad_q0_f32(const double *sums, uint64_t npx_global, float *q0, void *stream) {
+  JB_REQUIRE(sums && q0 && npx_global >= 1, "srad_q0: bad arguments");
+  srad_q0_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sums, (double)npx_global, q0);
+  JB_LAUNCHED("srad_q0");
   return JB_OK;
 }

@@ -1,0 +1,141 @@
+"""Multi-rank host logic (paper_2503_10855_b200.dist) on CPU with gloo,
+world_size 2 and 3: the same slab/halo/allreduce driver the GPU path runs,
+with the oracle restatement as the per-slab compute (test-only backend)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2503_10855_b200 import dist as D
+
+
+def test_partition_covers_exactly():
+    for n in (1, 7, 256, 1000):
+        for w in (1, 2, 3, 8):
+            spans = [D.partition(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0
+            assert sum(c for _, c in spans) == n
+            for (a, ca), (b, _) in zip(spans, spans[1:]):
+                assert a + ca == b
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+
+
+def test_srad_slab_plan_halos():
+    p = D.srad_slab(100, 4, 0)
+    assert (p["r0"], p["e0"], p["own_lo"]) == (0, 0, 0) and p["e1"] == p["r1"] + 2
+    p = D.srad_slab(100, 4, 3)
+    assert p["e1"] == 100 and p["e0"] == p["r0"] - 1 and p["own_lo"] == 1
+    with pytest.raises(ValueError):
+        D.srad_slab(5, 4, 0)
+
+
+class OracleSradBackend:
+    """CPU stand-in for CudaSradBackend built on the C restatement."""
+
+    def __init__(self):
+        from oracle import oracle
+        self.o = oracle
+
+    def extract(self, image_own, compress):
+        a = image_own.numpy()
+        J = self.o.srad_extract(a, compress=compress)
+        return torch.from_numpy(J), torch.from_numpy(self.o.srad_sums(J))
+
+    def step(self, J_ext, own_lo, own_hi, q0, lam, compress):
+        J = self.o.srad_iter(J_ext.numpy(), float(q0.item()), float(lam))[own_lo:own_hi]
+        if compress:
+            return torch.from_numpy(self.o.srad_compress(J)), torch.zeros(2, dtype=torch.float64)
+        return torch.from_numpy(np.ascontiguousarray(J)), torch.from_numpy(self.o.srad_sums(J))
+
+    def q0(self, sums, npx):
+        s, s2 = float(sums[0]), float(sums[1])
+        mean = s / npx
+        var = s2 / npx - mean * mean
+        return torch.tensor([np.float32(var / (mean * mean))])
+
+    def cat_rows(self, parts):
+        return torch.cat(parts, dim=0).contiguous()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, fn):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        if isinstance(v, Exception):
+            raise v
+    return [out[r] for r in range(world)]
+
+
+ROWS, COLS, NITER = 41, 23, 4
+
+
+def _srad_rank(rank, world):
+    from paper_2503_10855_b200 import workloads as W
+    img = W.srad_image(ROWS, COLS, seed=5)
+    plan = D.srad_slab(ROWS, world, rank)
+    own = torch.from_numpy(np.ascontiguousarray(img[plan["r0"]:plan["r1"]]))
+    return D.srad_distributed(own, NITER, 0.5, ROWS, COLS, OracleSradBackend()).numpy()
+
+
+def _frames_rank(rank, world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    g, st, sx, sy, th = W.edge_filters()
+    batch = W.edge_batch(5, 30, 44, seed=3, distinct=5)
+    f0, cnt = D.shard_frames(5, world, rank)
+    out = torch.from_numpy(oracle.edge(batch[f0:f0 + cnt], g, st, sx, sy, th))
+    sizes = [D.shard_frames(5, world, r)[1] for r in range(world)]
+    # uneven shards: gather through a padded buffer
+    pad = torch.zeros((max(sizes), 30, 44))
+    pad[:cnt] = out
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    return torch.cat([b[:s] for b, s in zip(bufs, sizes)]).numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_srad_row_slabs_match_single_device(world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    parts = _run(world, _srad_rank)
+    got = np.concatenate(parts)
+    ref = oracle.srad(W.srad_image(ROWS, COLS, seed=5), NITER, 0.5)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+def test_frame_sharding_gathers_the_batch():
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    g, st, sx, sy, th = W.edge_filters()
+    ref = oracle.edge(W.edge_batch(5, 30, 44, seed=3, distinct=5), g, st, sx, sy, th)
+    outs = _run(2, _frames_rank)
+    for o in outs:
+        assert np.array_equal(o.view(np.uint32), ref.view(np.uint32))
