@@ -67,7 +67,7 @@ struct Smem {
   int fast;
 };
 
-// flags[0]: 1 if the filters admit the fast path
+// flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair
 __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__restrict__ st,
                                   const float *__restrict__ sx, const float *__restrict__ sy,
                                   int *flags) {
@@ -79,12 +79,17 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
     ok &= (g >= 0.0f) && (g < 0x1p50f);  // rejects NaN and negatives
     if (g != 0.0f) ok &= (g >= 0x1p-60f);
   }
+  int std_sobel = 1;
+  const float SX[9] = {-1.f, 0.f, 1.f, -2.f, 0.f, 2.f, -1.f, 0.f, 1.f};
+  const float SY[9] = {-1.f, -2.f, -1.f, 0.f, 0.f, 0.f, 1.f, 2.f, 1.f};
   for (int k = 0; k < 9; k++) {
     const float a = fabsf(sx[k]), b = fabsf(sy[k]);
     ok &= (a == 0.f || a == 1.f || a == 2.f || a == 4.f);
     ok &= (b == 0.f || b == 1.f || b == 2.f || b == 4.f);
+    std_sobel &= (sx[k] == SX[k]) && (sy[k] == SY[k]);
   }
   flags[0] = ok;
+  flags[1] = ok && std_sobel;
 }
 
 struct FusedArgs {
@@ -105,7 +110,7 @@ __device__ __forceinline__ bool pix_ok(float v) {
 // FAST: packed/FTZ gaussian, FMNMX morphology, FFMA sobel (guarded exact);
 // otherwise the oracle's operation order with single-rounding scalar ops.
 // BORDER: the tile's halo leaves the frame (pads / clamped replicas needed).
-template <bool FAST, bool BORDER>
+template <bool FAST, bool BORDER, bool SOBEL_STD = false>
 __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
                                           int lane, int warp) {
   const int n = a.n, m = a.m;
@@ -321,7 +326,20 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
         const int k = r - q;  // output row k (0..14) gets tap row q
         if (k >= 0 && k < 15) {
           float gx = q == 0 ? 0.0f : gxs[k % 3], gy = q == 0 ? 0.0f : gys[k % 3];
-          if (FAST) {
+          if (FAST && SOBEL_STD) {
+            // the standard sobel pair: the oracle's 9-tap folds with the
+            // x*0 taps dropped (they only change the sign of a zero, which
+            // the squares erase) and x*(+-1), x*(+-2) exact -> 10 ops, not 18
+            if (q == 0) {
+              gx = add_rn(-v0, v2);
+              gy = sub_rn(fmaf(-2.0f, v1, -v0), v2);
+            } else if (q == 1) {
+              gx = fmaf(2.0f, v2, fmaf(-2.0f, v0, gx));
+            } else {
+              gx = add_rn(sub_rn(gx, v0), v2);
+              gy = add_rn(fmaf(2.0f, v1, add_rn(gy, v0)), v2);
+            }
+          } else if (FAST) {
             gx = fmaf(v0, sx[q * 3 + 0], gx); gy = fmaf(v0, sy[q * 3 + 0], gy);
             gx = fmaf(v1, sx[q * 3 + 1], gx); gy = fmaf(v1, sy[q * 3 + 1], gy);
             gx = fmaf(v2, sx[q * 3 + 2], gx); gy = fmaf(v2, sy[q * 3 + 2], gy);
@@ -363,6 +381,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   const int tiles_per_frame = a.tiles_x * a.tiles_y;
   const int total = tiles_per_frame * a.frames;
   const int filters_fast = a.flags[0];
+  const bool sobel_std = a.flags[1] != 0;
 
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const int f = tile / tiles_per_frame;
@@ -408,6 +427,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     const bool border = (y0 < 5) || (x0 < 5) || (y0 + IR - 5 > n) || (x0 + IR - 5 > m);
     if (filters_fast && all_ok) {
       if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp);
+      else if (sobel_std) edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp);
       else edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp);
     } else {
       edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp);

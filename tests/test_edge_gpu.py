@@ -51,6 +51,9 @@ def test_edge_exact_fallback_paths(jb, oracle):
     _bits_equal(jb.edge_detection(x[:2], g, st2, sx, sy, th), oracle.edge(x[:2], g, st2, sx, sy, th))
     sx2 = sx * np.float32(0.3)
     _bits_equal(jb.edge_detection(x[:2], g, st, sx2, sy, th), oracle.edge(x[:2], g, st, sx2, sy, th))
+    # power-of-two but non-standard sobel: generic FFMA fast path
+    sx4, sy4 = (-2 * sx).astype(np.float32), sy.T.copy()
+    _bits_equal(jb.edge_detection(x[:2], g, st, sx4, sy4, th), oracle.edge(x[:2], g, st, sx4, sy4, th))
 
 
 def test_edge_generic_sizes(jb, oracle):
