@@ -20,9 +20,10 @@
 //    64x64 smoothed tile with packed FMUL2/FADD2 (bit-exact, see the tile
 //    guard), the 62x62 laplacian with separable min/max, packs its sign
 //    bits with warp ballots, derives zero crossings with 64-bit mask logic,
-//    computes the sobel gradient, and stores gradient|zc<<31 (4 B/px) plus a
+//    computes the sobel gx^2+gy^2, and stores it | zc<<31 (4 B/px) plus a
 //    warp->block->grid max (atomicMax on the float bits, per frame).
-//  * edge_reject_kernel: out = zc && g > theta*max[frame].  The chunk's
+//  * edge_reject_kernel: g = sqrt(gx^2+gy^2) (the correctly rounded sqrt is
+//    monotone, so the max commutes with it) and out = zc && g > theta*max.  The chunk's
 //    packed scratch (<= 32 MB) is re-read from L2, not HBM.
 //  * a generic multi-kernel path (one kernel per stage, any gs/sz/sb) serves
 //    other filter sizes and the stage-level test entry.
@@ -41,6 +42,28 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
+
+// -DEDGE_STAGE_CLOCKS: per-stage SM-cycle accounting (tools/edge_stage_clocks.py)
+#ifdef EDGE_STAGE_CLOCKS
+__device__ unsigned long long g_edge_clk[8];
+__shared__ long long s_edge_clk;
+#define EDGE_T(i)                                                            \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      const long long _t = clock64();                                        \
+      atomicAdd(&g_edge_clk[i], (unsigned long long)(_t - s_edge_clk));      \
+      s_edge_clk = _t;                                                       \
+    }                                                                        \
+  } while (0)
+#define EDGE_T0()                                   \
+  do {                                              \
+    if (threadIdx.x == 0) s_edge_clk = clock64();   \
+  } while (0)
+#else
+#define EDGE_T(i) do {} while (0)
+#define EDGE_T0() do {} while (0)
+#endif
 
 namespace jb {
 namespace edge {
@@ -57,14 +80,18 @@ __constant__ float c_struct[9];
 __constant__ float c_sx[9];
 __constant__ float c_sy[9];
 
-struct Smem {
-  float inA[IR][IP];      // clamped input tile
-  float inB[IR][IP];      // same, shifted left by one column
+constexpr int RP = 76;                 // raw row pitch: input columns x0-8 .. x0+67
+struct alignas(128) Smem {
+  // raw[r][c] = input(y0-5+r, x0-8+c): the 16-byte-aligned TMA box (TMA needs
+  // an aligned inner start coordinate); the pairs (x, x+1) with x - x0 odd
+  // are read from here, the ones with x - x0 even from the copy inA
+  alignas(128) float raw[IR][RP];
+  alignas(128) float inA[IR][IP];  // inA[r][c] = input(y0-5+r, x0-5+c)
   float sm[SR][SR];       // smoothed tile (out-of-frame = clamped replica)
   uint32_t lapbits[LR][2];// laplacian > 0, bit = column within 32-col chunk
   uint32_t zcw[TH][2];    // zero crossing, bit = column within 32-col chunk
   float wmax[THREADS / 32];
-  int fast;
+  uint64_t tma_bar;       // completion of the two TMA loads of an interior tile
 };
 
 // flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair
@@ -93,6 +120,8 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
 }
 
 struct FusedArgs {
+  CUtensorMap tmap;     // [frames*n][m] input, box {72, 70} (valid if use_tma)
+  int use_tma;
   const float *in;      // [frames][n][m] (chunk base)
   uint32_t *packed;     // [frames][n][m] gradient bits | zc << 31
   unsigned *fmax;       // [frames] max gradient bits (chunk base)
@@ -106,13 +135,40 @@ __device__ __forceinline__ bool pix_ok(float v) {
   return (u - 0x21800000u) <= (0x5f800000u - 0x21800000u) || (u + u) == 0u;
 }
 
-// stages 1-2 of one 60x60 tile whose clamped input is staged in S.inA/S.inB.
+constexpr int RPW = (IR + THREADS / 32 - 1) / (THREADS / 32);  // staged rows per warp (9)
+
+__device__ __forceinline__ void tile_origin(const FusedArgs &a, int tile, int &f, int &y0, int &x0) {
+  const int tiles_per_frame = a.tiles_x * a.tiles_y;
+  f = tile / tiles_per_frame;
+  const int t2 = tile - f * tiles_per_frame;
+  const int ty = t2 / a.tiles_x, tx = t2 - ty * a.tiles_x;
+  y0 = ty * TH;
+  x0 = tx * TW;
+}
+
+// the 76x70 raw box lies inside the frame: no clamping, TMA can stage it
+__device__ __forceinline__ bool tile_interior(const FusedArgs &a, int y0, int x0) {
+  return y0 >= 5 && x0 >= 8 && y0 + IR - 5 <= a.n && x0 - 8 + RP <= a.m;
+}
+
+// one thread: stage an interior tile's input with one TMA box load into
+// S.raw; completion on S.tma_bar
+__device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int tile) {
+  int f, y0, x0;
+  tile_origin(a, tile, f, y0, x0);
+  tc::fence_proxy_async_smem();  // the generic-proxy accesses of raw/inA are done
+  tc::mbar_arrive_expect_tx(&S.tma_bar, IR * RP * 4);
+  // the chunk is a 2-D [frames*n][m] tensor: interior tiles never cross frames
+  tc::tma_load_2d(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, f * a.n + y0 - 5);
+}
+
+// stages 1-2 of one 60x60 tile whose clamped input is staged in S.inA/S.raw.
 // FAST: packed/FTZ gaussian, FMNMX morphology, FFMA sobel (guarded exact);
 // otherwise the oracle's operation order with single-rounding scalar ops.
 // BORDER: the tile's halo leaves the frame (pads / clamped replicas needed).
 template <bool FAST, bool BORDER, bool SOBEL_STD = false>
 __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
-                                          int lane, int warp) {
+                                          int lane, int warp, int next_tile) {
   const int n = a.n, m = a.m;
   // ---- stage 1: gaussian on the 64x64 smoothed region
   {
@@ -124,10 +180,11 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
 #pragma unroll
       for (int iy = 0; iy < 14; iy++) {
         const unsigned long long *ra = reinterpret_cast<const unsigned long long *>(&S.inA[r0 + iy][0]);
-        const unsigned long long *rb = reinterpret_cast<const unsigned long long *>(&S.inB[r0 + iy][0]);
+        const unsigned long long *rb = reinterpret_cast<const unsigned long long *>(&S.raw[r0 + iy][0]);
         unsigned long long v[7];
+        // pair (x0-5+2l+j, +1): even j from inA, odd j from raw at 2l+j+3
 #pragma unroll
-        for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + (j >> 1)] : ra[lane + (j >> 1)];
+        for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + ((j + 3) >> 1)] : ra[lane + (j >> 1)];
 #pragma unroll
         for (int o = 0; o < 8; o++) {
           const int i = iy - o;
@@ -166,6 +223,9 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
     }
   }
   __syncthreads();
+  EDGE_T(1);
+  // raw/inA are free from here on: prefetch the next (interior) tile by TMA
+  if (next_tile >= 0 && tid == 0) stage_tile_tma(S, a, next_tile);
   // out-of-frame smoothed positions take the clamped in-frame value, which is
   // what the gradient's clamp-to-edge indexing reads
   if (BORDER) {
@@ -250,6 +310,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
     }
   }
   __syncthreads();
+  EDGE_T(2);
 
   // ---- stage 2b: zero crossings (bit masks), one thread per output row
   if (tid < TH) {
@@ -303,6 +364,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
     S.zcw[orow][1] = (unsigned)(zc >> 32);
   }
   __syncthreads();
+  EDGE_T(3);
 
   // ---- stage 2c: sobel gradient, pack with zc, block max
   float bmax = 0.0f;
@@ -350,11 +412,13 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
           }
           gxs[k % 3] = gx; gys[k % 3] = gy;
           if (q == 2) {
-            const float g = __fsqrt_rn(add_rn(mul_rn(gx, gx), mul_rn(gy, gy)));
+            // gx^2 + gy^2; the reject pass takes the (correctly rounded,
+            // hence monotone) sqrt, so max(sqrt(a)) = sqrt(max(a))
+            const float g = add_rn(mul_rn(gx, gx), mul_rn(gy, gy));
             const unsigned z = (S.zcw[orow0 + k][cc] >> lane) & 1u;
             if (col_ok && (!BORDER || y0 + orow0 + k < n)) {
               prow[(size_t)k * m] = __float_as_uint(g) | (z << 31);
-              bmax = fmaxf(bmax, g);  // ignores NaN like the Python fold
+              bmax = fmaxf(bmax, g);  // max of gx^2+gy^2 (ignores NaN like the fold)
             }
           }
         }
@@ -364,6 +428,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
   bmax = warp_max(bmax);
   if (lane == 0) S.wmax[warp] = bmax;
   __syncthreads();
+  EDGE_T(4);
   if (tid == 0) {
     float v = S.wmax[0];
 #pragma unroll
@@ -375,65 +440,101 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
 __global__ void __launch_bounds__(THREADS, 3)
 edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+  const uint32_t pad = (128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u;
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n, m = a.m;
-  const int tiles_per_frame = a.tiles_x * a.tiles_y;
-  const int total = tiles_per_frame * a.frames;
+  const int total = a.tiles_x * a.tiles_y * a.frames;
   const int filters_fast = a.flags[0];
   const bool sobel_std = a.flags[1] != 0;
+  if (tid == 0) {
+    tc::mbar_init(&S.tma_bar, 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t tma_phase = 0;
+  if ((int)blockIdx.x < total && a.use_tma && tid == 0) {
+    int f, y0, x0;
+    tile_origin(a, blockIdx.x, f, y0, x0);
+    if (tile_interior(a, y0, x0)) stage_tile_tma(S, a, blockIdx.x);
+  }
+  EDGE_T0();
 
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    const int f = tile / tiles_per_frame;
-    const int t2 = tile - f * tiles_per_frame;
-    const int ty = t2 / a.tiles_x, tx = t2 - ty * a.tiles_x;
-    const int y0 = ty * TH, x0 = tx * TW;
-    const float *img = a.in + (size_t)f * n * m;
-
-    // ---- stage 0: clamped input tile -> smem (both alignments) + guard.
-    // Warp w loads rows w, w+8, ...; lanes stride the 70 columns.
-    // all loads are issued before any use so ~27 LDGs per lane are in flight
-    constexpr int RPW = (IR + THREADS / 32 - 1) / (THREADS / 32);  // rows per warp (9)
-    float vals[RPW][3];
-    const int cx0 = min(max(x0 - 5 + lane, 0), m - 1);
-    const int cx1 = min(max(x0 + 27 + lane, 0), m - 1);
-    const int cx2 = min(max(x0 + 59 + lane, 0), m - 1);
-#pragma unroll
-    for (int i = 0; i < RPW; i++) {
-      const int r = warp + i * (THREADS / 32);
-      const float *row = img + (size_t)min(max(y0 - 5 + min(r, IR - 1), 0), n - 1) * m;
-      vals[i][0] = __ldg(row + cx0);
-      vals[i][1] = __ldg(row + cx1);
-      vals[i][2] = lane < IR - 64 ? __ldg(row + cx2) : 0.0f;
-    }
+    int f, y0, x0;
+    tile_origin(a, tile, f, y0, x0);
+    const bool interior = tile_interior(a, y0, x0);
     bool ok = true;
+    if (a.use_tma && interior) {
+      // ---- stage 0 (interior): the TMA issued during the previous tile
+      tc::mbar_wait(&S.tma_bar, tma_phase);
+      tma_phase ^= 1u;
+      // inA = raw shifted by 3 columns, checking the guard on the way
 #pragma unroll
-    for (int i = 0; i < RPW; i++) {
-      const int r = warp + i * (THREADS / 32);
-      if (r < IR) {
+      for (int i = 0; i < RPW; i++) {
+        const int r = warp + i * (THREADS / 32);
+        if (r < IR) {
+          const float v0 = S.raw[r][lane + 3], v1 = S.raw[r][lane + 35];
+          ok &= pix_ok(v0) && pix_ok(v1);
+          S.inA[r][lane] = v0;
+          S.inA[r][lane + 32] = v1;
+          if (lane < IR - 64) {
+            const float v2 = S.raw[r][lane + 67];
+            ok &= pix_ok(v2);
+            S.inA[r][lane + 64] = v2;
+          }
+        }
+      }
+    } else {
+      // ---- stage 0 (border / no TMA): clamped loads, all issued before use
+      const float *img = a.in + (size_t)f * n * m;
+      float vals[RPW][3];
+      const int cx0 = min(max(x0 - 5 + lane, 0), m - 1);
+      const int cx1 = min(max(x0 + 27 + lane, 0), m - 1);
+      const int cx2 = min(max(x0 + 59 + lane, 0), m - 1);
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
-          const int c = q * 32 + lane;
-          if (c < IR) {
-            const float v = vals[i][q];
-            ok &= pix_ok(v);
-            S.inA[r][c] = v;
-            if (c > 0) S.inB[r][c - 1] = v;
+      for (int i = 0; i < RPW; i++) {
+        const int r = warp + i * (THREADS / 32);
+        const float *row = img + (size_t)min(max(y0 - 5 + min(r, IR - 1), 0), n - 1) * m;
+        vals[i][0] = __ldg(row + cx0);
+        vals[i][1] = __ldg(row + cx1);
+        vals[i][2] = lane < IR - 64 ? __ldg(row + cx2) : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < RPW; i++) {
+        const int r = warp + i * (THREADS / 32);
+        if (r < IR) {
+#pragma unroll
+          for (int q = 0; q < 3; q++) {
+            const int c = q * 32 + lane;
+            if (c < IR) {
+              const float v = vals[i][q];
+              ok &= pix_ok(v);
+              S.inA[r][c] = v;
+              S.raw[r][c + 3] = v;
+            }
           }
         }
       }
     }
     const int all_ok = __syncthreads_and(ok);
-    const bool border = (y0 < 5) || (x0 < 5) || (y0 + IR - 5 > n) || (x0 + IR - 5 > m);
-    if (filters_fast && all_ok) {
-      if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp);
-      else if (sobel_std) edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp);
-      else edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp);
+    EDGE_T(0);
+    const bool border = (y0 < 2) || (x0 < 2) || (y0 + SR - 2 > n) || (x0 + SR - 2 > m);
+    int next = tile + (int)gridDim.x < total ? tile + (int)gridDim.x : -1;
+    if (next >= 0 && a.use_tma) {
+      int nf, ny0, nx0;
+      tile_origin(a, next, nf, ny0, nx0);
+      if (!tile_interior(a, ny0, nx0)) next = -1;  // staged at its start instead
     } else {
-      edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp);
+      next = -1;
     }
-    // the next tile's stage 0 only writes inA/inB, which no thread reads
-    // after edge_tile's first __syncthreads
+    if (filters_fast && all_ok) {
+      if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, next);
+      else if (sobel_std) edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, next);
+      else edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp, next);
+    } else {
+      edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, next);
+    }
   }
 }
 
@@ -445,14 +546,14 @@ __global__ void edge_reject_kernel(const uint32_t *__restrict__ packed,
        i += (long long)gridDim.x * blockDim.x) {
     const long long e = i * 4;
     const int f = (int)(e / frame_px);
-    const float g00 = __uint_as_float(__ldg(packed + (size_t)f * frame_px) & 0x7fffffffu);
-    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __uint_as_float(__ldg(fmax + f)));
+    const float g00 = __fsqrt_rn(__uint_as_float(__ldg(packed + (size_t)f * frame_px) & 0x7fffffffu));
+    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __fsqrt_rn(__uint_as_float(__ldg(fmax + f))));
     const uint4 p = __ldg(reinterpret_cast<const uint4 *>(packed) + i);
     float4 o;
-    o.x = ((p.x >> 31) && __uint_as_float(p.x & 0x7fffffffu) > thr) ? 1.0f : 0.0f;
-    o.y = ((p.y >> 31) && __uint_as_float(p.y & 0x7fffffffu) > thr) ? 1.0f : 0.0f;
-    o.z = ((p.z >> 31) && __uint_as_float(p.z & 0x7fffffffu) > thr) ? 1.0f : 0.0f;
-    o.w = ((p.w >> 31) && __uint_as_float(p.w & 0x7fffffffu) > thr) ? 1.0f : 0.0f;
+    o.x = ((p.x >> 31) && __fsqrt_rn(__uint_as_float(p.x & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
+    o.y = ((p.y >> 31) && __fsqrt_rn(__uint_as_float(p.y & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
+    o.z = ((p.z >> 31) && __fsqrt_rn(__uint_as_float(p.z & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
+    o.w = ((p.w >> 31) && __fsqrt_rn(__uint_as_float(p.w & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
     __stcs(reinterpret_cast<float4 *>(out) + i, o);
   }
 }
@@ -464,10 +565,10 @@ __global__ void edge_reject_scalar_kernel(const uint32_t *__restrict__ packed,
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const int f = (int)(i / frame_px);
-    const float g00 = __uint_as_float(packed[(size_t)f * frame_px] & 0x7fffffffu);
-    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __uint_as_float(fmax[f]));
+    const float g00 = __fsqrt_rn(__uint_as_float(packed[(size_t)f * frame_px] & 0x7fffffffu));
+    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __fsqrt_rn(__uint_as_float(fmax[f])));
     const uint32_t p = packed[i];
-    out[i] = ((p >> 31) && __uint_as_float(p & 0x7fffffffu) > thr) ? 1.0f : 0.0f;
+    out[i] = ((p >> 31) && __fsqrt_rn(__uint_as_float(p & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
   }
 }
 
@@ -656,7 +757,7 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
-  const int smem = (int)sizeof(Smem);
+  const int smem = (int)sizeof(Smem) + 128;
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
     JB_CHECK_CUDA(cudaFuncSetAttribute(edge_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set[dev] = true;
@@ -664,7 +765,19 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   const int tiles_x = (int)((m + TW - 1) / TW), tiles_y = (int)((n + TH - 1) / TH);
   for (size_t f0 = 0; f0 < batch; f0 += chunk) {
     const int frames = (int)((batch - f0 < chunk) ? batch - f0 : chunk);
-    FusedArgs fa{in + f0 * frame_px, packed, fmax + f0, flags, (int)n, (int)m, frames, tiles_x, tiles_y};
+    FusedArgs fa;
+    fa.in = in + f0 * frame_px;
+    fa.packed = packed;
+    fa.fmax = fmax + f0;
+    fa.flags = flags;
+    fa.n = (int)n; fa.m = (int)m; fa.frames = frames; fa.tiles_x = tiles_x; fa.tiles_y = tiles_y;
+    fa.use_tma = 0;
+    if (m % 4 == 0 && ((uintptr_t)fa.in % 16) == 0 && tmap_encode_fn() != nullptr) {
+      const uint64_t dims[2] = {m, n * (uint64_t)frames};
+      const uint64_t strides[1] = {m * 4};
+      const uint32_t box[2] = {(uint32_t)RP, (uint32_t)IR};
+      fa.use_tma = make_tmap_f32(&fa.tmap, fa.in, 2, dims, strides, box, 0) ? 1 : 0;
+    }
     const int total = tiles_x * tiles_y * frames;
     const int grid = total < sm_count() * 3 ? total : sm_count() * 3;
     void *tok = prof_begin("edge_fused", s);
@@ -685,6 +798,12 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   }
   return JB_OK;
 }
+
+#ifdef EDGE_STAGE_CLOCKS
+extern "C" JB_API void jb_edge_stage_clocks(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, g_edge_clk, sizeof(unsigned long long) * 8);
+}
+#endif
 
 extern "C" jb_status jb_edge_stages_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_t gs,
                                         uint64_t sz, uint64_t sb, const float *in, const float *gf,

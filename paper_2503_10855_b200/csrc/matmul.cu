@@ -25,10 +25,6 @@
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer.
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
-#include <cudaTypedefs.h>
-
-#include <mutex>
-
 #include "common.cuh"
 #include "tcgen05.cuh"
 
@@ -264,32 +260,13 @@ __global__ void matmul_exact_kernel(const float *__restrict__ a, const float *__
 }
 
 // ---------------------------------------------------------------- host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 // 2-D fp32 tensor [rows][cols] (row pitch = cols), box {box_cols, box_rows}
 static bool make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols, uint32_t box_cols,
                      uint32_t box_rows, CUtensorMapSwizzle swz) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 4};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  const uint64_t dims[2] = {cols, rows};
+  const uint64_t strides[1] = {cols * 4};
+  const uint32_t box[2] = {box_cols, box_rows};
+  return make_tmap_f32(map, base, 2, dims, strides, box, (int)swz);
 }
 
 }  // namespace mm
@@ -321,7 +298,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   JB_REQUIRE(a && b, "matmul: null pointer");
   const bool tma_ok = (m % 4 == 0) && (l % 4 == 0) && ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
-                      mm::encode_fn() != nullptr;
+                      tmap_encode_fn() != nullptr;
   if (!tma_ok) return jb_matmul_exact_f32(n, m, l, a, b, res, stream);
 
   CUtensorMap m_a, m_b;

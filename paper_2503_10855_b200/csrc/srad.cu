@@ -34,7 +34,7 @@ namespace srad {
 constexpr int TH = 32, TW = 128;
 constexpr int JR = TH + 3, JC = TW + 3;     // J region rows/cols (halo N1 S2, W1 E2)
 constexpr int JP = 132;                     // J row pitch
-constexpr int CR = TH + 1, CC = TW + 1;     // c region (own + south row, east col)
+constexpr int CR = TH + 1;                  // c region rows (own + south row; cols: own + east)
 constexpr int THREADS = 256;
 
 struct Stats {
