@@ -42,6 +42,18 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 
 
+def load_traffic(workload):
+    """dram read+write bytes per launch of the workload's dominant kernel, from
+    the committed `ncu --set full` capture (profiles/ncu_traffic.json, written by
+    tools/ncu_summary.py --json); None when absent"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f)[workload]
+        return e["dram_bytes_per_launch"], e["source"]
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -700,6 +712,10 @@ def run_ours(args):
         value = vf(ms_max / args.steps)
         e2e_value = vf(e2e_ms / args.e2e_steps)
     peaks = load_peaks()
+    if args.traffic is None:
+        args.traffic, traffic_src = load_traffic(args.workload)
+    else:
+        traffic_src = "--traffic"
     roofline = None
     if kcount:
         avg_ms = kms / kcount
@@ -723,6 +739,8 @@ def run_ours(args):
                         "peak_source": f"{peaks['source']} MEASURED_PEAKS.json hbm_gbs",
                         "traffic": args.traffic, "avg_launch_ms": round(avg_ms, 4),
                         "units_per_launch": per_launch_units, "share_of_step": round(kms / ms, 3)}
+        roofline["traffic_unit"] = "bytes/launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+        roofline["traffic_source"] = traffic_src
         if hasattr(wl, "roofline_extra"):
             roofline.update(wl.roofline_extra(avg_ms, per_launch_units))
     h2d, d2h = wl.e2e_bytes()

@@ -56,6 +56,35 @@ def summary(rep):
     return "\n".join(out)
 
 
+def traffic(rep):
+    """(kernel name, dram read+write bytes, duration ns) of the captured launch"""
+    rows = list(csv.reader(io.StringIO(run([rep, '--page', 'raw', '--csv']))))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1, 'us': 1e3, 'ms': 1e6, 'usecond': 1e3,
+             'nsecond': 1, 'msecond': 1e6}
+
+    def get(k):
+        i = hdr.index(k)
+        return float(vals[i].replace(',', '')) * scale.get(units[i], 1)
+    return (vals[hdr.index('Kernel Name')], get('dram__bytes_read.sum') + get('dram__bytes_write.sum'),
+            get('gpu__time_duration.sum'))
+
+
 if __name__ == '__main__':
-    for rep in sys.argv[1:]:
+    # --json OUT: also write {workload: {kernel, dram_bytes_per_launch, ncu_duration_ns}} for bench.py
+    args = sys.argv[1:]
+    out_json = None
+    if args and args[0] == '--json':
+        out_json, args = args[1], args[2:]
+    table = {}
+    for rep in args:
         print(summary(rep))
+        if out_json:
+            k, b, t = traffic(rep)
+            w = rep.rsplit('/', 1)[-1].replace('prof_', '').replace('.ncu-rep', '')
+            table[w] = {"kernel": k.split('(')[0], "dram_bytes_per_launch": b, "ncu_duration_ns": t,
+                        "source": rep.rsplit('/', 1)[-1]}
+    if out_json:
+        import json
+        with open(out_json, 'w') as f:
+            json.dump(table, f, indent=1)
