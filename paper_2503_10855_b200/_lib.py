@@ -45,6 +45,7 @@ SIGNATURES = {
     "jb_euler_flux_f32": [_u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_bfs": [_u64, _u64, _vp, _vp, _vp, _u32, _vp, _vp],
     "jb_bp_train_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "jb_selftest_fastmath": [_u64, _u64, ctypes.c_int, ctypes.c_int, _vp, _vp],
 }
 
 _lib = None

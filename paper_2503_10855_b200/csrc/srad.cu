@@ -240,6 +240,242 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
   finish_stats(a, (long long)(a.row_hi - a.row_lo) * cols);
 }
 
+// ----------------------------------------------------------------- strips
+// srad_strip_kernel: the fast path for rows of 16-byte-aligned float4s
+// (cols % 4 == 0).  No shared memory and no block barriers in the loop:
+//  * a warp owns a strip of SW = 124 output columns x SH rows; lane l holds
+//    columns x0+4l .. x0+4l+3 of three consecutive rows in registers (one
+//    LDG.128 per lane per row) and walks down the strip;
+//  * west/east neighbours come from the adjacent lanes by shuffle (lane 0
+//    loads the west halo column itself); lane 31 only supplies the east
+//    halo coefficient c(x0+124) -- hence 124 = 31 x 4 output columns;
+//  * c(r) is computed once per pixel (+1/SH rows), the update of row r-1
+//    follows in the same step with c_S = c(r) and c_E from lane l+1;
+//  * divisions use the branch-free fast path (common.cuh) while the strip's
+//    J values lie in [2^-8, 2^8] and q0^2 in [2^-20, 2^20]: then every
+//    dividend, divisor and quotient is a normal float within [2^-105, 2^105]
+//    (DESIGN.md §srad derives the bounds), and the only special divisors,
+//    den^2 = 0 and 1 + den = 0, produce NaN in the fast path and are redone
+//    exactly.  A strip outside the guard is recomputed with IEEE division.
+// Arithmetic per pixel is the oracle's, op for op; the few fused forms
+// (0.25 L folded into the numerator/denominator) are exact rewrites that
+// only apply scalings by powers of two to normal values.
+constexpr int SW = 124, SH = 32, SWARPS = 8;
+
+struct StripCtx {
+  const float *src;
+  float *dst;
+  int rows, cols, row_lo, row_hi, compress;
+  float ql, q0, q0den, q0y;
+};
+
+__device__ __forceinline__ float4 ld_row(const float *src, int cols, int y, int xb) {
+  return __ldg(reinterpret_cast<const float4 *>(src + (size_t)y * cols + xb));
+}
+
+template <bool FAST>
+__device__ __forceinline__ float coef_px(float Jc, float n_, float s_, float w_, float e_, const StripCtx &k) {
+  if (!FAST) {
+    const float G2 = div_rn(add_rn(add_rn(add_rn(mul_rn(n_, n_), mul_rn(s_, s_)), mul_rn(w_, w_)), mul_rn(e_, e_)),
+                            mul_rn(Jc, Jc));
+    const float L = div_rn(add_rn(add_rn(add_rn(n_, s_), w_), e_), Jc);
+    const float num = sub_rn(mul_rn(0.5f, G2), mul_rn(0.0625f, mul_rn(L, L)));
+    const float den = add_rn(1.0f, mul_rn(0.25f, L));
+    const float qsqr = div_rn(num, mul_rn(den, den));
+    const float den2 = div_rn(sub_rn(qsqr, k.q0), k.q0den);
+    const float cv = div_rn(1.0f, add_rn(1.0f, den2));
+    return cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
+  } else {
+    const float G2 = div_fast(add_rn(add_rn(add_rn(mul_rn(n_, n_), mul_rn(s_, s_)), mul_rn(w_, w_)), mul_rn(e_, e_)),
+                              mul_rn(Jc, Jc));
+    // L4 = L/4 exactly; (L*L)*0.0625 == L4*L4 and 0.5*G2 - t == fma(0.5, G2, -t)
+    // because every scaling by a power of two is exact on these normal values
+    const float L4 = mul_rn(0.25f, div_fast(add_rn(add_rn(add_rn(n_, s_), w_), e_), Jc));
+    const float num = __fmaf_rn(0.5f, G2, -mul_rn(L4, L4));
+    const float den = add_rn(1.0f, L4);
+    const float qsqr = div_fast(num, mul_rn(den, den));
+    const float den2 = div_by(sub_rn(qsqr, k.q0), k.q0den, k.q0y);
+    const float cv = rcp_fast(add_rn(1.0f, den2));
+    // NaN here: a zero divisor (den^2 or 1+den) or NaN data -> exact redo
+    return cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
+  }
+}
+
+__device__ __noinline__ float coef_exact(float Jc, float n_, float s_, float w_, float e_, const StripCtx &k) {
+  return coef_px<false>(Jc, n_, s_, w_, e_, k);
+}
+
+// one strip; returns false (FAST only) when the strip fails the range guard
+template <bool FAST>
+__device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
+  const int lane = threadIdx.x & 31;
+  const int rows = k.rows, cols = k.cols;
+  const int xl = x0 + 4 * lane;
+  const int xb = xl < cols ? xl : cols - 4;                // clamp idle lanes onto real data
+  const bool out_lane = lane < 31 && xl < cols;
+  const bool east_edge = xl + 4 >= cols;                   // column xl+3 is the last image column
+  const int xw = x0 > 0 ? x0 - 1 : 0;                      // west halo column (clamped)
+  float mn = 3.0e38f, mx = -3.0e38f;
+  auto guard = [&](float4 v) {
+    if (FAST) {
+      mn = fminf(fminf(mn, v.x), fminf(fminf(v.y, v.z), v.w));
+      mx = fmaxf(fmaxf(mx, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+    }
+  };
+  auto cl = [&](int y) { return y < 0 ? 0 : (y > rows - 1 ? rows - 1 : y); };
+  float4 Jm = ld_row(k.src, cols, cl(y0 - 1), xb);
+  float4 J0 = ld_row(k.src, cols, cl(y0), xb);
+  float w0 = __ldg(k.src + (size_t)cl(y0) * cols + xw);
+  guard(Jm); guard(J0);
+  // prefetched next row + its west halo value
+  int yn = cl(y0 + 1);
+  float4 Jp = ld_row(k.src, cols, yn, xb);
+  float wp = __ldg(k.src + (size_t)yn * cols + xw);
+  float4 cprev = make_float4(0.f, 0.f, 0.f, 0.f);
+  float dn[4], ds[4], dw[4], de[4];
+  const int ylast = y1 < rows ? y1 : rows - 1;             // last row whose c is needed
+  const unsigned FULL = 0xffffffffu;
+  for (int r = y0; r <= ylast; r++) {
+    const float4 Jpp = Jp;
+    const float wpp = wp;
+    if (r < ylast) {  // prefetch row r+2
+      yn = cl(r + 2);
+      Jp = ld_row(k.src, cols, yn, xb);
+      wp = __ldg(k.src + (size_t)yn * cols + xw);
+    }
+    guard(Jpp);
+    // neighbours of row r
+    float W = __shfl_up_sync(FULL, J0.w, 1);
+    float E = __shfl_down_sync(FULL, J0.x, 1);
+    if (lane == 0) W = w0;
+    if (east_edge) E = J0.w;
+    if (FAST) { mn = fminf(mn, w0); mx = fmaxf(mx, w0); }
+    const float jc[4] = {J0.x, J0.y, J0.z, J0.w};
+    const float jn[4] = {Jm.x, Jm.y, Jm.z, Jm.w};
+    const float js[4] = {Jpp.x, Jpp.y, Jpp.z, Jpp.w};
+    const float jw[4] = {W, J0.x, J0.y, J0.z};
+    const float je[4] = {J0.y, J0.z, J0.w, E};
+    float cc[4], tn[4], ts[4], tw[4], te[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      tn[q] = sub_rn(jn[q], jc[q]);
+      ts[q] = sub_rn(js[q], jc[q]);
+      tw[q] = sub_rn(jw[q], jc[q]);
+      te[q] = sub_rn(je[q], jc[q]);
+      cc[q] = coef_px<FAST>(jc[q], tn[q], ts[q], tw[q], te[q], k);
+    }
+    if (FAST) {
+      const bool bad = (cc[0] != cc[0]) | (cc[1] != cc[1]) | (cc[2] != cc[2]) | (cc[3] != cc[3]);
+      if (__any_sync(FULL, bad)) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) cc[q] = coef_exact(jc[q], tn[q], ts[q], tw[q], te[q], k);
+      }
+    }
+    if (r > y0) {
+      // update row r-1 with c_N = cprev, c_S = cc, c_E from the east column
+      float cE3 = __shfl_down_sync(FULL, cprev.x, 1);
+      if (east_edge) cE3 = cprev.w;
+      const float cN[4] = {cprev.x, cprev.y, cprev.z, cprev.w};
+      const float cE[4] = {cprev.y, cprev.z, cprev.w, cE3};
+      const float jp[4] = {Jm.x, Jm.y, Jm.z, Jm.w};  // centre values of row r-1
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const float D = add_rn(add_rn(add_rn(mul_rn(cN[q], dn[q]), mul_rn(cc[q], ds[q])), mul_rn(cN[q], dw[q])),
+                               mul_rn(cE[q], de[q]));
+        o[q] = add_rn(jp[q], mul_rn(k.ql, D));
+      }
+      if (out_lane) {
+        const size_t off = (size_t)(r - 1 - k.row_lo) * cols + xl;
+        if (k.compress) {
+          *reinterpret_cast<float4 *>(k.dst + off) =
+              make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
+                          mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
+        } else {
+          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            s += (double)o[q];
+            s2 += (double)o[q] * (double)o[q];
+          }
+        }
+      }
+    }
+    if (r == y1 - 1 && r == ylast) {
+      // bottom image row: c_S is the row's own c (clamped index), update now
+      float cE3 = __shfl_down_sync(FULL, cc[0], 1);
+      if (east_edge) cE3 = cc[3];
+      const float cE[4] = {cc[1], cc[2], cc[3], cE3};
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const float D = add_rn(add_rn(add_rn(mul_rn(cc[q], tn[q]), mul_rn(cc[q], ts[q])), mul_rn(cc[q], tw[q])),
+                               mul_rn(cE[q], te[q]));
+        o[q] = add_rn(jc[q], mul_rn(k.ql, D));
+      }
+      if (out_lane) {
+        const size_t off = (size_t)(r - k.row_lo) * cols + xl;
+        if (k.compress) {
+          *reinterpret_cast<float4 *>(k.dst + off) =
+              make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
+                          mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
+        } else {
+          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            s += (double)o[q];
+            s2 += (double)o[q] * (double)o[q];
+          }
+        }
+      }
+    }
+    // roll the window
+    cprev = make_float4(cc[0], cc[1], cc[2], cc[3]);
+#pragma unroll
+    for (int q = 0; q < 4; q++) { dn[q] = tn[q]; ds[q] = ts[q]; dw[q] = tw[q]; de[q] = te[q]; }
+    Jm = J0;
+    J0 = Jpp;
+    w0 = wpp;
+  }
+  if (!FAST) return true;
+  return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f);
+}
+
+__device__ __noinline__ void strip_exact(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
+  srad_strip<false>(k, x0, y0, y1, s, s2);
+}
+
+__global__ void __launch_bounds__(SWARPS * 32, 2) srad_strip_kernel(Args a) {
+  const int warp = threadIdx.x >> 5;
+  StripCtx k;
+  k.src = a.src; k.dst = a.dst; k.rows = a.rows; k.cols = a.cols;
+  k.row_lo = a.row_lo; k.row_hi = a.row_hi; k.compress = a.compress; k.ql = a.ql;
+  k.q0 = *a.q0;
+  k.q0den = mul_rn(k.q0, add_rn(1.0f, k.q0));
+  k.q0y = recip_refined(k.q0den);
+  const bool q0ok = k.q0 >= 9.5367431640625e-07f && k.q0 <= 1048576.0f;  // [2^-20, 2^20]
+  const int sx = (a.cols + SW - 1) / SW;
+  const int nrows = a.row_hi - a.row_lo;
+  const int sy = (nrows + SH - 1) / SH;
+  const int strips = sx * sy;
+  double s = 0.0, s2 = 0.0;
+  for (int st = blockIdx.x * SWARPS + warp; st < strips; st += gridDim.x * SWARPS) {
+    const int ty = st / sx, tx = st - ty * sx;
+    const int x0 = tx * SW, y0 = a.row_lo + ty * SH;
+    const int y1 = min(y0 + SH, a.row_hi);
+    const double s_in = s, s2_in = s2;
+    bool ok = false;
+    if (q0ok) ok = srad_strip<true>(k, x0, y0, y1, s, s2);
+    if (!ok) {  // outside the fast-division guard: redo with IEEE division
+      s = s_in; s2 = s2_in;
+      strip_exact(k, x0, y0, y1, s, s2);
+    }
+  }
+  if (a.compress) return;
+  block_stats(s, s2, a.partials + blockIdx.x);
+  finish_stats(a, (long long)nrows * a.cols);
+}
+
 __global__ void copy_q0_kernel(const float *q0, float *out, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = q0[i];
 }
@@ -249,6 +485,20 @@ __global__ void copy_q0_kernel(const float *q0, float *out, int n) {
 
 using namespace jb;
 using namespace jb::srad;
+
+// the strip kernel needs 16-byte aligned rows of float4s
+static bool strip_ok(uint64_t cols, const void *p0, const void *p1) {
+  return cols % 4 == 0 && cols >= 4 && ((uintptr_t)p0 % 16) == 0 && ((uintptr_t)p1 % 16) == 0;
+}
+static int strip_grid() {
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_strip_kernel, SWARPS * 32, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  return sm_count() * per_sm;
+}
 
 extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, float lambda, const float *image,
                                  float *out, float *q0sqr, void *stream) {
@@ -265,7 +515,10 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
   if (per_sm < 1) per_sm = 1;
   const int grid = tiles < sm_count() * per_sm ? tiles : sm_count() * per_sm;
   const int grid_x = sm_count() * 8;
-  const int gmax = grid > grid_x ? grid : grid_x;
+  const bool strips = strip_ok(cols, image, out);
+  const int sgrid = strips ? strip_grid() : 0;
+  int gmax = grid > grid_x ? grid : grid_x;
+  if (sgrid > gmax) gmax = sgrid;
   // scratch: J ping-pong (2 images), q0 per iteration, partials, ticket
   const size_t img_bytes = ((npx * 4 + 255) / 256) * 256;
   const size_t q0_bytes = (((niter + 1) * 4 + 255) / 256) * 256;
@@ -299,7 +552,8 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
     a.q0_next = q0 + it + 1;
     a.compress = last;
     void *tok = prof_begin("srad_iter", s);
-    srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
+    if (strips) srad_strip_kernel<<<sgrid, SWARPS * 32, 0, s>>>(a);
+    else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
     prof_end(tok, s);
     JB_LAUNCHED("srad_iter");
   }
@@ -357,7 +611,9 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
   JB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_iter_kernel, THREADS, 0));
   if (per_sm < 1) per_sm = 1;
   const int grid = tiles < sm_count() * per_sm ? tiles : sm_count() * per_sm;
-  const size_t pb = ((grid * sizeof(Stats) + 255) / 256) * 256;
+  const bool strips = strip_ok(cols, J_ext, out_own);
+  const int sgrid = strips ? strip_grid() : 0;
+  const size_t pb = (((grid > sgrid ? grid : sgrid) * sizeof(Stats) + 255) / 256) * 256;
   char *ws = (char *)workspace(pb + 256, s);
   if (!ws) return JB_ECUDA;
   Args a{};
@@ -370,7 +626,8 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
   a.sums_out = sums;
   JB_CHECK_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s));
   void *tok = prof_begin("srad_iter", s);
-  srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
+  if (strips) srad_strip_kernel<<<sgrid, SWARPS * 32, 0, s>>>(a);
+  else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
   prof_end(tok, s);
   JB_LAUNCHED("srad_slab_step");
   return JB_OK;
