@@ -441,6 +441,149 @@ __device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, in
   return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f);
 }
 
+// ---- the packed fast strip: two pixels per FFMA2/FMUL2/FADD2 for the
+// coefficient (ranges proven by the guard, so .ftz adds never see a
+// subnormal), scalar single-rounding update; the row loop is unrolled 4x so
+// the 4-row register window rotates by renaming instead of moves.
+struct PxPair {
+  f2 n, s, w, e;  // neighbour differences of 2 pixels
+};
+
+// c for a pixel pair; returns -cv (unclamped) per lane pair
+__device__ __forceinline__ f2 ncoef2(f2 Jc, const PxPair &d, f2 q0, f2 q0den, f2 nq0y) {
+  const f2 Jc2 = mul2(Jc, Jc);
+  const f2 G2num = add2z(add2z(add2z(mul2(d.n, d.n), mul2(d.s, d.s)), mul2(d.w, d.w)), mul2(d.e, d.e));
+  const f2 nG2 = ndiv2(G2num, Jc2);                               // -G2
+  const f2 nL4 = mul2(ndiv2(add2z(add2z(add2z(d.n, d.s), d.w), d.e), Jc), bc2(0.25f));  // -L/4
+  const f2 t = mul2(nL4, nL4);                                    // (L*L)/16
+  const f2 nnum = fma2(nG2, bc2(0.5f), t);                        // -(0.5 G2 - t)
+  const f2 den = sub2z(bc2(1.0f), nL4);                           // 1 + L/4
+  const f2 qsqr = ndiv2(nnum, mul2(den, den));                    // num / den^2
+  const f2 nden2 = ndiv2_by(sub2z(qsqr, q0), q0den, nq0y);        // -(qsqr - q0)/q0den
+  return nrcp2(sub2z(bc2(1.0f), nden2));                          // -1/(1 + den)
+}
+
+__device__ __forceinline__ float clamp01_neg(float ncv) {  // clamp(-ncv) for non-NaN ncv
+  const float cv = -ncv;
+  return cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
+}
+
+__device__ __noinline__ bool strip_fast(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
+  const int lane = threadIdx.x & 31;
+  const int rows = k.rows, cols = k.cols;
+  const int xl = x0 + 4 * lane;
+  const int xb = xl < cols ? xl : cols - 4;
+  const bool out_lane = lane < 31 && xl < cols;
+  const bool east_edge = xl + 4 >= cols;
+  const int xw = x0 > 0 ? x0 - 1 : 0;
+  const unsigned FULL = 0xffffffffu;
+  const f2 q0 = bc2(k.q0), q0den = bc2(k.q0den), nq0y = bc2(-k.q0y);
+  float mn = 3.0e38f, mx = -3.0e38f;
+  auto cl = [&](int y) { return y < 0 ? 0 : (y > rows - 1 ? rows - 1 : y); };
+  auto ldw = [&](int y) { return __ldg(k.src + (size_t)cl(y) * cols + xw); };
+  auto guard = [&](const float4 &v, float w) {
+    mn = fminf(fminf(mn, w), fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+    mx = fmaxf(fmaxf(mx, w), fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  };
+  const int ylast = y1 < rows ? y1 : rows - 1;
+  float4 B0 = ld_row(k.src, cols, cl(y0 - 1), xb), B1 = ld_row(k.src, cols, cl(y0), xb);
+  float4 B2 = ld_row(k.src, cols, cl(y0 + 1), xb), B3;
+  float W0 = 0.f, W1 = ldw(y0), W2 = ldw(y0 + 1), W3 = 0.f;
+  guard(B0, W1);
+  guard(B1, W1);
+  PxPair DA[2], DB[2];
+  float4 CA = make_float4(0.f, 0.f, 0.f, 0.f), CB = CA;
+
+  // row r: window Jm (r-1), J0 (r), Jp (r+1); prefetch row r+2 into Jn.
+  // dprev/cprev hold row r-1's differences and coefficients, dcur/ccur get row r's.
+  auto step = [&](int r, const float4 &Jm, const float4 &J0, const float4 &Jp, float4 &Jn, const float &w0,
+                  const float &wp, float &wn, PxPair (&dprev)[2], PxPair (&dcur)[2], const float4 &cprev,
+                  float4 &ccur) {
+    if (r < ylast) {
+      Jn = ld_row(k.src, cols, cl(r + 2), xb);
+      wn = ldw(r + 2);
+    }
+    guard(Jp, wp);
+    float W = __shfl_up_sync(FULL, J0.w, 1);
+    float E = __shfl_down_sync(FULL, J0.x, 1);
+    if (lane == 0) W = w0;
+    if (east_edge) E = J0.w;
+    const f2 c01 = pk2(J0.x, J0.y), c23 = pk2(J0.z, J0.w);
+    dcur[0].n = sub2z(pk2(Jm.x, Jm.y), c01);
+    dcur[1].n = sub2z(pk2(Jm.z, Jm.w), c23);
+    dcur[0].s = sub2z(pk2(Jp.x, Jp.y), c01);
+    dcur[1].s = sub2z(pk2(Jp.z, Jp.w), c23);
+    dcur[0].w = sub2z(pk2(W, J0.x), c01);
+    dcur[1].w = sub2z(pk2(J0.y, J0.z), c23);
+    dcur[0].e = sub2z(pk2(J0.y, J0.z), c01);
+    dcur[1].e = sub2z(pk2(J0.w, E), c23);
+    const f2 n01 = ncoef2(c01, dcur[0], q0, q0den, nq0y);
+    const f2 n23 = ncoef2(c23, dcur[1], q0, q0den, nq0y);
+    float nc[4] = {lo2(n01), hi2(n01), lo2(n23), hi2(n23)};
+    const bool bad = (nc[0] != nc[0]) | (nc[1] != nc[1]) | (nc[2] != nc[2]) | (nc[3] != nc[3]);
+    if (__any_sync(FULL, bad)) {  // a zero divisor (or NaN data): exact coefficient
+      const float jc[4] = {J0.x, J0.y, J0.z, J0.w};
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const PxPair &d = dcur[q >> 1];
+        const float dn = (q & 1) ? hi2(d.n) : lo2(d.n), ds = (q & 1) ? hi2(d.s) : lo2(d.s);
+        const float dw = (q & 1) ? hi2(d.w) : lo2(d.w), de = (q & 1) ? hi2(d.e) : lo2(d.e);
+        nc[q] = -coef_exact(jc[q], dn, ds, dw, de, k);
+      }
+    }
+    ccur = make_float4(clamp01_neg(nc[0]), clamp01_neg(nc[1]), clamp01_neg(nc[2]), clamp01_neg(nc[3]));
+    // update of row r-1 (c_S = row r's c), or of row r itself at the image bottom
+    auto update = [&](int ro, const float4 &Jc4, const PxPair (&d)[2], const float4 &cN4, const float4 &cS4) {
+      float cE3 = __shfl_down_sync(FULL, cN4.x, 1);
+      if (east_edge) cE3 = cN4.w;
+      const float cN[4] = {cN4.x, cN4.y, cN4.z, cN4.w};
+      const float cS[4] = {cS4.x, cS4.y, cS4.z, cS4.w};
+      const float cE[4] = {cN4.y, cN4.z, cN4.w, cE3};
+      const float jc[4] = {Jc4.x, Jc4.y, Jc4.z, Jc4.w};
+      const float dn[4] = {lo2(d[0].n), hi2(d[0].n), lo2(d[1].n), hi2(d[1].n)};
+      const float ds[4] = {lo2(d[0].s), hi2(d[0].s), lo2(d[1].s), hi2(d[1].s)};
+      const float dw[4] = {lo2(d[0].w), hi2(d[0].w), lo2(d[1].w), hi2(d[1].w)};
+      const float de[4] = {lo2(d[0].e), hi2(d[0].e), lo2(d[1].e), hi2(d[1].e)};
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const float D = add_rn(add_rn(add_rn(mul_rn(cN[q], dn[q]), mul_rn(cS[q], ds[q])), mul_rn(cN[q], dw[q])),
+                               mul_rn(cE[q], de[q]));
+        o[q] = add_rn(jc[q], mul_rn(k.ql, D));
+      }
+      if (out_lane) {
+        const size_t off = (size_t)(ro - k.row_lo) * cols + xl;
+        if (k.compress) {
+          *reinterpret_cast<float4 *>(k.dst + off) =
+              make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
+                          mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
+        } else {
+          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            s += (double)o[q];
+            s2 += (double)o[q] * (double)o[q];
+          }
+        }
+      }
+    };
+    if (r > y0) update(r - 1, Jm, dprev, cprev, ccur);
+    if (r == y1 - 1 && r == ylast) update(r, J0, dcur, ccur, ccur);
+  };
+
+  for (int r = y0;; r += 4) {
+    step(r, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
+    if (r + 1 > ylast) break;
+    step(r + 1, B1, B2, B3, B0, W2, W3, W0, DA, DB, CA, CB);
+    if (r + 2 > ylast) break;
+    step(r + 2, B2, B3, B0, B1, W3, W0, W1, DB, DA, CB, CA);
+    if (r + 3 > ylast) break;
+    step(r + 3, B3, B0, B1, B2, W0, W1, W2, DA, DB, CA, CB);
+    if (r + 4 > ylast) break;
+  }
+  return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f);
+}
+
 __device__ __noinline__ void strip_exact(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
   srad_strip<false>(k, x0, y0, y1, s, s2);
 }
@@ -465,7 +608,7 @@ __global__ void __launch_bounds__(SWARPS * 32, 2) srad_strip_kernel(Args a) {
     const int y1 = min(y0 + SH, a.row_hi);
     const double s_in = s, s2_in = s2;
     bool ok = false;
-    if (q0ok) ok = srad_strip<true>(k, x0, y0, y1, s, s2);
+    if (q0ok) ok = strip_fast(k, x0, y0, y1, s, s2);
     if (!ok) {  // outside the fast-division guard: redo with IEEE division
       s = s_in; s2 = s2_in;
       strip_exact(k, x0, y0, y1, s, s2);

@@ -4,7 +4,7 @@
 set -u
 mkdir -p gpurun_out
 OUT=gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q ${TESTS:-} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q ${TESTS_K:+-k "$TESTS_K"} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 : > $OUT/bench_iter.jsonl
 for w in ${WORKLOADS:-}; do
   timeout 600 python bench.py --workload $w ${BENCH_ARGS:---steps 5 --warmup 3 --no-cpu} >> $OUT/bench_iter.jsonl 2> $OUT/bench_$w.err || echo "{\"workload\": \"$w\", \"failed\": true}" >> $OUT/bench_iter.jsonl
