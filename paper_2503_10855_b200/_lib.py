@@ -13,7 +13,7 @@ import os
 import re
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libjunob200.so")
+LIB_PATH = os.environ.get("JB_LIB") or os.path.join(_PKG, "libjunob200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "junob200.h")
 
 JB_OK, JB_EINVAL, JB_ERUNTIME, JB_ECUDA, JB_ENOTSUP = 0, 1, 2, 3, 4

@@ -19,8 +19,11 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libjunob200.so")
+# JB_BUILD_TAG=x builds an experiment variant (extra nvcc flags in
+# JB_NVCC_EXTRA) into _build_x/ and libjunob200_x.so; load it with JB_LIB
+_TAG = os.environ.get("JB_BUILD_TAG", "")
+BUILD = os.path.join(PKG, "_build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(PKG, "libjunob200" + ("_" + _TAG if _TAG else "") + ".so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -31,7 +34,7 @@ FLAGS = [
     "-fmad=false",
     "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
     "-I" + os.path.join(ROOT, "include"),
-]
+] + os.environ.get("JB_NVCC_EXTRA", "").split()
 
 
 def _sources():

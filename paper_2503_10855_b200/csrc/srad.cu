@@ -261,6 +261,9 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
 // (0.25 L folded into the numerator/denominator) are exact rewrites that
 // only apply scalings by powers of two to normal values.
 constexpr int SW = 124, SH = 32, SWARPS = 8;
+#ifndef SRAD_MINB
+#define SRAD_MINB 2
+#endif
 
 struct StripCtx {
   const float *src;
@@ -301,7 +304,10 @@ __device__ __forceinline__ float coef_px(float Jc, float n_, float s_, float w_,
   }
 }
 
-__device__ __noinline__ float coef_exact(float Jc, float n_, float s_, float w_, float e_, const StripCtx &k) {
+__device__ __noinline__ float coef_exact(float Jc, float n_, float s_, float w_, float e_, float q0, float q0den) {
+  StripCtx k;
+  k.q0 = q0;
+  k.q0den = q0den;
   return coef_px<false>(Jc, n_, s_, w_, e_, k);
 }
 
@@ -368,7 +374,7 @@ __device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, in
       const bool bad = (cc[0] != cc[0]) | (cc[1] != cc[1]) | (cc[2] != cc[2]) | (cc[3] != cc[3]);
       if (__any_sync(FULL, bad)) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) cc[q] = coef_exact(jc[q], tn[q], ts[q], tw[q], te[q], k);
+        for (int q = 0; q < 4; q++) cc[q] = coef_exact(jc[q], tn[q], ts[q], tw[q], te[q], k.q0, k.q0den);
       }
     }
     if (r > y0) {
@@ -463,46 +469,47 @@ __device__ __forceinline__ f2 ncoef2(f2 Jc, const PxPair &d, f2 q0, f2 q0den, f2
   return nrcp2(sub2z(bc2(1.0f), nden2));                          // -1/(1 + den)
 }
 
-__device__ __forceinline__ float clamp01_neg(float ncv) {  // clamp(-ncv) for non-NaN ncv
-  const float cv = -ncv;
-  return cv < 0.0f ? 0.0f : (cv > 1.0f ? 1.0f : cv);
-}
-
-__device__ __noinline__ bool strip_fast(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
+// Interior strips only (rows y0-1 .. y1+2 exist, so no row clamping and no
+// bottom-row special case; the kernel sends the rest to srad_strip<true>).
+template <bool COMPRESS>
+__device__ __forceinline__ bool strip_fast(const StripCtx k, int x0, int y0, int y1, double &s, double &s2) {
   const int lane = threadIdx.x & 31;
-  const int rows = k.rows, cols = k.cols;
+  const int cols = k.cols;
   const int xl = x0 + 4 * lane;
   const int xb = xl < cols ? xl : cols - 4;
   const bool out_lane = lane < 31 && xl < cols;
   const bool east_edge = xl + 4 >= cols;
   const int xw = x0 > 0 ? x0 - 1 : 0;
   const unsigned FULL = 0xffffffffu;
-  const f2 q0 = bc2(k.q0), q0den = bc2(k.q0den), nq0y = bc2(-k.q0y);
-  float mn = 3.0e38f, mx = -3.0e38f;
-  auto cl = [&](int y) { return y < 0 ? 0 : (y > rows - 1 ? rows - 1 : y); };
-  auto ldw = [&](int y) { return __ldg(k.src + (size_t)cl(y) * cols + xw); };
+  const f2 q0 = bc2(k.q0), q0den = bc2(k.q0den), nq0y = bc2(-k.q0y), ql = bc2(k.ql);
+  float mn = 3.0e38f, mx = -3.0e38f, mnc = 1.0f;
+  const size_t cs = (size_t)cols;
+  const float *pw = k.src + (size_t)(y0 - 1) * cs + xw;            // west halo column
+  const float4 *pj = reinterpret_cast<const float4 *>(k.src + (size_t)(y0 - 1) * cs + xb);
+  const size_t cs4 = cs / 4;
+  float *po = k.dst + (size_t)(y0 - k.row_lo) * cs + xl;            // output row y0
   auto guard = [&](const float4 &v, float w) {
     mn = fminf(fminf(mn, w), fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
     mx = fmaxf(fmaxf(mx, w), fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
   };
-  const int ylast = y1 < rows ? y1 : rows - 1;
-  float4 B0 = ld_row(k.src, cols, cl(y0 - 1), xb), B1 = ld_row(k.src, cols, cl(y0), xb);
-  float4 B2 = ld_row(k.src, cols, cl(y0 + 1), xb), B3;
-  float W0 = 0.f, W1 = ldw(y0), W2 = ldw(y0 + 1), W3 = 0.f;
+  float4 B0 = __ldg(pj), B1 = __ldg(pj + cs4), B2 = __ldg(pj + 2 * cs4), B3;
+  float W1 = __ldg(pw + cs), W2 = __ldg(pw + 2 * cs), W3 = 0.f, W0 = 0.f;
+  pj += 3 * cs4;
+  pw += 3 * cs;
   guard(B0, W1);
   guard(B1, W1);
   PxPair DA[2], DB[2];
-  float4 CA = make_float4(0.f, 0.f, 0.f, 0.f), CB = CA;
+  f2 CA[2], CB[2];
 
   // row r: window Jm (r-1), J0 (r), Jp (r+1); prefetch row r+2 into Jn.
-  // dprev/cprev hold row r-1's differences and coefficients, dcur/ccur get row r's.
-  auto step = [&](int r, const float4 &Jm, const float4 &J0, const float4 &Jp, float4 &Jn, const float &w0,
-                  const float &wp, float &wn, PxPair (&dprev)[2], PxPair (&dcur)[2], const float4 &cprev,
-                  float4 &ccur) {
-    if (r < ylast) {
-      Jn = ld_row(k.src, cols, cl(r + 2), xb);
-      wn = ldw(r + 2);
-    }
+  // dprev/cprev: row r-1's differences / coefficients; dcur/ccur: row r's.
+  auto step = [&](bool upd, const float4 &Jm, const float4 &J0, const float4 &Jp, float4 &Jn, const float &w0,
+                  const float &wp, float &wn, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
+                  f2 (&ccur)[2]) {
+    Jn = __ldg(pj);
+    wn = __ldg(pw);
+    pj += cs4;
+    pw += cs;
     guard(Jp, wp);
     float W = __shfl_up_sync(FULL, J0.w, 1);
     float E = __shfl_down_sync(FULL, J0.x, 1);
@@ -519,8 +526,10 @@ __device__ __noinline__ bool strip_fast(const StripCtx &k, int x0, int y0, int y
     dcur[1].e = sub2z(pk2(J0.w, E), c23);
     const f2 n01 = ncoef2(c01, dcur[0], q0, q0den, nq0y);
     const f2 n23 = ncoef2(c23, dcur[1], q0, q0den, nq0y);
-    float nc[4] = {lo2(n01), hi2(n01), lo2(n23), hi2(n23)};
-    const bool bad = (nc[0] != nc[0]) | (nc[1] != nc[1]) | (nc[2] != nc[2]) | (nc[3] != nc[3]);
+    float nc0 = lo2(n01), nc1 = hi2(n01), nc2 = lo2(n23), nc3 = hi2(n23);
+    float c[4] = {fminf(fmaxf(-nc0, 0.0f), 1.0f), fminf(fmaxf(-nc1, 0.0f), 1.0f),
+                  fminf(fmaxf(-nc2, 0.0f), 1.0f), fminf(fmaxf(-nc3, 0.0f), 1.0f)};
+    const bool bad = isnan(nc0) | isnan(nc1) | isnan(nc2) | isnan(nc3);
     if (__any_sync(FULL, bad)) {  // a zero divisor (or NaN data): exact coefficient
       const float jc[4] = {J0.x, J0.y, J0.z, J0.w};
 #pragma unroll
@@ -528,67 +537,77 @@ __device__ __noinline__ bool strip_fast(const StripCtx &k, int x0, int y0, int y
         const PxPair &d = dcur[q >> 1];
         const float dn = (q & 1) ? hi2(d.n) : lo2(d.n), ds = (q & 1) ? hi2(d.s) : lo2(d.s);
         const float dw = (q & 1) ? hi2(d.w) : lo2(d.w), de = (q & 1) ? hi2(d.e) : lo2(d.e);
-        nc[q] = -coef_exact(jc[q], dn, ds, dw, de, k);
+        c[q] = coef_exact(jc[q], dn, ds, dw, de, k.q0, k.q0den);
       }
     }
-    ccur = make_float4(clamp01_neg(nc[0]), clamp01_neg(nc[1]), clamp01_neg(nc[2]), clamp01_neg(nc[3]));
-    // update of row r-1 (c_S = row r's c), or of row r itself at the image bottom
-    auto update = [&](int ro, const float4 &Jc4, const PxPair (&d)[2], const float4 &cN4, const float4 &cS4) {
-      float cE3 = __shfl_down_sync(FULL, cN4.x, 1);
-      if (east_edge) cE3 = cN4.w;
-      const float cN[4] = {cN4.x, cN4.y, cN4.z, cN4.w};
-      const float cS[4] = {cS4.x, cS4.y, cS4.z, cS4.w};
-      const float cE[4] = {cN4.y, cN4.z, cN4.w, cE3};
-      const float jc[4] = {Jc4.x, Jc4.y, Jc4.z, Jc4.w};
-      const float dn[4] = {lo2(d[0].n), hi2(d[0].n), lo2(d[1].n), hi2(d[1].n)};
-      const float ds[4] = {lo2(d[0].s), hi2(d[0].s), lo2(d[1].s), hi2(d[1].s)};
-      const float dw[4] = {lo2(d[0].w), hi2(d[0].w), lo2(d[1].w), hi2(d[1].w)};
-      const float de[4] = {lo2(d[0].e), hi2(d[0].e), lo2(d[1].e), hi2(d[1].e)};
-      float o[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const float D = add_rn(add_rn(add_rn(mul_rn(cN[q], dn[q]), mul_rn(cS[q], ds[q])), mul_rn(cN[q], dw[q])),
-                               mul_rn(cE[q], de[q]));
-        o[q] = add_rn(jc[q], mul_rn(k.ql, D));
-      }
+    mnc = fminf(mnc, fminf(fminf(c[0], c[1]), fminf(c[2], c[3])));
+    ccur[0] = pk2(c[0], c[1]);
+    ccur[1] = pk2(c[2], c[3]);
+    if (upd) {
+      // update row r-1: c_N = cprev, c_S = ccur, c_E = cprev shifted one column east
+      float cE3 = __shfl_down_sync(FULL, lo2(cprev[0]), 1);
+      if (east_edge) cE3 = hi2(cprev[1]);
+      const f2 cE01 = pk2(hi2(cprev[0]), lo2(cprev[1])), cE23 = pk2(hi2(cprev[1]), cE3);
+      // D = cN dN + cS dS + cN dW + cE dE ; J' = J + ql D  (operand order of the oracle)
+      // s(r-1) = J(r) - J(r-1) = -n(r) exactly, so cS*s(r-1) = -(cS*n(r)) and the
+      // add becomes a sub: the row's south differences need no registers
+      const f2 D01 = add2z(add2z(sub2z(mul2(cprev[0], dprev[0].n), mul2(ccur[0], dcur[0].n)),
+                                 mul2(cprev[0], dprev[0].w)), mul2(cE01, dprev[0].e));
+      const f2 D23 = add2z(add2z(sub2z(mul2(cprev[1], dprev[1].n), mul2(ccur[1], dcur[1].n)),
+                                 mul2(cprev[1], dprev[1].w)), mul2(cE23, dprev[1].e));
+      const f2 o01 = add2z(pk2(Jm.x, Jm.y), mul2(ql, D01));
+      const f2 o23 = add2z(pk2(Jm.z, Jm.w), mul2(ql, D23));
+      const float o[4] = {lo2(o01), hi2(o01), lo2(o23), hi2(o23)};
       if (out_lane) {
-        const size_t off = (size_t)(ro - k.row_lo) * cols + xl;
-        if (k.compress) {
-          *reinterpret_cast<float4 *>(k.dst + off) =
-              make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
-                          mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
+        if (COMPRESS) {
+          *reinterpret_cast<float4 *>(po) = make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
+                                                        mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
         } else {
-          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4 *>(po) = make_float4(o[0], o[1], o[2], o[3]);
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            s += (double)o[q];
-            s2 += (double)o[q] * (double)o[q];
+            const double v = (double)o[q];
+            s += v;
+            s2 = fma(v, v, s2);  // v*v is exact in double: same as s2 + v*v
           }
         }
       }
-    };
-    if (r > y0) update(r - 1, Jm, dprev, cprev, ccur);
-    if (r == y1 - 1 && r == ylast) update(r, J0, dcur, ccur, ccur);
+      po += cs;
+    }
   };
 
-  for (int r = y0;; r += 4) {
-    step(r, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
-    if (r + 1 > ylast) break;
-    step(r + 1, B1, B2, B3, B0, W2, W3, W0, DA, DB, CA, CB);
-    if (r + 2 > ylast) break;
-    step(r + 2, B2, B3, B0, B1, W3, W0, W1, DB, DA, CB, CA);
-    if (r + 3 > ylast) break;
-    step(r + 3, B3, B0, B1, B2, W0, W1, W2, DA, DB, CA, CB);
-    if (r + 4 > ylast) break;
+  // prologue: c(y0); then SH rows, each computing c(r) and updating row r-1
+  step(false, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
+  for (int r = y0 + 1; r <= y1; r += 4) {
+    step(true, B1, B2, B3, B0, W2, W3, W0, DA, DB, CA, CB);
+    if (r + 1 > y1) break;
+    step(true, B2, B3, B0, B1, W3, W0, W1, DB, DA, CB, CA);
+    if (r + 2 > y1) break;
+    step(true, B3, B0, B1, B2, W0, W1, W2, DA, DB, CA, CB);
+    if (r + 3 > y1) break;
+    step(true, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
   }
-  return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f);
+  // every value the fast path touched was inside the proven ranges
+  return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f && mnc >= 8.6736174e-19f);  // c >= 2^-60
 }
 
-__device__ __noinline__ void strip_exact(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
-  srad_strip<false>(k, x0, y0, y1, s, s2);
+struct StripRes {
+  double s, s2;
+  bool ok;
+};
+__device__ __noinline__ StripRes strip_edge(const StripCtx k, int x0, int y0, int y1) {
+  StripRes r{0.0, 0.0, false};
+  r.ok = srad_strip<true>(k, x0, y0, y1, r.s, r.s2);
+  return r;
 }
 
-__global__ void __launch_bounds__(SWARPS * 32, 2) srad_strip_kernel(Args a) {
+__device__ __noinline__ StripRes strip_exact(const StripCtx k, int x0, int y0, int y1) {
+  StripRes r{0.0, 0.0, true};
+  srad_strip<false>(k, x0, y0, y1, r.s, r.s2);
+  return r;
+}
+
+__global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args a) {
   const int warp = threadIdx.x >> 5;
   StripCtx k;
   k.src = a.src; k.dst = a.dst; k.rows = a.rows; k.cols = a.cols;
@@ -606,13 +625,18 @@ __global__ void __launch_bounds__(SWARPS * 32, 2) srad_strip_kernel(Args a) {
     const int ty = st / sx, tx = st - ty * sx;
     const int x0 = tx * SW, y0 = a.row_lo + ty * SH;
     const int y1 = min(y0 + SH, a.row_hi);
-    const double s_in = s, s2_in = s2;
-    bool ok = false;
-    if (q0ok) ok = strip_fast(k, x0, y0, y1, s, s2);
-    if (!ok) {  // outside the fast-division guard: redo with IEEE division
-      s = s_in; s2 = s2_in;
-      strip_exact(k, x0, y0, y1, s, s2);
+    StripRes res{0.0, 0.0, false};
+    if (q0ok) {
+      if (y0 >= 1 && y1 + 2 <= a.rows - 1 && y1 - y0 == SH) {  // interior strip
+        res.ok = a.compress ? strip_fast<true>(k, x0, y0, y1, res.s, res.s2)
+                            : strip_fast<false>(k, x0, y0, y1, res.s, res.s2);
+      } else {
+        res = strip_edge(k, x0, y0, y1);
+      }
     }
+    if (!res.ok) res = strip_exact(k, x0, y0, y1);  // outside the fast-division guard
+    s += res.s;
+    s2 += res.s2;
   }
   if (a.compress) return;
   block_stats(s, s2, a.partials + blockIdx.x);
