@@ -471,8 +471,32 @@ __device__ __forceinline__ f2 ncoef2(f2 Jc, const PxPair &d, f2 q0, f2 q0den, f2
 
 // Interior strips only (rows y0-1 .. y1+2 exist, so no row clamping and no
 // bottom-row special case; the kernel sends the rest to srad_strip<true>).
+// Per-warp cp.async ring of rows: RING slots of 32 float4 (the lanes'
+// columns) + the west halo value; rows are requested PD rows ahead, so a warp
+// keeps PD x 512 B in flight without spending registers on them.
+constexpr int RING = 8, PD = 6;
+struct RowRing {
+  float4 v[RING][32];
+  float w[RING][4];
+};
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Interior strips only (rows y0-1 .. y1+1 exist, so no row clamping and no
+// bottom-row special case; the kernel sends the rest to srad_strip<true>).
 template <bool COMPRESS>
-__device__ __forceinline__ bool strip_fast(const StripCtx k, int x0, int y0, int y1, double &s, double &s2) {
+__device__ __forceinline__ bool strip_fast(const StripCtx k, RowRing &R, int x0, int y0, int y1, double &s,
+                                           double &s2) {
   const int lane = threadIdx.x & 31;
   const int cols = k.cols;
   const int xl = x0 + 4 * lane;
@@ -484,33 +508,40 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, int x0, int y0, int
   const f2 q0 = bc2(k.q0), q0den = bc2(k.q0den), nq0y = bc2(-k.q0y), ql = bc2(k.ql);
   float mn = 3.0e38f, mx = -3.0e38f, mnc = 1.0f;
   const size_t cs = (size_t)cols;
-  const float *pw = k.src + (size_t)(y0 - 1) * cs + xw;            // west halo column
-  const float4 *pj = reinterpret_cast<const float4 *>(k.src + (size_t)(y0 - 1) * cs + xb);
-  const size_t cs4 = cs / 4;
+  const int nrow = y1 - y0 + 3;                                     // rows y0-1 .. y1+1
+  const float *gj = k.src + (size_t)(y0 - 1) * cs + xb;             // next row to request
+  const float *gw = k.src + (size_t)(y0 - 1) * cs + xw;
   float *po = k.dst + (size_t)(y0 - k.row_lo) * cs + xl;            // output row y0
-  auto guard = [&](const float4 &v, float w) {
-    mn = fminf(fminf(mn, w), fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
-    mx = fmaxf(fmaxf(mx, w), fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  int issued = 0;
+  auto request = [&]() {  // one commit group per row (empty past the strip)
+    if (issued < nrow) {
+      const int sl = issued % RING;
+      cp_async16(&R.v[sl][lane], gj);
+      if (lane == 0) cp_async4(&R.w[sl][0], gw);
+      gj += cs;
+      gw += cs;
+    }
+    issued++;
+    cp_commit();
   };
-  float4 B0 = __ldg(pj), B1 = __ldg(pj + cs4), B2 = __ldg(pj + 2 * cs4), B3;
-  float W1 = __ldg(pw + cs), W2 = __ldg(pw + 2 * cs), W3 = 0.f, W0 = 0.f;
-  pj += 3 * cs4;
-  pw += 3 * cs;
-  guard(B0, W1);
-  guard(B1, W1);
+#pragma unroll
+  for (int i = 0; i < PD; i++) request();
   PxPair DA[2], DB[2];
   f2 CA[2], CB[2];
 
-  // row r: window Jm (r-1), J0 (r), Jp (r+1); prefetch row r+2 into Jn.
-  // dprev/cprev: row r-1's differences / coefficients; dcur/ccur: row r's.
-  auto step = [&](bool upd, const float4 &Jm, const float4 &J0, const float4 &Jp, float4 &Jn, const float &w0,
-                  const float &wp, float &wn, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
+  // centre row i (ring index; row y0-1+i): needs rows i-1, i, i+1
+  auto step = [&](int i, bool upd, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
                   f2 (&ccur)[2]) {
-    Jn = __ldg(pj);
-    wn = __ldg(pw);
-    pj += cs4;
-    pw += cs;
-    guard(Jp, wp);
+    request();      // row i+PD
+    cp_wait<PD - 1>();  // rows <= i+1 have landed (this lane's own copies)
+    const float4 Jm = R.v[(i - 1) % RING][lane], J0 = R.v[i % RING][lane], Jp = R.v[(i + 1) % RING][lane];
+    const float w0 = R.w[i % RING][0];
+    mn = fminf(fminf(mn, w0), fminf(fminf(Jp.x, Jp.y), fminf(Jp.z, Jp.w)));
+    mx = fmaxf(fmaxf(mx, w0), fmaxf(fmaxf(Jp.x, Jp.y), fmaxf(Jp.z, Jp.w)));
+    if (i == 1) {
+      mn = fminf(mn, fminf(fminf(fminf(Jm.x, Jm.y), fminf(Jm.z, Jm.w)), fminf(fminf(J0.x, J0.y), fminf(J0.z, J0.w))));
+      mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(Jm.x, Jm.y), fmaxf(Jm.z, Jm.w)), fmaxf(fmaxf(J0.x, J0.y), fmaxf(J0.z, J0.w))));
+    }
     float W = __shfl_up_sync(FULL, J0.w, 1);
     float E = __shfl_down_sync(FULL, J0.x, 1);
     if (lane == 0) W = w0;
@@ -548,9 +579,8 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, int x0, int y0, int
       float cE3 = __shfl_down_sync(FULL, lo2(cprev[0]), 1);
       if (east_edge) cE3 = hi2(cprev[1]);
       const f2 cE01 = pk2(hi2(cprev[0]), lo2(cprev[1])), cE23 = pk2(hi2(cprev[1]), cE3);
-      // D = cN dN + cS dS + cN dW + cE dE ; J' = J + ql D  (operand order of the oracle)
-      // s(r-1) = J(r) - J(r-1) = -n(r) exactly, so cS*s(r-1) = -(cS*n(r)) and the
-      // add becomes a sub: the row's south differences need no registers
+      // D = cN dN + cS dS + cN dW + cE dE ; J' = J + ql D  (operand order of the oracle);
+      // s(r-1) = J(r) - J(r-1) = -n(r) exactly, so cS*s(r-1) = -(cS*n(r)): a sub
       const f2 D01 = add2z(add2z(sub2z(mul2(cprev[0], dprev[0].n), mul2(ccur[0], dcur[0].n)),
                                  mul2(cprev[0], dprev[0].w)), mul2(cE01, dprev[0].e));
       const f2 D23 = add2z(add2z(sub2z(mul2(cprev[1], dprev[1].n), mul2(ccur[1], dcur[1].n)),
@@ -576,17 +606,14 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, int x0, int y0, int
     }
   };
 
-  // prologue: c(y0); then SH rows, each computing c(r) and updating row r-1
-  step(false, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
-  for (int r = y0 + 1; r <= y1; r += 4) {
-    step(true, B1, B2, B3, B0, W2, W3, W0, DA, DB, CA, CB);
-    if (r + 1 > y1) break;
-    step(true, B2, B3, B0, B1, W3, W0, W1, DB, DA, CB, CA);
-    if (r + 2 > y1) break;
-    step(true, B3, B0, B1, B2, W0, W1, W2, DA, DB, CA, CB);
-    if (r + 3 > y1) break;
-    step(true, B0, B1, B2, B3, W1, W2, W3, DB, DA, CB, CA);
+  // prologue: c(y0) (ring row 1); then SH rows, each computing c(r) and updating row r-1
+  step(1, false, DB, DA, CB, CA);
+  for (int i = 2; i < nrow - 1; i += 2) {
+    step(i, true, DA, DB, CA, CB);
+    if (i + 1 >= nrow - 1) break;
+    step(i + 1, true, DB, DA, CB, CA);
   }
+  cp_wait<0>();  // nothing in flight into the ring when the next strip starts
   // every value the fast path touched was inside the proven ranges
   return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f && mnc >= 8.6736174e-19f);  // c >= 2^-60
 }
@@ -620,6 +647,7 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
   const int nrows = a.row_hi - a.row_lo;
   const int sy = (nrows + SH - 1) / SH;
   const int strips = sx * sy;
+  __shared__ RowRing rings[SWARPS];
   double s = 0.0, s2 = 0.0;
   for (int st = blockIdx.x * SWARPS + warp; st < strips; st += gridDim.x * SWARPS) {
     const int ty = st / sx, tx = st - ty * sx;
@@ -627,9 +655,9 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
     const int y1 = min(y0 + SH, a.row_hi);
     StripRes res{0.0, 0.0, false};
     if (q0ok) {
-      if (y0 >= 1 && y1 + 2 <= a.rows - 1 && y1 - y0 == SH) {  // interior strip
-        res.ok = a.compress ? strip_fast<true>(k, x0, y0, y1, res.s, res.s2)
-                            : strip_fast<false>(k, x0, y0, y1, res.s, res.s2);
+      if (y0 >= 1 && y1 + 1 <= a.rows - 1 && y1 - y0 == SH) {  // interior strip
+        res.ok = a.compress ? strip_fast<true>(k, rings[warp], x0, y0, y1, res.s, res.s2)
+                            : strip_fast<false>(k, rings[warp], x0, y0, y1, res.s, res.s2);
       } else {
         res = strip_edge(k, x0, y0, y1);
       }
