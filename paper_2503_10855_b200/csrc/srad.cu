@@ -474,7 +474,7 @@ __device__ __forceinline__ f2 ncoef2(f2 Jc, const PxPair &d, f2 q0, f2 q0den, f2
 // Per-warp cp.async ring of rows: RING slots of 32 float4 (the lanes'
 // columns) + the west halo value; rows are requested PD rows ahead, so a warp
 // keeps PD x 512 B in flight without spending registers on them.
-constexpr int RING = 8, PD = 6;
+constexpr int RING = 8, PD = 7;  // PD-2 rows in flight past the 3-row window
 struct RowRing {
   float4 v[RING][32];
   float w[RING][4];
@@ -532,10 +532,11 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, RowRing &R, int x0,
   // centre row i (ring index; row y0-1+i): needs rows i-1, i, i+1
   auto step = [&](int i, bool upd, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
                   f2 (&ccur)[2]) {
-    request();      // row i+PD
-    cp_wait<PD - 1>();  // rows <= i+1 have landed (this lane's own copies)
+    request();          // row i+PD-1: PD+i groups committed so far
+    cp_wait<PD - 2>();  // groups 0..i+1 (rows <= i+1) have landed (this lane's own copies)
     const float4 Jm = R.v[(i - 1) % RING][lane], J0 = R.v[i % RING][lane], Jp = R.v[(i + 1) % RING][lane];
-    const float w0 = R.w[i % RING][0];
+    // the west halo value is lane 0's own copy: only lane 0 may read it
+    const float w0 = lane == 0 ? R.w[i % RING][0] : J0.x;
     mn = fminf(fminf(mn, w0), fminf(fminf(Jp.x, Jp.y), fminf(Jp.z, Jp.w)));
     mx = fmaxf(fmaxf(mx, w0), fmaxf(fmaxf(Jp.x, Jp.y), fmaxf(Jp.z, Jp.w)));
     if (i == 1) {

@@ -28,7 +28,7 @@ def _exact(got, ref):
 
 # ------------------------------------------------------------------ SRAD
 @pytest.mark.parametrize("shape,niter", [((64, 64), 3), ((100, 130), 5), ((257, 129), 4), ((1, 1), 2),
-                                         ((33, 260), 1), ((48, 48), 0), ((512, 512), 10)])
+                                         ((33, 260), 1), ((48, 48), 0), ((512, 512), 10), ((700, 1000), 3)])
 def test_srad_matches_oracle(jb, oracle, shape, niter):
     img = W.srad_image(*shape, seed=shape[0])
     out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True)
