@@ -13,7 +13,7 @@
 // the paper's GPU backend lowers to warp reductions.
 //
 // B200 design:
-//  * edge_fused_kernel: one persistent kernel per chunk of frames. A CTA owns
+//  * edge_fused_kernel: one persistent kernel for the whole batch. A CTA owns
 //    a 60x60 output tile; it stages the 70x70 clamped input tile in shared
 //    memory (twice: aligned and shifted by one column so every gaussian tap
 //    is one conflict-free 64-bit LDS of two adjacent pixels), computes the
@@ -22,9 +22,12 @@
 //    bits with warp ballots, derives zero crossings with 64-bit mask logic,
 //    computes the sobel gx^2+gy^2, and stores it | zc<<31 (4 B/px) plus a
 //    warp->block->grid max (atomicMax on the float bits, per frame).
-//  * edge_reject_kernel: g = sqrt(gx^2+gy^2) (the correctly rounded sqrt is
-//    monotone, so the max commutes with it) and out = zc && g > theta*max.  The chunk's
-//    packed scratch (<= 32 MB) is re-read from L2, not HBM.
+//  * the reject runs inside the same kernel as a second work queue: a frame
+//    whose tiles are done publishes its threshold (sqrt.rn is monotone, so
+//    zc && sqrt(g) > theta*sqrt(max g) becomes an integer compare on the
+//    packed bits), and CTAs claim its reject units between compute tiles.
+//    The packed scratch is a ring of L2-sized frame slots whose lines are
+//    discarded from L2 after the reject reads them (never written back).
 //  * a generic multi-kernel path (one kernel per stage, any gs/sz/sb) serves
 //    other filter sizes and the stage-level test entry.
 //
@@ -40,6 +43,8 @@
 // Otherwise the tile runs the exact scalar path (same kernel, block-uniform
 // branch), which follows the oracle operation by operation.
 #include <math.h>
+#include <string.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tcgen05.cuh"
@@ -92,6 +97,10 @@ struct alignas(128) Smem {
   uint32_t zcw[TH][2];    // zero crossing, bit = column within 32-col chunk
   float wmax[THREADS / 32];
   uint64_t tma_bar;       // completion of the two TMA loads of an interior tile
+  int next_tile;          // claimed by thread 0 (dynamic tile scheduler)
+  int flag;               // reject unit claimed by thread 0 (or a state, see claim_reject)
+  int hflag;              // the same for the per-tile help unit (no barrier between the two)
+  int lo;                 // that unit's threshold
 };
 
 // flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair
@@ -120,13 +129,26 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
 }
 
 struct FusedArgs {
-  CUtensorMap tmap;     // [frames*n][m] input, box {72, 70} (valid if use_tma)
+  CUtensorMap tmap;     // [frames*n][m] input, box {76, 70} (valid if use_tma)
   int use_tma;
-  const float *in;      // [frames][n][m] (chunk base)
-  uint32_t *packed;     // [frames][n][m] gradient bits | zc << 31
-  unsigned *fmax;       // [frames] max gradient bits (chunk base)
+  const float *in;      // [frames][n][m]
+  float *out;           // [frames][n][m] edge maps
+  uint32_t *packed;     // ring [ring][slot_px]: gradient bits | zc << 31
+  unsigned *fmax;       // [frames] max gx^2+gy^2 bits
+  unsigned *done;       // [frames] finished tiles; tiles+1 once lo[f] is published
+  unsigned *rdone;      // [frames] finished reject units
+  unsigned long long *ready;  // [frames] (1 << 32 | threshold) once published
+  unsigned *pub;        // [frames] publisher election
+  unsigned *rj;         // [frames] claimed reject units
+  unsigned *sched;      // [0] next compute tile, [1] reject frame cursor
   const int *flags;
+  float theta;
   int n, m, frames, tiles_x, tiles_y;
+  int ring;             // frame slots in the packed ring
+  int units, unit_px;   // reject units per frame, pixels per unit (multiple of 1024)
+  int vec4;             // frame_px % 4 == 0 and out 16-byte aligned
+  long long frame_px, slot_px;
+  int opts;             // experiment bits (JB_EDGE_OPTS): 1 no discard
 };
 
 // fast-path data guard: v == +-0 or 2^-60 <= v <= 2^64 (raw-bit compare)
@@ -374,7 +396,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
     const bool col_ok = oc < TW && (!BORDER || x0 + oc < m);
     const int scol = min(oc, TW - 1);
     const int orow0 = rb * 15;
-    uint32_t *prow = a.packed + ((size_t)f * n + y0 + orow0) * m + x0 + scol;
+    uint32_t *prow = a.packed + (size_t)(f % a.ring) * a.slot_px + (size_t)(y0 + orow0) * m + x0 + scol;
     float sx[9], sy[9];
 #pragma unroll
     for (int q = 0; q < 9; q++) { sx[q] = c_sx[q]; sy[q] = c_sy[q]; }
@@ -428,13 +450,160 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
   bmax = warp_max(bmax);
   if (lane == 0) S.wmax[warp] = bmax;
   __syncthreads();
-  EDGE_T(4);
   if (tid == 0) {
     float v = S.wmax[0];
 #pragma unroll
     for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
     if (!(v != v)) atomicMax(a.fmax + f, __float_as_uint(v));
   }
+  EDGE_T(4);
+}
+
+// ------------------------------------------------ in-kernel reject (stage 3)
+// The reject needs the frame's max gradient, a grid-wide dependency.  Rather
+// than a second kernel over a scratch image, the persistent kernel runs it as
+// a second work queue: once a frame's tiles are all finished, its threshold
+// is published and CTAs claim the frame's reject units between compute
+// tiles.  The packed gradients live in a ring of `ring` frame slots
+// (L2-sized); a tile may only start writing slot f % ring once frame
+// f - ring is rejected.  Compute tiles are claimed from an atomic counter, so
+// every wait below is for work a running CTA already owns: no co-residency
+// assumption, no deadlock.
+//
+// All scheduling is done by thread 0 with as few L2 round trips as possible
+// (each one stalls the CTA at its next barrier): releases are one-thread
+// fences after a CTA barrier (cumulative), tile completion is a
+// fire-and-forget reduction, a reject claim is one atomicAdd ticket in the
+// steady state, and frame readiness + threshold travel in one 64-bit word.
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add(unsigned *p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// drop a 128-byte L2 line without writing it back (the ring slot is dead
+// once its reject unit has read it)
+__device__ __forceinline__ void discard_l2(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+constexpr int kNoneReady = -1, kSlotFree = -2, kAllClaimed = -3;
+
+// thread-0 scheduler state (registers of thread 0)
+struct Sched {
+  int cf;        // frame whose reject units we are drawing (ready), or -1
+  int lo;        // its threshold
+  int free_upto; // frames <= free_upto may write their ring slot
+};
+
+// thread 0, frame f finished (done[f] == tiles): compute and publish the
+// threshold on the packed bits (once, whoever wins pub[f]).
+// out = zc && sqrt(g) > thr, thr = theta * sqrt(max g) (NaN if g[0,0] is NaN:
+// the oracle's fold starts there).  sqrt.rn is monotone, so sqrt(g) > thr
+// <=> bits(g) > lo, lo = the largest bit pattern whose sqrt is <= thr.
+__device__ int publish_threshold(const FusedArgs &a, int f) {
+  fence_acq_rel();  // acquire: every tile's packed stores and atomicMax
+  const uint32_t p00 = __ldcg(a.packed + (size_t)(f % a.ring) * a.slot_px);
+  const float g00 = __fsqrt_rn(__uint_as_float(p00 & 0x7fffffffu));
+  const float thr = (g00 != g00) ? g00 : mul_rn(a.theta, __fsqrt_rn(__uint_as_float(__ldcg(a.fmax + f))));
+  int lo;
+  if (thr != thr) {
+    lo = 0x7fffffff;  // nothing passes
+  } else if (thr < 0.0f) {
+    lo = -1;          // every non-NaN gradient passes
+  } else {
+    int b = (int)min(__float_as_uint(mul_rn(thr, thr)), 0x7f800000u);
+    while (b > 0 && __fsqrt_rn(__int_as_float(b)) > thr) b--;
+    while (b < 0x7f800000 && !(__fsqrt_rn(__int_as_float(b + 1)) > thr)) b++;
+    lo = b;
+  }
+  atomicExch(a.ready + f, (1ull << 32) | (unsigned)lo);
+  return lo;
+}
+
+// thread 0: claim the next reject unit if its frame is ready.  sched[1] is
+// the frame cursor and rj[f] hands out frame f's units as atomicAdd tickets
+// (a CAS loop here is a 444-CTA retry storm); an over-claim just means
+// "frame exhausted" and advances the cursor.
+__device__ int claim_reject(const FusedArgs &a, Sched &q) {
+  const unsigned tpf = (unsigned)(a.tiles_x * a.tiles_y);
+  for (;;) {
+    if (q.cf >= 0) {
+      const unsigned u = atomicAdd(a.rj + q.cf, 1u);
+      if (u < (unsigned)a.units) return q.cf * a.units + (int)u;
+      atomicCAS(a.sched + 1, (unsigned)q.cf, (unsigned)q.cf + 1);
+      q.cf = -1;
+    }
+    const unsigned f = ld_relaxed(a.sched + 1);
+    if (f >= (unsigned)a.frames) return kAllClaimed;
+    const unsigned long long r = ld_relaxed64(a.ready + f);
+    if (r >> 32) {
+      q.lo = (int)(unsigned)r;
+    } else {
+      if (ld_relaxed(a.done + f) != tpf || atomicCAS(a.pub + f, 0u, 1u) != 0u) return kNoneReady;
+      q.lo = publish_threshold(a, (int)f);
+    }
+    q.cf = (int)f;
+  }
+}
+
+__device__ __forceinline__ float reject_px(uint32_t p, int lo) {
+  const int g = (int)(p & 0x7fffffffu);
+  return ((p >> 31) && g > lo && g <= 0x7f800000) ? 1.0f : 0.0f;
+}
+
+// the whole CTA: reject unit `unit` with threshold `lo` (from thread 0)
+__device__ void reject_unit(const FusedArgs &a, int unit, int lo) {
+  const int f = unit / a.units, u = unit - f * a.units;
+  const long long b0 = (long long)u * a.unit_px;
+  const long long cnt = min((long long)a.unit_px, a.frame_px - b0);
+  const uint32_t *src = a.packed + (size_t)(f % a.ring) * a.slot_px + b0;
+  float *dst = a.out + (size_t)f * a.frame_px + b0;
+  if (a.vec4) {
+    const int n4 = (int)(cnt >> 2);
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+    for (int base = 0; base < n4; base += THREADS) {
+      const int i = base + threadIdx.x;
+      if (i < n4) {
+        const uint4 p = __ldcg(s4 + i);
+        __stcs(d4 + i, make_float4(reject_px(p.x, lo), reject_px(p.y, lo), reject_px(p.z, lo), reject_px(p.w, lo)));
+      }
+      __syncwarp();
+      // the slot base and unit start are 4 KB aligned: lane 8k starts a line
+      if (!(a.opts & 1) && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
+    }
+  } else {
+    for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), lo);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel();  // release: the slot's reads are done
+    red_add(a.rdone + f, 1u);
+  }
+}
+
+// thread 0: may frame f write its ring slot?  Checks frames f-ring .. f-ring+2
+// with one round trip of independent loads and remembers the answer.
+__device__ bool slot_free(const FusedArgs &a, Sched &q, int f) {
+  if (f < a.ring || f <= q.free_upto) return true;
+  const int g = f - a.ring;
+  const unsigned r0 = ld_relaxed(a.rdone + g);
+  const unsigned r1 = g + 1 < a.frames ? ld_relaxed(a.rdone + g + 1) : 0u;
+  const unsigned r2 = g + 2 < a.frames ? ld_relaxed(a.rdone + g + 2) : 0u;
+  const unsigned U = (unsigned)a.units;
+  if (r0 < U) return false;
+  q.free_upto = r1 < U ? f : (r2 < U ? f + 1 : f + 2);
+  fence_acq_rel();  // acquire: the old frame's reads precede our stores
+  return true;
 }
 
 __global__ void __launch_bounds__(THREADS, 3)
@@ -444,25 +613,55 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n, m = a.m;
-  const int total = a.tiles_x * a.tiles_y * a.frames;
+  const int tpf = a.tiles_x * a.tiles_y;
+  const int total = tpf * a.frames;
   const int filters_fast = a.flags[0];
   const bool sobel_std = a.flags[1] != 0;
+  Sched q{-1, 0, -1};
   if (tid == 0) {
     tc::mbar_init(&S.tma_bar, 1);
     tc::fence_mbar_init();
+    const int t = (int)atomicAdd(a.sched, 1u);
+    S.next_tile = t;
+    if (t < total && a.use_tma) {
+      int f, y0, x0;
+      tile_origin(a, t, f, y0, x0);
+      if (tile_interior(a, y0, x0)) stage_tile_tma(S, a, t);
+    }
   }
   __syncthreads();
   uint32_t tma_phase = 0;
-  if ((int)blockIdx.x < total && a.use_tma && tid == 0) {
-    int f, y0, x0;
-    tile_origin(a, blockIdx.x, f, y0, x0);
-    if (tile_interior(a, y0, x0)) stage_tile_tma(S, a, blockIdx.x);
-  }
+  int tile = S.next_tile;
+  __syncthreads();  // thread 0 rewrites next_tile below
   EDGE_T0();
 
-  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  while (tile < total) {
     int f, y0, x0;
     tile_origin(a, tile, f, y0, x0);
+    // ---- the ring slot of frame f must be rejected (help while waiting)
+    for (;;) {
+      if (tid == 0) {
+        int v = kSlotFree;
+        if (!slot_free(a, q, f)) {
+          v = claim_reject(a, q);
+          if (v == kAllClaimed) v = kNoneReady;  // the slot's last units are in flight
+        }
+        S.flag = v;
+        S.lo = q.lo;
+      }
+      __syncthreads();
+      const int v = S.flag;
+      if (v == kSlotFree) break;
+      if (v >= 0) {
+        reject_unit(a, v, S.lo);
+      } else {
+        if (tid == 0) __nanosleep(256);
+        __syncthreads();
+      }
+    }
+    EDGE_T(6);
+    int claim = 0;
+    if (tid == 0) claim = (int)atomicAdd(a.sched, 1u);  // consumed after stage 0
     const bool interior = tile_interior(a, y0, x0);
     bool ok = true;
     if (a.use_tma && interior) {
@@ -505,10 +704,10 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         const int r = warp + i * (THREADS / 32);
         if (r < IR) {
 #pragma unroll
-          for (int q = 0; q < 3; q++) {
-            const int c = q * 32 + lane;
+          for (int q2 = 0; q2 < 3; q2++) {
+            const int c = q2 * 32 + lane;
             if (c < IR) {
-              const float v = vals[i][q];
+              const float v = vals[i][q2];
               ok &= pix_ok(v);
               S.inA[r][c] = v;
               S.raw[r][c + 3] = v;
@@ -517,16 +716,16 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         }
       }
     }
+    if (tid == 0) S.next_tile = claim;
     const int all_ok = __syncthreads_and(ok);
     EDGE_T(0);
+    const int claimed = S.next_tile;
     const bool border = (y0 < 2) || (x0 < 2) || (y0 + SR - 2 > n) || (x0 + SR - 2 > m);
-    int next = tile + (int)gridDim.x < total ? tile + (int)gridDim.x : -1;
-    if (next >= 0 && a.use_tma) {
+    int next = -1;
+    if (claimed < total && a.use_tma) {
       int nf, ny0, nx0;
-      tile_origin(a, next, nf, ny0, nx0);
-      if (!tile_interior(a, ny0, nx0)) next = -1;  // staged at its start instead
-    } else {
-      next = -1;
+      tile_origin(a, claimed, nf, ny0, nx0);
+      if (tile_interior(a, ny0, nx0)) next = claimed;  // else staged at its start
     }
     if (filters_fast && all_ok) {
       if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, next);
@@ -535,40 +734,37 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     } else {
       edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, next);
     }
+    // ---- tile done + help the reject queue along (one unit per tile).  The
+    // barrier at the end of edge_tile orders the CTA's packed stores before
+    // thread 0's release fence (cumulative); the atomicMax is thread 0's own.
+    if (tid == 0) {
+      const int v = claim_reject(a, q);  // independent of the fence: overlaps it
+      fence_acq_rel();
+      red_add(a.done + f, 1u);
+      S.hflag = v;
+      S.lo = q.lo;
+    }
+    __syncthreads();
+    EDGE_T(7);
+    if (S.hflag >= 0) reject_unit(a, S.hflag, S.lo);
+    EDGE_T(5);
+    tile = claimed;
   }
-}
-
-__global__ void edge_reject_kernel(const uint32_t *__restrict__ packed,
-                                   const unsigned *__restrict__ fmax, float theta,
-                                   float *__restrict__ out, int frames, long long frame_px) {
-  const long long total4 = (long long)frames * frame_px / 4;  // frame_px % 4 == 0 path
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i * 4;
-    const int f = (int)(e / frame_px);
-    const float g00 = __fsqrt_rn(__uint_as_float(__ldg(packed + (size_t)f * frame_px) & 0x7fffffffu));
-    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __fsqrt_rn(__uint_as_float(__ldg(fmax + f))));
-    const uint4 p = __ldg(reinterpret_cast<const uint4 *>(packed) + i);
-    float4 o;
-    o.x = ((p.x >> 31) && __fsqrt_rn(__uint_as_float(p.x & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
-    o.y = ((p.y >> 31) && __fsqrt_rn(__uint_as_float(p.y & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
-    o.z = ((p.z >> 31) && __fsqrt_rn(__uint_as_float(p.z & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
-    o.w = ((p.w >> 31) && __fsqrt_rn(__uint_as_float(p.w & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
-    __stcs(reinterpret_cast<float4 *>(out) + i, o);
-  }
-}
-
-__global__ void edge_reject_scalar_kernel(const uint32_t *__restrict__ packed,
-                                          const unsigned *__restrict__ fmax, float theta,
-                                          float *__restrict__ out, int frames, long long frame_px) {
-  const long long total = (long long)frames * frame_px;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int f = (int)(i / frame_px);
-    const float g00 = __fsqrt_rn(__uint_as_float(packed[(size_t)f * frame_px] & 0x7fffffffu));
-    const float thr = (g00 != g00) ? g00 : mul_rn(theta, __fsqrt_rn(__uint_as_float(fmax[f])));
-    const uint32_t p = packed[i];
-    out[i] = ((p >> 31) && __fsqrt_rn(__uint_as_float(p & 0x7fffffffu)) > thr) ? 1.0f : 0.0f;
+  // ---- drain: every compute tile is claimed; finish the reject queue
+  for (;;) {
+    if (tid == 0) {
+      S.flag = claim_reject(a, q);
+      S.lo = q.lo;
+    }
+    __syncthreads();
+    const int v = S.flag;
+    if (v == kAllClaimed) break;
+    if (v >= 0) {
+      reject_unit(a, v, S.lo);
+    } else {
+      if (tid == 0) __nanosleep(512);
+      __syncthreads();
+    }
   }
 }
 
@@ -734,23 +930,41 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
                        nullptr, nullptr, nullptr, s);
 
   const size_t frame_px = (size_t)n * m;
-  // chunk so the packed gradient scratch stays L2-resident (<= 32 MiB)
-  size_t chunk = (32ull << 20) / (frame_px * 4);
-  if (chunk < 1) chunk = 1;
-  if (chunk > batch) chunk = batch;
-  const size_t packed_bytes = ((chunk * frame_px * 4 + 255) / 256) * 256;
-  const size_t fmax_bytes = ((batch * 4 + 255) / 256) * 256;
-  char *ws = (char *)workspace(packed_bytes + fmax_bytes + 256, s);
+  const int tiles_x = (int)((m + TW - 1) / TW), tiles_y = (int)((n + TH - 1) / TH);
+  const int tpf = tiles_x * tiles_y;
+  JB_REQUIRE((uint64_t)tpf * batch < (1ull << 31), "edge_detection: batch too large");
+  // packed-gradient ring: as many frame slots as fit ~40 MB of L2 (>= 2)
+  const size_t slot_px = (frame_px + 1023) / 1024 * 1024;
+  size_t ring = (40ull << 20) / (slot_px * 4);
+  if (ring < 2) ring = 2;
+  if (ring > batch) ring = batch;
+  // reject units: one per ~two compute tiles, whole 4 KB blocks of lines
+  const size_t unit_px = ((2 * frame_px + tpf - 1) / tpf + 1023) / 1024 * 1024;
+  const size_t units = (frame_px + unit_px - 1) / unit_px;
+  const size_t ring_bytes = ring * slot_px * 4;
+  const size_t pf = ((batch * 8 + 255) / 256) * 256;  // one per-frame array (<= 8 B/frame)
+  // control block: fmax | done | rdone | pub | rj | ready (u64) | sched[2] + flags[2]
+  const size_t ctl_bytes = 6 * pf + 256;
+  char *ws = (char *)workspace(ring_bytes + ctl_bytes, s);
   if (!ws) return JB_ECUDA;
   uint32_t *packed = (uint32_t *)ws;
-  unsigned *fmax = (unsigned *)(ws + packed_bytes);
-  int *flags = (int *)(ws + packed_bytes + fmax_bytes);
+  char *ctl = ws + ring_bytes;
+  FusedArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.fmax = (unsigned *)ctl;
+  fa.done = (unsigned *)(ctl + pf);
+  fa.rdone = (unsigned *)(ctl + 2 * pf);
+  fa.pub = (unsigned *)(ctl + 3 * pf);
+  fa.rj = (unsigned *)(ctl + 4 * pf);
+  fa.ready = (unsigned long long *)(ctl + 5 * pf);
+  fa.sched = (unsigned *)(ctl + 6 * pf);
+  int *flags = (int *)(ctl + 6 * pf + 128);
 
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_gauss, gf, 49 * 4, 0, cudaMemcpyDeviceToDevice, s));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_struct, st, 9 * 4, 0, cudaMemcpyDeviceToDevice, s));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_sx, sx, 9 * 4, 0, cudaMemcpyDeviceToDevice, s));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_sy, sy, 9 * 4, 0, cudaMemcpyDeviceToDevice, s));
-  JB_CHECK_CUDA(cudaMemsetAsync(fmax, 0, batch * 4, s));
+  JB_CHECK_CUDA(cudaMemsetAsync(ctl, 0, 6 * pf + 128, s));
   edge_check_kernel<<<1, 32, 0, s>>>(gf, st, sx, sy, flags);
   JB_LAUNCHED("edge_check");
 
@@ -762,40 +976,32 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
     JB_CHECK_CUDA(cudaFuncSetAttribute(edge_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set[dev] = true;
   }
-  const int tiles_x = (int)((m + TW - 1) / TW), tiles_y = (int)((n + TH - 1) / TH);
-  for (size_t f0 = 0; f0 < batch; f0 += chunk) {
-    const int frames = (int)((batch - f0 < chunk) ? batch - f0 : chunk);
-    FusedArgs fa;
-    fa.in = in + f0 * frame_px;
-    fa.packed = packed;
-    fa.fmax = fmax + f0;
-    fa.flags = flags;
-    fa.n = (int)n; fa.m = (int)m; fa.frames = frames; fa.tiles_x = tiles_x; fa.tiles_y = tiles_y;
-    fa.use_tma = 0;
-    if (m % 4 == 0 && ((uintptr_t)fa.in % 16) == 0 && tmap_encode_fn() != nullptr) {
-      const uint64_t dims[2] = {m, n * (uint64_t)frames};
-      const uint64_t strides[1] = {m * 4};
-      const uint32_t box[2] = {(uint32_t)RP, (uint32_t)IR};
-      fa.use_tma = make_tmap_f32(&fa.tmap, fa.in, 2, dims, strides, box, 0) ? 1 : 0;
-    }
-    const int total = tiles_x * tiles_y * frames;
-    const int grid = total < sm_count() * 3 ? total : sm_count() * 3;
-    void *tok = prof_begin("edge_fused", s);
-    edge_fused_kernel<<<grid, THREADS, smem, s>>>(fa);
-    prof_end(tok, s);
-    JB_LAUNCHED("edge_fused");
-    const long long work = (long long)frames * (long long)frame_px;
-    if (frame_px % 4 == 0 && ((uintptr_t)out % 16) == 0) {
-      edge_reject_kernel<<<grid_for(work / 4, 256), 256, 0, s>>>(packed, fmax + f0, theta,
-                                                                 out + f0 * frame_px, frames,
-                                                                 (long long)frame_px);
-    } else {
-      edge_reject_scalar_kernel<<<grid_for(work, 256), 256, 0, s>>>(packed, fmax + f0, theta,
-                                                                    out + f0 * frame_px, frames,
-                                                                    (long long)frame_px);
-    }
-    JB_LAUNCHED("edge_reject");
+  fa.in = in;
+  fa.out = out;
+  fa.packed = packed;
+  fa.flags = flags;
+  fa.theta = theta;
+  fa.n = (int)n; fa.m = (int)m; fa.frames = (int)batch; fa.tiles_x = tiles_x; fa.tiles_y = tiles_y;
+  fa.ring = (int)ring; fa.units = (int)units; fa.unit_px = (int)unit_px;
+  fa.vec4 = frame_px % 4 == 0 && ((uintptr_t)out % 16) == 0;
+  fa.frame_px = (long long)frame_px; fa.slot_px = (long long)slot_px;
+  {
+    const char *e = getenv("JB_EDGE_OPTS");
+    fa.opts = e ? atoi(e) : 0;
   }
+  fa.use_tma = 0;
+  if (m % 4 == 0 && ((uintptr_t)in % 16) == 0 && tmap_encode_fn() != nullptr) {
+    const uint64_t dims[2] = {m, n * (uint64_t)batch};
+    const uint64_t strides[1] = {m * 4};
+    const uint32_t box[2] = {(uint32_t)RP, (uint32_t)IR};
+    fa.use_tma = make_tmap_f32(&fa.tmap, in, 2, dims, strides, box, 0) ? 1 : 0;
+  }
+  const long long total = (long long)tpf * batch;
+  const int grid = total < sm_count() * 3 ? (int)total : sm_count() * 3;
+  void *tok = prof_begin("edge_fused", s);
+  edge_fused_kernel<<<grid, THREADS, smem, s>>>(fa);
+  prof_end(tok, s);
+  JB_LAUNCHED("edge_fused");
   return JB_OK;
 }
 

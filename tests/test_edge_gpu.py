@@ -26,7 +26,10 @@ def test_edge_matches_golden(jb, name):
 
 
 @pytest.mark.parametrize("shape", [(1, 60, 60), (2, 61, 59), (3, 128, 200), (1, 7, 5), (1, 1, 1),
-                                   (2, 1080, 1920), (4, 121, 245)])
+                                   (2, 1080, 1920), (4, 121, 245),
+                                   # more frames than packed-ring slots (slot reuse), and an odd
+                                   # width (no TMA, scalar reject units)
+                                   (12, 1080, 1920), (7, 1080, 1918)])
 def test_edge_fused_vs_oracle(jb, oracle, shape):
     b, n, m = shape
     g, st, sx, sy, th = W.edge_filters()
@@ -74,3 +77,14 @@ def test_edge_device_tensors_and_execute(jb, oracle):
     _bits_equal(out.cpu().numpy(), oracle.edge(x[None], g, st, sx, sy, th)[0])
     out2 = jb.execute("edge_detection", [96, 128, 7, 3, 3], [x, g, st, sx, sy, th])
     _bits_equal(out2, out.cpu().numpy())
+
+
+@pytest.mark.parametrize("theta", [0.0, -0.0, -0.5, 1.0, 0.999, 3.0e38, float("inf"), float("nan")])
+def test_edge_threshold_cases(jb, oracle, theta):
+    """The in-kernel reject compares packed gradient bits against a per-frame
+    threshold derived from theta * sqrt(max); it must agree with the oracle's
+    float compare for every theta, including signed zero, inf and NaN."""
+    g, st, sx, sy, _ = W.edge_filters()
+    x = np.stack([W.edge_frame(130, 190, seed=s) for s in range(3)])
+    th = np.float32(theta)
+    _bits_equal(jb.edge_detection(x, g, st, sx, sy, th), oracle.edge(x, g, st, sx, sy, th))

@@ -25,7 +25,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 8)()
 lib.jb_edge_stage_clocks(buf)
-v = np.array(list(buf)[:5], dtype=np.float64)
-names = ["stage0 load+guard", "gaussian", "laplacian", "zero-cross", "sobel+store+max"]
-for n_, c in zip(names, v): print(f"{n_:22s} {c / v.sum() * 100:5.1f}%")
+v = np.array(list(buf)[:8], dtype=np.float64)
+names = ["stage0 load+guard", "gaussian", "laplacian", "zero-cross", "sobel+store+max", "reject help", "slot wait", "done+publish"]
+for n_, c in zip(names, v): print(f"{n_:22s} {c / v.sum() * 100:5.1f}%  {c / 3 / 444 / 1.9e3:9.1f} us/CTA/call")
 PY
