@@ -98,6 +98,7 @@ struct alignas(128) Smem {
   float wmax[THREADS / 32];
   uint64_t tma_bar;       // completion of the two TMA loads of an interior tile
   int next_tile;          // claimed by thread 0 (dynamic tile scheduler)
+  int nt_f, nt_y0, nt_x0; // its frame and origin (computed once, by thread 0)
   int flag;               // reject unit claimed by thread 0 (or a state, see claim_reject)
   int hflag;              // the same for the per-tile help unit (no barrier between the two)
   int lo;                 // that unit's threshold
@@ -130,6 +131,7 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
 
 struct FusedArgs {
   CUtensorMap tmap;     // [frames*n][m] input, box {76, 70} (valid if use_tma)
+  CUtensorMap pmap;     // [ring][n][m] packed ring, box {60, 60, 1} (valid if use_tma)
   int use_tma;
   const float *in;      // [frames][n][m]
   float *out;           // [frames][n][m] edge maps
@@ -148,6 +150,7 @@ struct FusedArgs {
   int units, unit_px;   // reject units per frame, pixels per unit (multiple of 1024)
   int vec4;             // frame_px % 4 == 0 and out 16-byte aligned
   long long frame_px, slot_px;
+  int lag;              // tiles of frame f + lag run the reject units of frame f
   int opts;             // experiment bits (JB_EDGE_OPTS): 1 no discard
 };
 
@@ -175,9 +178,7 @@ __device__ __forceinline__ bool tile_interior(const FusedArgs &a, int y0, int x0
 
 // one thread: stage an interior tile's input with one TMA box load into
 // S.raw; completion on S.tma_bar
-__device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int tile) {
-  int f, y0, x0;
-  tile_origin(a, tile, f, y0, x0);
+__device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int f, int y0, int x0) {
   tc::fence_proxy_async_smem();  // the generic-proxy accesses of raw/inA are done
   tc::mbar_arrive_expect_tx(&S.tma_bar, IR * RP * 4);
   // the chunk is a 2-D [frames*n][m] tensor: interior tiles never cross frames
@@ -189,8 +190,8 @@ __device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int 
 // otherwise the oracle's operation order with single-rounding scalar ops.
 // BORDER: the tile's halo leaves the frame (pads / clamped replicas needed).
 template <bool FAST, bool BORDER, bool SOBEL_STD = false>
-__device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
-                                          int lane, int warp, int next_tile) {
+__device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
+                                          int lane, int warp, bool prefetch, int nf, int ny0, int nx0) {
   const int n = a.n, m = a.m;
   // ---- stage 1: gaussian on the 64x64 smoothed region
   {
@@ -247,7 +248,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
   __syncthreads();
   EDGE_T(1);
   // raw/inA are free from here on: prefetch the next (interior) tile by TMA
-  if (next_tile >= 0 && tid == 0) stage_tile_tma(S, a, next_tile);
+  if (prefetch && tid == 0) stage_tile_tma(S, a, nf, ny0, nx0);
   // out-of-frame smoothed positions take the clamped in-frame value, which is
   // what the gradient's clamp-to-edge indexing reads
   if (BORDER) {
@@ -390,6 +391,7 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
 
   // ---- stage 2c: sobel gradient, pack with zc, block max
   float bmax = 0.0f;
+  unsigned amax = 0;
   {
     const int cc = warp & 1, rb = warp >> 1;
     const int oc = cc * 32 + lane;
@@ -397,6 +399,9 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
     const int scol = min(oc, TW - 1);
     const int orow0 = rb * 15;
     uint32_t *prow = a.packed + (size_t)(f % a.ring) * a.slot_px + (size_t)(y0 + orow0) * m + x0 + scol;
+    // TMA path: the packed tile goes to smem (aliasing inA, dead after the
+    // gaussian) and leaves with one bulk tensor store; the box clips borders
+    uint32_t(*P)[TW] = reinterpret_cast<uint32_t(*)[TW]>(&S.inA[0][0]);
     float sx[9], sy[9];
 #pragma unroll
     for (int q = 0; q < 9; q++) { sx[q] = c_sx[q]; sy[q] = c_sy[q]; }
@@ -438,7 +443,10 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
             // hence monotone) sqrt, so max(sqrt(a)) = sqrt(max(a))
             const float g = add_rn(mul_rn(gx, gx), mul_rn(gy, gy));
             const unsigned z = (S.zcw[orow0 + k][cc] >> lane) & 1u;
-            if (col_ok && (!BORDER || y0 + orow0 + k < n)) {
+            if (a.use_tma) {
+              if (oc < TW) P[orow0 + k][oc] = __float_as_uint(g) | (z << 31);
+              if (col_ok && (!BORDER || y0 + orow0 + k < n)) bmax = fmaxf(bmax, g);
+            } else if (col_ok && (!BORDER || y0 + orow0 + k < n)) {
               prow[(size_t)k * m] = __float_as_uint(g) | (z << 31);
               bmax = fmaxf(bmax, g);  // max of gx^2+gy^2 (ignores NaN like the fold)
             }
@@ -447,16 +455,24 @@ __device__ __forceinline__ void edge_tile(Smem &S, const FusedArgs &a, int f, in
       }
     }
   }
+  if (a.use_tma) tc::fence_proxy_async_smem();  // P -> async proxy
   bmax = warp_max(bmax);
   if (lane == 0) S.wmax[warp] = bmax;
   __syncthreads();
   if (tid == 0) {
+    if (a.use_tma) {
+      tc::tma_store_3d(&a.pmap, &S.inA[0][0], x0, y0, f % a.ring);
+      tc::bulk_commit();
+    }
     float v = S.wmax[0];
 #pragma unroll
     for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
-    if (!(v != v)) atomicMax(a.fmax + f, __float_as_uint(v));
+    // thread 0's atom: its return value (consumed a tile later, flush_done)
+    // tells that the max has been performed before the tile is counted
+    if (!(v != v)) amax = atomicMax(a.fmax + f, __float_as_uint(v));
   }
   EDGE_T(4);
+  return amax;
 }
 
 // ------------------------------------------------ in-kernel reject (stage 3)
@@ -499,10 +515,29 @@ constexpr int kNoneReady = -1, kSlotFree = -2, kAllClaimed = -3;
 
 // thread-0 scheduler state (registers of thread 0)
 struct Sched {
-  int cf;        // frame whose reject units we are drawing (ready), or -1
-  int lo;        // its threshold
-  int free_upto; // frames <= free_upto may write their ring slot
+  int free_upto;  // frames <= free_upto may write their ring slot
+  int sp_base;    // first frame of the in-flight slot probe, or -1
+  unsigned sp[3]; // rdone of frames sp_base .. sp_base+2
+  int pd;         // frame of the tile whose bulk store is in flight (not yet counted), or -1
+  unsigned pd_max;// that tile's atomicMax result (consumed before it is counted)
+  int ru;         // reject unit assigned to the current tile, or -1
+  unsigned long long rr;  // ready word of its frame (loaded at tile start)
+  unsigned rdn;   // done count of its frame (loaded at tile start)
 };
+
+// thread 0: count the tile whose bulk store is in flight as done, once the
+// store has completed (all but the newest group, or all) and its atomicMax
+// has been performed (its return value consumed).  No fence: both writes
+// are complete at L2 -- the coherence point the readers' ld.cg go to --
+// before the count is sent.
+__device__ __forceinline__ void flush_done(const FusedArgs &a, Sched &q, bool newest_pending) {
+  if (q.pd < 0) return;
+  if (newest_pending) tc::bulk_wait<1>();
+  else tc::bulk_wait<0>();
+  if (q.pd_max == 0xffffffffu) red_add(a.done + q.pd, 0u);  // never true: orders the red after the atom
+  red_add(a.done + q.pd, 1u);
+  q.pd = -1;
+}
 
 // thread 0, frame f finished (done[f] == tiles): compute and publish the
 // threshold on the packed bits (once, whoever wins pub[f]).
@@ -525,43 +560,45 @@ __device__ int publish_threshold(const FusedArgs &a, int f) {
     while (b < 0x7f800000 && !(__fsqrt_rn(__int_as_float(b + 1)) > thr)) b++;
     lo = b;
   }
-  atomicExch(a.ready + f, (1ull << 32) | (unsigned)lo);
-  return lo;
+  // reject_px's bound: zc=1 puts the sign bit on, so "zc && lo < g <= inf"
+  // is  A <= (int)p <= (int)0xff800000  with A = (lo + 1) - 2^31
+  const int A = (int)((unsigned)(lo + 1) - 0x80000000u);
+  atomicExch(a.ready + f, (1ull << 32) | (unsigned)A);
+  return A;
 }
 
-// thread 0: claim the next reject unit if its frame is ready.  sched[1] is
-// the frame cursor and rj[f] hands out frame f's units as atomicAdd tickets
-// (a CAS loop here is a 444-CTA retry storm); an over-claim just means
-// "frame exhausted" and advances the cursor.
-__device__ int claim_reject(const FusedArgs &a, Sched &q) {
+// thread 0: the compare bound of frame f given its probed ready word and
+// done count; publishes it if the frame is complete and nobody has; returns
+// false when the frame is not ready yet.
+__device__ bool frame_bound(const FusedArgs &a, int f, unsigned long long r, unsigned d, int &A) {
+  if (r >> 32) {
+    A = (int)(unsigned)r;
+    return true;
+  }
   const unsigned tpf = (unsigned)(a.tiles_x * a.tiles_y);
+  if (d == tpf && atomicCAS(a.pub + f, 0u, 1u) == 0u) {
+    A = publish_threshold(a, f);
+    return true;
+  }
+  return false;
+}
+
+// thread 0: spin until frame f is ready (the caller has no pending work
+// anyone could be waiting on); returns its compare bound
+__device__ int wait_frame(const FusedArgs &a, int f) {
   for (;;) {
-    if (q.cf >= 0) {
-      const unsigned u = atomicAdd(a.rj + q.cf, 1u);
-      if (u < (unsigned)a.units) return q.cf * a.units + (int)u;
-      atomicCAS(a.sched + 1, (unsigned)q.cf, (unsigned)q.cf + 1);
-      q.cf = -1;
-    }
-    const unsigned f = ld_relaxed(a.sched + 1);
-    if (f >= (unsigned)a.frames) return kAllClaimed;
-    const unsigned long long r = ld_relaxed64(a.ready + f);
-    if (r >> 32) {
-      q.lo = (int)(unsigned)r;
-    } else {
-      if (ld_relaxed(a.done + f) != tpf || atomicCAS(a.pub + f, 0u, 1u) != 0u) return kNoneReady;
-      q.lo = publish_threshold(a, (int)f);
-    }
-    q.cf = (int)f;
+    int A;
+    if (frame_bound(a, f, ld_relaxed64(a.ready + f), ld_relaxed(a.done + f), A)) return A;
+    __nanosleep(200);
   }
 }
 
-__device__ __forceinline__ float reject_px(uint32_t p, int lo) {
-  const int g = (int)(p & 0x7fffffffu);
-  return ((p >> 31) && g > lo && g <= 0x7f800000) ? 1.0f : 0.0f;
+__device__ __forceinline__ float reject_px(uint32_t p, int A) {
+  return ((int)p >= A && (int)p <= (int)0xff800000u) ? 1.0f : 0.0f;
 }
 
-// the whole CTA: reject unit `unit` with threshold `lo` (from thread 0)
-__device__ void reject_unit(const FusedArgs &a, int unit, int lo) {
+// the whole CTA: reject unit `unit` with compare bound `A` (from thread 0)
+__device__ void reject_unit(const FusedArgs &a, int unit, int A) {
   const int f = unit / a.units, u = unit - f * a.units;
   const long long b0 = (long long)u * a.unit_px;
   const long long cnt = min((long long)a.unit_px, a.frame_px - b0);
@@ -575,35 +612,50 @@ __device__ void reject_unit(const FusedArgs &a, int unit, int lo) {
       const int i = base + threadIdx.x;
       if (i < n4) {
         const uint4 p = __ldcg(s4 + i);
-        __stcs(d4 + i, make_float4(reject_px(p.x, lo), reject_px(p.y, lo), reject_px(p.z, lo), reject_px(p.w, lo)));
+        __stcs(d4 + i, make_float4(reject_px(p.x, A), reject_px(p.y, A), reject_px(p.z, A), reject_px(p.w, A)));
       }
       __syncwarp();
       // the slot base and unit start are 4 KB aligned: lane 8k starts a line
       if (!(a.opts & 1) && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
     }
   } else {
-    for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), lo);
+    for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), A);
   }
+  // every read of the unit's slot lines has returned (the values were
+  // stored): the count needs no fence
   __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_acq_rel();  // release: the slot's reads are done
-    red_add(a.rdone + f, 1u);
-  }
+  if (threadIdx.x == 0) red_add(a.rdone + f, 1u);
 }
 
-// thread 0: may frame f write its ring slot?  Checks frames f-ring .. f-ring+2
-// with one round trip of independent loads and remembers the answer.
+// thread 0: may frame f write its ring slot?  Uses the probe of rdone issued
+// one tile earlier when it covers f; otherwise loads (stall) -- rare.
 __device__ bool slot_free(const FusedArgs &a, Sched &q, int f) {
   if (f < a.ring || f <= q.free_upto) return true;
-  const int g = f - a.ring;
-  const unsigned r0 = ld_relaxed(a.rdone + g);
-  const unsigned r1 = g + 1 < a.frames ? ld_relaxed(a.rdone + g + 1) : 0u;
-  const unsigned r2 = g + 2 < a.frames ? ld_relaxed(a.rdone + g + 2) : 0u;
   const unsigned U = (unsigned)a.units;
-  if (r0 < U) return false;
-  q.free_upto = r1 < U ? f : (r2 < U ? f + 1 : f + 2);
-  fence_acq_rel();  // acquire: the old frame's reads precede our stores
+  if (q.sp_base >= 0 && q.sp_base <= f - a.ring) {  // consume the probe
+    const int k = f - a.ring - q.sp_base;  // 0..2: frames before f-ring were free (free_upto)
+    int c = 0;
+    while (c < 3 && q.sp[c] >= U) c++;
+    q.sp_base = -1;
+    if (c > k) {
+      q.free_upto = f + (c - 1 - k);
+      return true;
+    }
+  }
+  const int g = f - a.ring;
+  if (ld_relaxed(a.rdone + g) < U) return false;
+  q.free_upto = f;
   return true;
+}
+
+// thread 0, after the slot check of frame f: probe frames f+1-ring .. f+3-ring
+__device__ __forceinline__ void slot_probe(const FusedArgs &a, Sched &q, int f) {
+  if (q.sp_base >= 0 || f + 1 < a.ring || q.free_upto > f) return;
+  const int g = f + 1 - a.ring;
+  q.sp_base = g;
+  q.sp[0] = ld_relaxed(a.rdone + g);
+  q.sp[1] = g + 1 < a.frames ? ld_relaxed(a.rdone + g + 1) : 0u;
+  q.sp[2] = g + 2 < a.frames ? ld_relaxed(a.rdone + g + 2) : 0u;
 }
 
 __global__ void __launch_bounds__(THREADS, 3)
@@ -617,51 +669,62 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   const int total = tpf * a.frames;
   const int filters_fast = a.flags[0];
   const bool sobel_std = a.flags[1] != 0;
-  Sched q{-1, 0, -1};
+  Sched q;
+  q.free_upto = -1; q.sp_base = -1; q.sp[0] = q.sp[1] = q.sp[2] = 0; q.pd = -1; q.pd_max = 0;
+  q.ru = -1; q.rr = 0; q.rdn = 0;
+  // Reject units are assigned statically: tile j (< units) of frame f + lag
+  // runs unit j of frame f at its end, so no queue is needed on the hot
+  // path; the last `lag` frames are drained through a ticket counter.
+  const int lag = a.lag;
+  // Tiles are claimed two ahead: the claim issued during tile t is resolved
+  // (origin computed once, broadcast through smem) during tile t+1, and the
+  // input of tile t+1 is prefetched by TMA during tile t.
+  unsigned claim2 = 0;
+  auto publish_desc = [&](int t) {  // thread 0
+    int f = 0, y0 = 0, x0 = 0;
+    if (t < total) tile_origin(a, t, f, y0, x0);
+    S.next_tile = t;
+    S.nt_f = f; S.nt_y0 = y0; S.nt_x0 = x0;
+  };
   if (tid == 0) {
     tc::mbar_init(&S.tma_bar, 1);
     tc::fence_mbar_init();
-    const int t = (int)atomicAdd(a.sched, 1u);
-    S.next_tile = t;
-    if (t < total && a.use_tma) {
-      int f, y0, x0;
-      tile_origin(a, t, f, y0, x0);
-      if (tile_interior(a, y0, x0)) stage_tile_tma(S, a, t);
-    }
+    publish_desc((int)atomicAdd(a.sched, 1u));
+    if (S.next_tile < total && a.use_tma && tile_interior(a, S.nt_y0, S.nt_x0))
+      stage_tile_tma(S, a, S.nt_f, S.nt_y0, S.nt_x0);
   }
   __syncthreads();
+  int tile = S.next_tile, f = S.nt_f, y0 = S.nt_y0, x0 = S.nt_x0;  // current tile
+  __syncthreads();
+  if (tid == 0) {
+    publish_desc((int)atomicAdd(a.sched, 1u));
+    claim2 = atomicAdd(a.sched, 1u);
+  }
+  __syncthreads();
+  int t1 = S.next_tile, f1 = S.nt_f, y1 = S.nt_y0, x1 = S.nt_x0;  // the next tile
   uint32_t tma_phase = 0;
-  int tile = S.next_tile;
-  __syncthreads();  // thread 0 rewrites next_tile below
   EDGE_T0();
 
   while (tile < total) {
-    int f, y0, x0;
-    tile_origin(a, tile, f, y0, x0);
-    // ---- the ring slot of frame f must be rejected (help while waiting)
-    for (;;) {
-      if (tid == 0) {
-        int v = kSlotFree;
-        if (!slot_free(a, q, f)) {
-          v = claim_reject(a, q);
-          if (v == kAllClaimed) v = kNoneReady;  // the slot's last units are in flight
-        }
-        S.flag = v;
-        S.lo = q.lo;
+    // ---- the ring slot of frame f must be rejected; probe this tile's
+    // reject frame (consumed at the tile's end)
+    if (tid == 0) {
+      tc::bulk_wait_read<0>();  // the last packed tile has left smem
+      if (!slot_free(a, q, f)) {
+        flush_done(a, q, false);  // someone may be waiting on it
+        while (ld_relaxed(a.rdone + f - a.ring) < (unsigned)a.units) __nanosleep(128);
+        q.free_upto = f;
       }
-      __syncthreads();
-      const int v = S.flag;
-      if (v == kSlotFree) break;
-      if (v >= 0) {
-        reject_unit(a, v, S.lo);
-      } else {
-        if (tid == 0) __nanosleep(256);
-        __syncthreads();
+      slot_probe(a, q, f);
+      const int j = tile - f * tpf;
+      q.ru = -1;
+      if (f >= lag && j < a.units) {
+        q.ru = (f - lag) * a.units + j;
+        q.rr = ld_relaxed64(a.ready + f - lag);
+        q.rdn = ld_relaxed(a.done + f - lag);
       }
     }
     EDGE_T(6);
-    int claim = 0;
-    if (tid == 0) claim = (int)atomicAdd(a.sched, 1u);  // consumed after stage 0
     const bool interior = tile_interior(a, y0, x0);
     bool ok = true;
     if (a.use_tma && interior) {
@@ -716,55 +779,73 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         }
       }
     }
-    if (tid == 0) S.next_tile = claim;
+    // thread 0: resolve the claim issued one tile ago (tile t+2), issue the next
+    if (tid == 0) {
+      publish_desc((int)claim2);
+      claim2 = atomicAdd(a.sched, 1u);
+    }
     const int all_ok = __syncthreads_and(ok);
     EDGE_T(0);
-    const int claimed = S.next_tile;
+    const int t2 = S.next_tile, f2 = S.nt_f, y2 = S.nt_y0, x2 = S.nt_x0;
+    const bool prefetch = t1 < total && a.use_tma && tile_interior(a, y1, x1);
     const bool border = (y0 < 2) || (x0 < 2) || (y0 + SR - 2 > n) || (x0 + SR - 2 > m);
-    int next = -1;
-    if (claimed < total && a.use_tma) {
-      int nf, ny0, nx0;
-      tile_origin(a, claimed, nf, ny0, nx0);
-      if (tile_interior(a, ny0, nx0)) next = claimed;  // else staged at its start
-    }
+    unsigned amax;
     if (filters_fast && all_ok) {
-      if (border) edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, next);
-      else if (sobel_std) edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, next);
-      else edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp, next);
+      if (border) amax = edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+      else if (sobel_std) amax = edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+      else amax = edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     } else {
-      edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, next);
+      amax = edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     }
-    // ---- tile done + help the reject queue along (one unit per tile).  The
-    // barrier at the end of edge_tile orders the CTA's packed stores before
-    // thread 0's release fence (cumulative); the atomicMax is thread 0's own.
+    // ---- tile done + help the reject queue along (at most one unit per
+    // tile).  TMA path: this tile's bulk store was just issued and the
+    // previous tile is counted (its store has landed by now).  STG path: the
+    // barrier at the end of edge_tile orders the CTA's stores before thread
+    // 0's release fence (cumulative).
     if (tid == 0) {
-      const int v = claim_reject(a, q);  // independent of the fence: overlaps it
-      fence_acq_rel();
-      red_add(a.done + f, 1u);
+      if (a.use_tma) {
+        flush_done(a, q, true);
+        q.pd = f;
+        q.pd_max = amax;
+      } else {
+        fence_acq_rel();
+        red_add(a.done + f, 1u);
+      }
+      int v = q.ru, A = 0;
+      if (v >= 0) {
+        const int rf = v / a.units;
+        if (!frame_bound(a, rf, q.rr, q.rdn, A)) {
+          flush_done(a, q, false);
+          A = wait_frame(a, rf);
+        }
+      }
       S.hflag = v;
-      S.lo = q.lo;
+      S.lo = A;
     }
     __syncthreads();
     EDGE_T(7);
     if (S.hflag >= 0) reject_unit(a, S.hflag, S.lo);
     EDGE_T(5);
-    tile = claimed;
+    tile = t1; f = f1; y0 = y1; x0 = x1;
+    t1 = t2; f1 = f2; y1 = y2; x1 = x2;
   }
-  // ---- drain: every compute tile is claimed; finish the reject queue
+  // ---- drain: every compute tile is claimed; the last `lag` frames'
+  // reject units go through a ticket counter
+  const int tail0 = max(a.frames - lag, 0);
+  const int tail_units = (a.frames - tail0) * a.units;
   for (;;) {
     if (tid == 0) {
-      S.flag = claim_reject(a, q);
-      S.lo = q.lo;
+      flush_done(a, q, false);
+      const int u = (int)atomicAdd(a.sched + 1, 1u);
+      int A = 0;
+      if (u < tail_units) A = wait_frame(a, tail0 + u / a.units);
+      S.flag = u < tail_units ? tail0 * a.units + u : -1;
+      S.lo = A;
     }
     __syncthreads();
     const int v = S.flag;
-    if (v == kAllClaimed) break;
-    if (v >= 0) {
-      reject_unit(a, v, S.lo);
-    } else {
-      if (tid == 0) __nanosleep(512);
-      __syncthreads();
-    }
+    if (v < 0) break;
+    reject_unit(a, v, S.lo);
   }
 }
 
@@ -933,9 +1014,9 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   const int tiles_x = (int)((m + TW - 1) / TW), tiles_y = (int)((n + TH - 1) / TH);
   const int tpf = tiles_x * tiles_y;
   JB_REQUIRE((uint64_t)tpf * batch < (1ull << 31), "edge_detection: batch too large");
-  // packed-gradient ring: as many frame slots as fit ~40 MB of L2 (>= 2)
+  // packed-gradient ring: as many frame slots as fit ~64 MB of L2 (>= 2)
   const size_t slot_px = (frame_px + 1023) / 1024 * 1024;
-  size_t ring = (40ull << 20) / (slot_px * 4);
+  size_t ring = (64ull << 20) / (slot_px * 4);
   if (ring < 2) ring = 2;
   if (ring > batch) ring = batch;
   // reject units: one per ~two compute tiles, whole 4 KB blocks of lines
@@ -983,6 +1064,10 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   fa.theta = theta;
   fa.n = (int)n; fa.m = (int)m; fa.frames = (int)batch; fa.tiles_x = tiles_x; fa.tiles_y = tiles_y;
   fa.ring = (int)ring; fa.units = (int)units; fa.unit_px = (int)unit_px;
+  // lag: tiles in flight (3 per CTA: current + two claimed) span ~2.3
+  // 1080p frames, so frame f is complete by the time frame f+4's tiles end;
+  // lag <= ring - 2 keeps the slot of frame f + ring free when it is needed
+  fa.lag = (int)(ring >= 6 ? 4 : (ring >= 3 ? ring - 2 : 1));
   fa.vec4 = frame_px % 4 == 0 && ((uintptr_t)out % 16) == 0;
   fa.frame_px = (long long)frame_px; fa.slot_px = (long long)slot_px;
   {
@@ -995,6 +1080,11 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
     const uint64_t strides[1] = {m * 4};
     const uint32_t box[2] = {(uint32_t)RP, (uint32_t)IR};
     fa.use_tma = make_tmap_f32(&fa.tmap, in, 2, dims, strides, box, 0) ? 1 : 0;
+    // the packed ring as [ring][n][m] u32 (bit copies: the f32 map type is fine)
+    const uint64_t pdims[3] = {m, n, (uint64_t)ring};
+    const uint64_t pstrides[2] = {m * 4, slot_px * 4};
+    const uint32_t pbox[3] = {(uint32_t)TW, (uint32_t)TH, 1};
+    if (fa.use_tma && !make_tmap_f32(&fa.pmap, packed, 3, pdims, pstrides, pbox, 0)) fa.use_tma = 0;
   }
   const long long total = (long long)tpf * batch;
   const int grid = total < sm_count() * 3 ? (int)total : sm_count() * 3;
