@@ -86,6 +86,14 @@ __constant__ float c_sx[9];
 __constant__ float c_sy[9];
 
 constexpr int RP = 76;                 // raw row pitch: input columns x0-8 .. x0+67
+// thread 0's scheduler state (kept in smem: fewer live registers in the tile code)
+struct Sched {
+  int free_upto;  // frames <= free_upto may write their ring slot
+  int sp_base;    // first frame of the in-flight slot probe, or -1
+  int pd;         // frame of the tile whose bulk store is in flight (not yet counted), or -1
+  int ru;         // reject unit assigned to the current tile, or -1
+};
+
 struct alignas(128) Smem {
   // raw[r][c] = input(y0-5+r, x0-8+c): the 16-byte-aligned TMA box (TMA needs
   // an aligned inner start coordinate); the pairs (x, x+1) with x - x0 odd
@@ -102,6 +110,7 @@ struct alignas(128) Smem {
   int flag;               // reject unit claimed by thread 0 (or a state, see claim_reject)
   int hflag;              // the same for the per-tile help unit (no barrier between the two)
   int lo;                 // that unit's threshold
+  Sched q;                // thread 0 only
 };
 
 // flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair
@@ -185,6 +194,42 @@ __device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int 
   tc::tma_load_2d(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, f * a.n + y0 - 5);
 }
 
+extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ Smem &smem_tile() {
+  const uint32_t pad = (128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u;
+  return *reinterpret_cast<Smem *>(smem_raw + pad);
+}
+
+// stage 1, fast path: packed gaussian of 8 smoothed rows x 2 columns per
+// lane.  Not inlined: one copy is shared by every tile variant, which keeps
+// the hot code inside the instruction cache.
+__device__ __noinline__ void gauss_fast(int warp, int lane) {
+  Smem &S = smem_tile();
+  const int r0 = warp * 8;
+  unsigned long long acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; o++) acc[o] = 0ull;  // (+0.0f, +0.0f)
+#pragma unroll
+  for (int iy = 0; iy < 14; iy++) {
+    const unsigned long long *ra = reinterpret_cast<const unsigned long long *>(&S.inA[r0 + iy][0]);
+    const unsigned long long *rb = reinterpret_cast<const unsigned long long *>(&S.raw[r0 + iy][0]);
+    unsigned long long v[7];
+    // pair (x0-5+2l+j, +1): even j from inA, odd j from raw at 2l+j+3
+#pragma unroll
+    for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + ((j + 3) >> 1)] : ra[lane + (j >> 1)];
+#pragma unroll
+    for (int o = 0; o < 8; o++) {
+      const int i = iy - o;
+      if (i >= 0 && i < 7) {
+#pragma unroll
+        for (int j = 0; j < 7; j++) acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[i * 7 + j]));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < 8; o++) *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
+}
+
 // stages 1-2 of one 60x60 tile whose clamped input is staged in S.inA/S.raw.
 // FAST: packed/FTZ gaussian, FMNMX morphology, FFMA sobel (guarded exact);
 // otherwise the oracle's operation order with single-rounding scalar ops.
@@ -197,28 +242,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   {
     const int r0 = warp * 8;  // 8 smoothed rows per warp, 2 columns per lane
     if (FAST) {
-      unsigned long long acc[8];
-#pragma unroll
-      for (int o = 0; o < 8; o++) acc[o] = 0ull;  // (+0.0f, +0.0f)
-#pragma unroll
-      for (int iy = 0; iy < 14; iy++) {
-        const unsigned long long *ra = reinterpret_cast<const unsigned long long *>(&S.inA[r0 + iy][0]);
-        const unsigned long long *rb = reinterpret_cast<const unsigned long long *>(&S.raw[r0 + iy][0]);
-        unsigned long long v[7];
-        // pair (x0-5+2l+j, +1): even j from inA, odd j from raw at 2l+j+3
-#pragma unroll
-        for (int j = 0; j < 7; j++) v[j] = (j & 1) ? rb[lane + ((j + 3) >> 1)] : ra[lane + (j >> 1)];
-#pragma unroll
-        for (int o = 0; o < 8; o++) {
-          const int i = iy - o;
-          if (i >= 0 && i < 7) {
-#pragma unroll
-            for (int j = 0; j < 7; j++) acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[i * 7 + j]));
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 0; o < 8; o++) *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
+      gauss_fast(warp, lane);
     } else {
       float2 acc[8];
 #pragma unroll
@@ -514,27 +538,17 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 constexpr int kNoneReady = -1, kSlotFree = -2, kAllClaimed = -3;
 
 // thread-0 scheduler state (registers of thread 0)
-struct Sched {
-  int free_upto;  // frames <= free_upto may write their ring slot
-  int sp_base;    // first frame of the in-flight slot probe, or -1
-  unsigned sp[3]; // rdone of frames sp_base .. sp_base+2
-  int pd;         // frame of the tile whose bulk store is in flight (not yet counted), or -1
-  unsigned pd_max;// that tile's atomicMax result (consumed before it is counted)
-  int ru;         // reject unit assigned to the current tile, or -1
-  unsigned long long rr;  // ready word of its frame (loaded at tile start)
-  unsigned rdn;   // done count of its frame (loaded at tile start)
-};
 
 // thread 0: count the tile whose bulk store is in flight as done, once the
 // store has completed (all but the newest group, or all) and its atomicMax
 // has been performed (its return value consumed).  No fence: both writes
 // are complete at L2 -- the coherence point the readers' ld.cg go to --
 // before the count is sent.
-__device__ __forceinline__ void flush_done(const FusedArgs &a, Sched &q, bool newest_pending) {
+__device__ __forceinline__ void flush_done(const FusedArgs &a, Sched &q, unsigned pd_max, bool newest_pending) {
   if (q.pd < 0) return;
   if (newest_pending) tc::bulk_wait<1>();
   else tc::bulk_wait<0>();
-  if (q.pd_max == 0xffffffffu) red_add(a.done + q.pd, 0u);  // never true: orders the red after the atom
+  if (pd_max == 0xffffffffu) red_add(a.done + q.pd, 0u);  // never true: orders the red after the atom
   red_add(a.done + q.pd, 1u);
   q.pd = -1;
 }
@@ -627,15 +641,23 @@ __device__ void reject_unit(const FusedArgs &a, int unit, int A) {
   if (threadIdx.x == 0) red_add(a.rdone + f, 1u);
 }
 
+// thread 0's in-flight load results: registers, so that nothing waits for
+// them before they are consumed (a tile later)
+struct Inflight {
+  unsigned sp[3];          // rdone of frames q.sp_base .. +2
+  unsigned long long rr;   // ready word of the current tile's reject frame
+  unsigned rdn;            // its done count
+};
+
 // thread 0: may frame f write its ring slot?  Uses the probe of rdone issued
 // one tile earlier when it covers f; otherwise loads (stall) -- rare.
-__device__ bool slot_free(const FusedArgs &a, Sched &q, int f) {
+__device__ bool slot_free(const FusedArgs &a, Sched &q, const Inflight &r, int f) {
   if (f < a.ring || f <= q.free_upto) return true;
   const unsigned U = (unsigned)a.units;
   if (q.sp_base >= 0 && q.sp_base <= f - a.ring) {  // consume the probe
     const int k = f - a.ring - q.sp_base;  // 0..2: frames before f-ring were free (free_upto)
     int c = 0;
-    while (c < 3 && q.sp[c] >= U) c++;
+    while (c < 3 && r.sp[c] >= U) c++;
     q.sp_base = -1;
     if (c > k) {
       q.free_upto = f + (c - 1 - k);
@@ -649,29 +671,30 @@ __device__ bool slot_free(const FusedArgs &a, Sched &q, int f) {
 }
 
 // thread 0, after the slot check of frame f: probe frames f+1-ring .. f+3-ring
-__device__ __forceinline__ void slot_probe(const FusedArgs &a, Sched &q, int f) {
+__device__ __forceinline__ void slot_probe(const FusedArgs &a, Sched &q, Inflight &r, int f) {
   if (q.sp_base >= 0 || f + 1 < a.ring || q.free_upto > f) return;
   const int g = f + 1 - a.ring;
   q.sp_base = g;
-  q.sp[0] = ld_relaxed(a.rdone + g);
-  q.sp[1] = g + 1 < a.frames ? ld_relaxed(a.rdone + g + 1) : 0u;
-  q.sp[2] = g + 2 < a.frames ? ld_relaxed(a.rdone + g + 2) : 0u;
+  r.sp[0] = ld_relaxed(a.rdone + g);
+  r.sp[1] = g + 1 < a.frames ? ld_relaxed(a.rdone + g + 1) : 0u;
+  r.sp[2] = g + 2 < a.frames ? ld_relaxed(a.rdone + g + 2) : 0u;
 }
 
 __global__ void __launch_bounds__(THREADS, 3)
 edge_fused_kernel(const __grid_constant__ FusedArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const uint32_t pad = (128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u;
-  Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
+  Smem &S = smem_tile();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n, m = a.m;
   const int tpf = a.tiles_x * a.tiles_y;
   const int total = tpf * a.frames;
   const int filters_fast = a.flags[0];
   const bool sobel_std = a.flags[1] != 0;
-  Sched q;
-  q.free_upto = -1; q.sp_base = -1; q.sp[0] = q.sp[1] = q.sp[2] = 0; q.pd = -1; q.pd_max = 0;
-  q.ru = -1; q.rr = 0; q.rdn = 0;
+  Sched &q = S.q;
+  unsigned pd_max = 0;  // thread 0: atomicMax result of the tile in flight
+  Inflight rf_{{0u, 0u, 0u}, 0ull, 0u};
+  if (tid == 0) {
+    q.free_upto = -1; q.sp_base = -1; q.pd = -1; q.ru = -1;
+  }
   // Reject units are assigned statically: tile j (< units) of frame f + lag
   // runs unit j of frame f at its end, so no queue is needed on the hot
   // path; the last `lag` frames are drained through a ticket counter.
@@ -710,18 +733,18 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     // reject frame (consumed at the tile's end)
     if (tid == 0) {
       tc::bulk_wait_read<0>();  // the last packed tile has left smem
-      if (!slot_free(a, q, f)) {
-        flush_done(a, q, false);  // someone may be waiting on it
+      if (!slot_free(a, q, rf_, f)) {
+        flush_done(a, q, pd_max, false);  // someone may be waiting on it
         while (ld_relaxed(a.rdone + f - a.ring) < (unsigned)a.units) __nanosleep(128);
         q.free_upto = f;
       }
-      slot_probe(a, q, f);
+      slot_probe(a, q, rf_, f);
       const int j = tile - f * tpf;
       q.ru = -1;
       if (f >= lag && j < a.units) {
         q.ru = (f - lag) * a.units + j;
-        q.rr = ld_relaxed64(a.ready + f - lag);
-        q.rdn = ld_relaxed(a.done + f - lag);
+        rf_.rr = ld_relaxed64(a.ready + f - lag);
+        rf_.rdn = ld_relaxed(a.done + f - lag);
       }
     }
     EDGE_T(6);
@@ -804,9 +827,9 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     // 0's release fence (cumulative).
     if (tid == 0) {
       if (a.use_tma) {
-        flush_done(a, q, true);
+        flush_done(a, q, pd_max, true);
         q.pd = f;
-        q.pd_max = amax;
+        pd_max = amax;  // a register: consumed (waited for) one tile later
       } else {
         fence_acq_rel();
         red_add(a.done + f, 1u);
@@ -814,8 +837,8 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       int v = q.ru, A = 0;
       if (v >= 0) {
         const int rf = v / a.units;
-        if (!frame_bound(a, rf, q.rr, q.rdn, A)) {
-          flush_done(a, q, false);
+        if (!frame_bound(a, rf, rf_.rr, rf_.rdn, A)) {
+          flush_done(a, q, pd_max, false);
           A = wait_frame(a, rf);
         }
       }
@@ -835,7 +858,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   const int tail_units = (a.frames - tail0) * a.units;
   for (;;) {
     if (tid == 0) {
-      flush_done(a, q, false);
+      flush_done(a, q, pd_max, false);
       const int u = (int)atomicAdd(a.sched + 1, 1u);
       int A = 0;
       if (u < tail_units) A = wait_frame(a, tail0 + u / a.units);
