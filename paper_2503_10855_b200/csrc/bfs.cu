@@ -6,10 +6,15 @@
 //
 // B200 design: one persistent cooperative kernel runs every
 // level (no host round trip per level):
-//  * top-down frontier-queue expansion, thread per frontier vertex;
+//  * top-down frontier-queue expansion, thread per frontier vertex; its
+//    edges are processed in batches of 8 whose edge-id loads, visited probes
+//    and claiming atomics are each issued back to back (memory-level
+//    parallelism instead of three dependent round trips per edge);
 //  * a visited bitmap (n/8 bytes: 2 MiB at n = 2^24, L2-resident) filters
-//    the random neighbour probes before the claiming atomicOr, so the
-//    random traffic stays in the 126 MB L2 instead of HBM;
+//    the random neighbour probes before the claiming atomicOr;
+//  * levels go to a byte array (n bytes, L2-resident) instead of random
+//    4-byte writes into the HBM cost array; one coalesced pass at the end
+//    expands it to i32 costs (levels >= 254 are rare and written directly);
 //  * newly claimed vertices go to a block-local queue in shared memory
 //    (shared-memory atomics), then one global atomicAdd per block reserves
 //    space in the next frontier (block-aggregated atomics);
@@ -25,15 +30,33 @@ namespace bfs {
 
 constexpr int THREADS = 512;
 constexpr int LQ = 4096;  // block-local queue capacity
+constexpr int EB = 8;     // edges per batch
+constexpr uint8_t kUnseen = 0xFF, kDeep = 0xFE;  // level byte codes
 
 struct Args {
   const uint32_t *starting, *nedges, *edges;
   int32_t *cost;
+  uint8_t *level;     // [n] level byte (kUnseen / level / kDeep: see cost[])
   uint32_t *visited;  // bitmap
   uint32_t *q[2];     // frontier queues
   uint32_t *qsize;    // [4]: size of q[0], q[1] (+ padding)
   uint32_t n;
 };
+
+__device__ __forceinline__ void enqueue(const Args &a, uint32_t v, int nxt, uint32_t *lq, uint32_t &lcount,
+                                        uint32_t *nq) {
+  const uint32_t slot = atomicAdd(&lcount, 1u);
+  if (slot < LQ) {
+    lq[slot] = v;
+  } else {  // overflow: warp-aggregated direct append
+    const uint32_t mask = __activemask();
+    const int leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(a.qsize + nxt, __popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    nq[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = v;
+  }
+}
 
 __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
@@ -49,6 +72,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
     const uint32_t *fq = a.q[cur];
     uint32_t *nq = a.q[nxt];
     const int32_t nl = level + 1;
+    const uint8_t nb = nl < kDeep ? (uint8_t)nl : kDeep;
     // uniform trip count across the block so __syncthreads stays legal
     const uint32_t rounds = (fsize + gsize - 1) / gsize;
     for (uint32_t r = 0; r < rounds; r++) {
@@ -56,25 +80,26 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
       __syncthreads();
       const uint32_t i = r * gsize + gtid;
       if (i < fsize) {
-        const uint32_t u = fq[i];
-        const uint32_t e0 = __ldg(a.starting + u), e1 = e0 + __ldg(a.nedges + u);
-        for (uint32_t e = e0; e < e1; e++) {
-          const uint32_t v = __ldg(a.edges + e);
-          const uint32_t bit = 1u << (v & 31);
-          if (a.visited[v >> 5] & bit) continue;  // cheap L2 probe
-          const uint32_t old = atomicOr(a.visited + (v >> 5), bit);
-          if (old & bit) continue;                 // someone else claimed v
-          a.cost[v] = nl;
-          const uint32_t slot = atomicAdd(&lcount, 1u);
-          if (slot < LQ) {
-            lq[slot] = v;
-          } else {  // overflow: warp-aggregated direct append
-            const uint32_t mask = __activemask();
-            const int leader = __ffs(mask) - 1;
-            uint32_t base = 0;
-            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(a.qsize + nxt, __popc(mask));
-            base = __shfl_sync(mask, base, leader);
-            nq[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = v;
+        const uint32_t u = __ldcg(fq + i);
+        const uint32_t e0 = __ldg(a.starting + u), ne = __ldg(a.nedges + u);
+        for (uint32_t b = 0; b < ne; b += EB) {
+          uint32_t v[EB], w[EB];
+#pragma unroll
+          for (int j = 0; j < EB; j++) v[j] = b + j < ne ? __ldg(a.edges + e0 + b + j) : 0xffffffffu;
+          // probes may come from L1 (stale only towards "unseen": the
+          // atomicOr below re-checks)
+#pragma unroll
+          for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
+#pragma unroll
+          for (int j = 0; j < EB; j++) {
+            if (v[j] == 0xffffffffu) continue;
+            const uint32_t bit = 1u << (v[j] & 31);
+            if (w[j] & bit) continue;
+            const uint32_t old = atomicOr(a.visited + (v[j] >> 5), bit);
+            if (old & bit) continue;  // someone else claimed v
+            a.level[v[j]] = nb;
+            if (nb == kDeep) a.cost[v[j]] = nl;
+            enqueue(a, v[j], nxt, lq, lcount, nq);
           }
         }
       }
@@ -90,9 +115,11 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
   }
 }
 
-__global__ void bfs_init_kernel(int32_t *cost, uint32_t *visited, uint32_t n, uint32_t words, uint32_t source,
+__global__ void bfs_init_kernel(uint8_t *level, uint32_t *visited, uint32_t n, uint32_t words, uint32_t source,
                                 uint32_t *q0, uint32_t *qsize) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) cost[i] = -1;
+  const uint32_t n4 = (n + 3) / 4;  // the level array is padded to whole words
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
+    reinterpret_cast<uint32_t *>(level)[i] = 0xFFFFFFFFu;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gridDim.x * blockDim.x) visited[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     qsize[0] = 1;
@@ -101,9 +128,36 @@ __global__ void bfs_init_kernel(int32_t *cost, uint32_t *visited, uint32_t n, ui
   }
 }
 
-__global__ void bfs_seed_kernel(int32_t *cost, uint32_t *visited, uint32_t source) {
-  cost[source] = 0;
+__global__ void bfs_seed_kernel(uint8_t *level, uint32_t *visited, uint32_t source) {
+  level[source] = 0;
   visited[source >> 5] |= 1u << (source & 31);
+}
+
+// level bytes -> i32 costs (4 vertices per thread, coalesced)
+__global__ void bfs_expand_kernel(const uint8_t *level, int32_t *cost, uint32_t n, int vec) {
+  const uint32_t n4 = n / 4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (vec ? n4 : n); i += gridDim.x * blockDim.x) {
+    if (vec) {
+      const uint32_t b = __ldcs(reinterpret_cast<const unsigned int *>(level) + i);
+      int4 c;
+      const int32_t *old = cost + 4 * (size_t)i;
+      const uint32_t b0 = b & 0xff, b1 = (b >> 8) & 0xff, b2 = (b >> 16) & 0xff, b3 = b >> 24;
+      c.x = b0 == kUnseen ? -1 : (b0 == kDeep ? old[0] : (int)b0);
+      c.y = b1 == kUnseen ? -1 : (b1 == kDeep ? old[1] : (int)b1);
+      c.z = b2 == kUnseen ? -1 : (b2 == kDeep ? old[2] : (int)b2);
+      c.w = b3 == kUnseen ? -1 : (b3 == kDeep ? old[3] : (int)b3);
+      __stcs(reinterpret_cast<int4 *>(cost) + i, c);
+    } else {
+      const uint32_t b = level[i];
+      cost[i] = b == kUnseen ? -1 : (b == kDeep ? cost[i] : (int)b);
+    }
+  }
+  if (vec) {  // the tail
+    for (uint32_t i = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint32_t b = level[i];
+      cost[i] = b == kUnseen ? -1 : (b == kDeep ? cost[i] : (int)b);
+    }
+  }
 }
 
 }  // namespace bfs
@@ -122,18 +176,20 @@ extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, co
   const uint32_t words = (uint32_t)((n + 31) / 32);
   const size_t qbytes = ((n * 4 + 255) / 256) * 256;
   const size_t vbytes = ((words * 4 + 255) / 256) * 256;
-  char *ws = (char *)workspace(2 * qbytes + vbytes + 256, s);
+  const size_t lbytes = ((n + 255) / 256) * 256;
+  char *ws = (char *)workspace(2 * qbytes + vbytes + lbytes + 256, s);
   if (!ws) return JB_ECUDA;
   Args a;
   a.starting = starting; a.nedges = nedges; a.edges = edges; a.cost = cost;
   a.q[0] = (uint32_t *)ws;
   a.q[1] = (uint32_t *)(ws + qbytes);
   a.visited = (uint32_t *)(ws + 2 * qbytes);
-  a.qsize = (uint32_t *)(ws + 2 * qbytes + vbytes);
+  a.level = (uint8_t *)(ws + 2 * qbytes + vbytes);
+  a.qsize = (uint32_t *)(ws + 2 * qbytes + vbytes + lbytes);
   a.n = (uint32_t)n;
-  bfs_init_kernel<<<sm_count() * 4, 256, 0, s>>>(cost, a.visited, (uint32_t)n, words, source, a.q[0], a.qsize);
+  bfs_init_kernel<<<sm_count() * 4, 256, 0, s>>>(a.level, a.visited, (uint32_t)n, words, source, a.q[0], a.qsize);
   JB_LAUNCHED("bfs_init");
-  bfs_seed_kernel<<<1, 1, 0, s>>>(cost, a.visited, source);
+  bfs_seed_kernel<<<1, 1, 0, s>>>(a.level, a.visited, source);
   JB_LAUNCHED("bfs_seed");
   int per_sm = 0;
   JB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, THREADS, 0));
@@ -144,5 +200,8 @@ extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, co
   JB_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)bfs_kernel, dim3(grid), dim3(THREADS), args, 0, s));
   prof_end(tok, s);
   JB_LAUNCHED("bfs_levels");
+  const int vec = ((uintptr_t)cost % 16) == 0;
+  bfs_expand_kernel<<<sm_count() * 8, 256, 0, s>>>(a.level, cost, (uint32_t)n, vec);
+  JB_LAUNCHED("bfs_expand");
   return JB_OK;
 }

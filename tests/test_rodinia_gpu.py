@@ -95,6 +95,18 @@ def test_bfs_edge_cases(jb, oracle):
     assert one.tolist() == [0]
 
 
+@pytest.mark.parametrize("n", [300, 1001])
+def test_bfs_deep_chain(jb, oracle, n):
+    """A path graph: levels beyond the 254 the level bytes hold go through
+    the direct-cost fallback; odd n exercises the unaligned expand tail."""
+    s = np.arange(n, dtype=np.uint32)
+    d = np.ones(n, np.uint32)
+    d[-1] = 0
+    e = np.arange(1, n, dtype=np.uint32)
+    _exact(jb.bfs(s, d, e, 0), oracle.bfs(s, d, e, 0))
+    _exact(jb.bfs(s, d, e, 5), oracle.bfs(s, d, e, 5))
+
+
 # ------------------------------------------------------------------ backprop
 @pytest.mark.parametrize("n_in,n_hid", [(1000, 16), (65536, 16), (4097, 8), (333, 32)])
 def test_backprop_matches_oracle(jb, oracle, n_in, n_hid):
