@@ -31,6 +31,7 @@ namespace bfs {
 constexpr int THREADS = 512;
 constexpr int LQ = 4096;  // block-local queue capacity
 constexpr int EB = 8;     // edges per batch
+constexpr int VPT = 2;    // frontier vertices per thread per round
 constexpr uint8_t kUnseen = 0xFF, kDeep = 0xFE;  // level byte codes
 
 struct Args {
@@ -73,19 +74,42 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
     uint32_t *nq = a.q[nxt];
     const int32_t nl = level + 1;
     const uint8_t nb = nl < kDeep ? (uint8_t)nl : kDeep;
-    // uniform trip count across the block so __syncthreads stays legal
-    const uint32_t rounds = (fsize + gsize - 1) / gsize;
+    // Dense levels (a large share of all vertices in the frontier) scan the
+    // level bytes in vertex order instead of reading the queue: the node
+    // records and edge lists are then read nearly sequentially (coalesced)
+    // instead of one random sector pair per vertex.
+    const bool scan = level < kDeep && fsize > (a.n >> 2);
+    const uint32_t work = scan ? a.n : fsize;
+    // uniform trip count across the block so __syncthreads stays legal;
+    // VPT vertices per thread per round, their record loads issued together
+    const uint32_t per_round = gsize * VPT;
+    const uint32_t rounds = (work + per_round - 1) / per_round;
     for (uint32_t r = 0; r < rounds; r++) {
       if (threadIdx.x == 0) lcount = 0;
       __syncthreads();
-      const uint32_t i = r * gsize + gtid;
-      if (i < fsize) {
-        const uint32_t u = __ldcg(fq + i);
-        const uint32_t e0 = __ldg(a.starting + u), ne = __ldg(a.nedges + u);
-        for (uint32_t b = 0; b < ne; b += EB) {
+      uint32_t e0[VPT], ne[VPT];
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        const uint32_t i = r * per_round + k * gsize + gtid;
+        ne[k] = 0;
+        e0[k] = 0;
+        if (i < work) {
+          bool live = true;
+          uint32_t u = i;
+          if (scan) live = __ldcg(a.level + i) == (uint8_t)level;
+          else u = __ldcg(fq + i);
+          if (live) {
+            e0[k] = __ldg(a.starting + u);
+            ne[k] = __ldg(a.nedges + u);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < VPT; k++) {
+        for (uint32_t b = 0; b < ne[k]; b += EB) {
           uint32_t v[EB], w[EB];
 #pragma unroll
-          for (int j = 0; j < EB; j++) v[j] = b + j < ne ? __ldg(a.edges + e0 + b + j) : 0xffffffffu;
+          for (int j = 0; j < EB; j++) v[j] = b + j < ne[k] ? __ldg(a.edges + e0[k] + b + j) : 0xffffffffu;
           // probes may come from L1 (stale only towards "unseen": the
           // atomicOr below re-checks)
 #pragma unroll
