@@ -28,6 +28,24 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 
+#ifdef MM_TRACE
+// per-CTA phase timestamps (globaltimer ns) for tools/mm_trace.py
+__device__ unsigned long long g_mm_trace[512][12];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MM_CTA (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z))
+#define MM_T(slot) g_mm_trace[MM_CTA][slot] = gtimer()
+#define MM_ACC_BEGIN unsigned long long _mm_t = gtimer()
+#define MM_ACC(slot) g_mm_trace[MM_CTA][slot] += gtimer() - _mm_t
+#else
+#define MM_T(slot) do {} while (0)
+#define MM_ACC_BEGIN do {} while (0)
+#define MM_ACC(slot) do {} while (0)
+#endif
+
 namespace jb {
 namespace mm {
 
@@ -90,6 +108,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   const int kb0 = (int)((long long)kblocks * blockIdx.z / splitk);
   const int kb1 = (int)((long long)kblocks * (blockIdx.z + 1) / splitk);
   const int nkb = kb1 - kb0;
+  if (threadIdx.x == 0) MM_T(0);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; s++) {
@@ -116,7 +135,11 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     if (lane == 0) {
       for (int j = 0; j < nkb; j++) {
         const int s = j % STAGES;
-        if (j >= STAGES) tc::mbar_wait(&S.empty[s], ((j / STAGES) - 1) & 1);
+        {
+          MM_ACC_BEGIN;
+          if (j >= STAGES) tc::mbar_wait(&S.empty[s], ((j / STAGES) - 1) & 1);
+          MM_ACC(10);
+        }
         tc::mbar_arrive_expect_tx(&S.full[s], A_TILE + B_TILE);
         const int k0 = (kb0 + j) * BK;
         tc::tma_load_2d(S.a_raw[s], &tm_a, &S.full[s], k0, m0);
@@ -130,8 +153,13 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     constexpr uint32_t idesc = tc::idesc_tf32(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 1);
     for (int j = 0; j < nkb; j++) {
       const int s = j % STAGES, ls = j % LO_STAGES;
-      tc::mbar_wait(&S.conv[ls], (j / LO_STAGES) & 1);
+      {
+        MM_ACC_BEGIN;
+        tc::mbar_wait(&S.conv[ls], (j / LO_STAGES) & 1);
+        if (lane == 0 && j > 0) MM_ACC(6);
+      }
       tc::tc_fence_after();
+      if (lane == 0 && j == 0) MM_T(2);
       if (lane == 0) {
         const uint32_t ahi = tc::smem_u32(S.a_raw[s]), alo = tc::smem_u32(S.a_lo[ls]);
         const uint32_t bhi = tc::smem_u32(S.b_raw[s]), blo = tc::smem_u32(S.b_lo[ls]);
@@ -151,7 +179,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
         }
         tc::mma_commit(&S.empty[s]);      // raw slot may be refilled by TMA
         tc::mma_commit(&S.lo_empty[ls]);  // lo slot may be rewritten
-        if (j == nkb - 1) tc::mma_commit(&S.tmem_full);
+        if (j == nkb - 1) {
+          tc::mma_commit(&S.tmem_full);
+          MM_T(3);
+        }
       }
       __syncwarp();
     }
@@ -160,8 +191,18 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     const int ct = threadIdx.x - 64;  // 0..255
     for (int j = 0; j < nkb; j++) {
       const int s = j % STAGES, ls = j % LO_STAGES;
-      tc::mbar_wait(&S.full[s], (j / STAGES) & 1);
-      if (j >= LO_STAGES) tc::mbar_wait(&S.lo_empty[ls], ((j / LO_STAGES) - 1) & 1);
+      {
+        MM_ACC_BEGIN;
+        tc::mbar_wait(&S.full[s], (j / STAGES) & 1);
+        if (ct == 0 && j > 0) MM_ACC(7);
+      }
+      if (j == 0 && ct == 0) MM_T(1);
+      {
+        MM_ACC_BEGIN;
+        if (j >= LO_STAGES) tc::mbar_wait(&S.lo_empty[ls], ((j / LO_STAGES) - 1) & 1);
+        if (ct == 0) MM_ACC(8);
+      }
+      MM_ACC_BEGIN;
       // elementwise, layout preserving: lo = x - trunc_tf32(x) for A and B
       const float4 *ar = reinterpret_cast<const float4 *>(S.a_raw[s]);
       const float4 *br = reinterpret_cast<const float4 *>(S.b_raw[s]);
@@ -182,11 +223,13 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
                                               tf32_residual(vb[i].z), tf32_residual(vb[i].w));
       tc::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
       tc::mbar_arrive(&S.conv[ls]);
+      if (ct == 0) MM_ACC(9);
     }
     // ------------------------------------------------------ epilogue
     if (warp >= 6 || nkb == 0) goto done;  // four warps cover the 128 TMEM lanes
     tc::mbar_wait(&S.tmem_full, 0);
     tc::tc_fence_after();
+    if (ct == 0) MM_T(4);
     {
       const int q = warp & 3;  // TMEM lane quarter this warp may read
       const int row = m0 + q * 32 + lane;
@@ -221,6 +264,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
       }
     }
     tc::tc_fence_before();
+    if (ct == 0) MM_T(5);
   }
 done:
   __syncthreads();
@@ -274,6 +318,12 @@ static bool make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t
 
 using namespace jb;
 using namespace jb::mm;
+
+#ifdef MM_TRACE
+extern "C" JB_API void jb_mm_trace(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, g_mm_trace, sizeof(g_mm_trace));
+}
+#endif
 
 extern "C" jb_status jb_matmul_exact_f32(uint64_t n, uint64_t m, uint64_t l, const float *a, const float *b,
                                          float *res, void *stream) {
