@@ -8,7 +8,7 @@ prof() {  # workload kernel-regex skip
      -o gpurun_out/prof_$1 -f python bench.py --workload $1 --steps 1 --warmup 3 --no-cpu --e2e-steps 1 \
      > gpurun_out/ncu_$1.log 2>&1 || echo "ncu $1 failed" >> gpurun_out/ncu_failures.log
 }
-SPECS=${SPECS:-"edge edge_fused 4;matmul gemm_3xtf32 3;srad srad_ 3;euler euler_rk 3;bfs bfs_kernel 1;backprop bp_adjust 1;cava cava_kernel 1"}
+SPECS=${SPECS:-"edge edge_fused 3;matmul gemm_3xtf32 3;srad srad_ 3;euler euler_rk 3;bfs bfs_kernel 1;backprop bp_adjust 1;cava cava_kernel 1"}
 IFS=';' read -ra LIST <<< "$SPECS"
 for spec in "${LIST[@]}"; do
   prof $spec
