@@ -351,12 +351,30 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
                       tmap_encode_fn() != nullptr;
   if (!tma_ok) return jb_matmul_exact_f32(n, m, l, a, b, res, stream);
 
-  CUtensorMap m_a, m_b;
-  if (!make_map(&m_a, a, n, m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&m_b, b, m, l, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
-    set_error("matmul: cuTensorMapEncodeTiled failed");
-    return JB_ECUDA;
+  // tensor maps are encoded on the host (~microseconds each): keep the last
+  // pair per device, keyed by operand pointers and extents
+  struct MapCache {
+    const void *a, *b;
+    uint64_t n, m, l;
+    CUtensorMap ma, mb;
+    bool valid;
+  };
+  static MapCache cache[64] = {};
+  int cdev = 0;
+  cudaGetDevice(&cdev);
+  JB_REQUIRE(cdev >= 0 && cdev < 64, "matmul: device index out of range");
+  MapCache &mc = cache[cdev];
+  if (!(mc.valid && mc.a == a && mc.b == b && mc.n == n && mc.m == m && mc.l == l)) {
+    mc.valid = false;
+    if (!make_map(&mc.ma, a, n, m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map(&mc.mb, b, m, l, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      set_error("matmul: cuTensorMapEncodeTiled failed");
+      return JB_ECUDA;
+    }
+    mc.a = a; mc.b = b; mc.n = n; mc.m = m; mc.l = l;
+    mc.valid = true;
   }
+  const CUtensorMap &m_a = mc.ma, &m_b = mc.mb;
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
