@@ -191,7 +191,9 @@ __device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int 
   tc::fence_proxy_async_smem();  // the generic-proxy accesses of raw/inA are done
   tc::mbar_arrive_expect_tx(&S.tma_bar, IR * RP * 4);
   // the chunk is a 2-D [frames*n][m] tensor: interior tiles never cross frames
-  tc::tma_load_2d(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, f * a.n + y0 - 5);
+  // the input is read once: evict it first, so the packed ring (evict last)
+  // survives in L2 until its reject units read it
+  tc::tma_load_2d_hint(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, f * a.n + y0 - 5, tc::policy_evict_first());
 }
 
 extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -485,7 +487,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   __syncthreads();
   if (tid == 0) {
     if (a.use_tma) {
-      tc::tma_store_3d(&a.pmap, &S.inA[0][0], x0, y0, f % a.ring);
+      tc::tma_store_3d_hint(&a.pmap, &S.inA[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
       tc::bulk_commit();
     }
     float v = S.wmax[0];
