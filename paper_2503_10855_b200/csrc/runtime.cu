@@ -36,6 +36,11 @@ void *tmap_encode_fn() {
 
 bool make_tmap_f32(CUtensorMap *map, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
                    const uint32_t *box, int swizzle) {
+  return make_tmap(map, (int)CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, rank, dims, strides_bytes, box, swizzle);
+}
+
+bool make_tmap(CUtensorMap *map, int dtype, const void *base, int rank, const uint64_t *dims,
+               const uint64_t *strides_bytes, const uint32_t *box, int swizzle) {
   auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tmap_encode_fn());
   if (!fn) return false;
   cuuint64_t d[5], st[4];
@@ -46,7 +51,7 @@ bool make_tmap_f32(CUtensorMap *map, const void *base, int rank, const uint64_t 
     e[i] = 1;
     if (i + 1 < rank) st[i] = strides_bytes[i];
   }
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void *>(base), d, st, b, e,
+  CUresult r = fn(map, (CUtensorMapDataType)dtype, rank, const_cast<void *>(base), d, st, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, (CUtensorMapSwizzle)swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
