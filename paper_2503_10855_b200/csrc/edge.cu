@@ -163,11 +163,24 @@ struct FusedArgs {
   int opts;             // experiment bits (JB_EDGE_OPTS): 1 no discard
 };
 
-// fast-path data guard: v == +-0 or 2^-60 <= v <= 2^64 (raw-bit compare)
-__device__ __forceinline__ bool pix_ok(float v) {
-  const unsigned u = __float_as_uint(v);
-  return (u - 0x21800000u) <= (0x5f800000u - 0x21800000u) || (u + u) == 0u;
-}
+// fast-path data guard: every staged pixel is +0 or in [2^-60, 2^64].  On
+// the raw bits: max(u) <= bits(2^64) (rejects negatives, -0, inf, NaN) and
+// min(u - 1) >= bits(2^-60) - 1 (u = +0 wraps to 0xffffffff), accumulated
+// with 3-input integer min/max: two instructions per pixel pair.
+struct PixGuard {
+  unsigned mx = 0u, mn = 0xffffffffu;
+  __device__ __forceinline__ void add(float a) {
+    const unsigned u = __float_as_uint(a);
+    mx = max(mx, u);
+    mn = min(mn, u - 1u);
+  }
+  __device__ __forceinline__ void add2(float a, float b) {
+    const unsigned u = __float_as_uint(a), w = __float_as_uint(b);
+    mx = __vimax3_u32(mx, u, w);
+    mn = __vimin3_u32(mn, u - 1u, w - 1u);
+  }
+  __device__ __forceinline__ bool ok() const { return mx <= 0x5f800000u && mn >= 0x217fffffu; }
+};
 
 constexpr int RPW = (IR + THREADS / 32 - 1) / (THREADS / 32);  // staged rows per warp (9)
 
@@ -751,7 +764,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     }
     EDGE_T(6);
     const bool interior = tile_interior(a, y0, x0);
-    bool ok = true;
+    PixGuard pg;
     if (a.use_tma && interior) {
       // ---- stage 0 (interior): the TMA issued during the previous tile
       tc::mbar_wait(&S.tma_bar, tma_phase);
@@ -762,12 +775,12 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         const int r = warp + i * (THREADS / 32);
         if (r < IR) {
           const float v0 = S.raw[r][lane + 3], v1 = S.raw[r][lane + 35];
-          ok &= pix_ok(v0) && pix_ok(v1);
+          pg.add2(v0, v1);
           S.inA[r][lane] = v0;
           S.inA[r][lane + 32] = v1;
           if (lane < IR - 64) {
             const float v2 = S.raw[r][lane + 67];
-            ok &= pix_ok(v2);
+            pg.add(v2);
             S.inA[r][lane + 64] = v2;
           }
         }
@@ -796,7 +809,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
             const int c = q2 * 32 + lane;
             if (c < IR) {
               const float v = vals[i][q2];
-              ok &= pix_ok(v);
+              pg.add(v);
               S.inA[r][c] = v;
               S.raw[r][c + 3] = v;
             }
@@ -809,7 +822,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       publish_desc((int)claim2);
       claim2 = atomicAdd(a.sched, 1u);
     }
-    const int all_ok = __syncthreads_and(ok);
+    const int all_ok = __syncthreads_and(pg.ok());
     EDGE_T(0);
     const int t2 = S.next_tile, f2 = S.nt_f, y2 = S.nt_y0, x2 = S.nt_x0;
     const bool prefetch = t1 < total && a.use_tma && tile_interior(a, y1, x1);

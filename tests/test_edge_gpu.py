@@ -49,6 +49,7 @@ def test_edge_exact_fallback_paths(jb, oracle):
     x[0, 10:20, 10:20] = -rng.random((10, 10), dtype=np.float32)   # negative pixels
     x[1, 70:75, 100:110] = np.float32(1e-39)                         # subnormals
     x[2, 0, 0] = np.float32(np.inf)                                  # non-finite
+    x[2, 60:63, 90:93] = np.float32(-0.0)                            # negative zeros
     _bits_equal(jb.edge_detection(x, g, st, sx, sy, th), oracle.edge(x, g, st, sx, sy, th))
     st2 = st.copy(); st2[1, 1] = 0.5
     _bits_equal(jb.edge_detection(x[:2], g, st2, sx, sy, th), oracle.edge(x[:2], g, st2, sx, sy, th))
