@@ -76,6 +76,7 @@ def dist_env():
 class Dist:
     def __init__(self, backend="nccl"):
         self.rank, self.world, self.local = dist_env()
+        self.backend = backend
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
@@ -91,7 +92,8 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+        on_gpu = torch.cuda.is_available() and self.backend == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -647,8 +649,12 @@ WORKLOADS = {"edge": EdgeWorkload, "matmul": MatmulWorkload, "srad": SradWorkloa
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    d = Dist("nccl")
+    # JB_BENCH_SHARE_GPU=1 (testing only): every rank on the visible GPU(s)
+    # round-robin with a gloo control plane, to exercise the N>1 code path on
+    # a one-GPU box; its numbers are not scaling results
+    share = os.environ.get("JB_BENCH_SHARE_GPU") == "1"
+    torch.cuda.set_device(local % torch.cuda.device_count() if share else local)
+    d = Dist("gloo" if share else "nccl")
     from paper_2503_10855_b200 import _lib
     wl = WORKLOADS[args.workload](args, rank, world)
     wl.setup_device(torch)
@@ -690,7 +696,7 @@ def run_ours(args):
     _lib.prof_reset()
     _lib.prof_enable(True)
     launches0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         ms = timed(wl.step_device, args.steps)
     launches = _lib.launch_count() - launches0
     _lib.prof_enable(False)
