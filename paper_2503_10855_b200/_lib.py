@@ -41,6 +41,7 @@ SIGNATURES = {
     "jb_srad_slab_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, _vp, ctypes.c_int, _vp],
     "jb_srad_q0_f32": [_vp, _u64, _vp, _vp],
     "jb_euler_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "jb_euler_stage_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_euler_step_factor_f32": [_u64, _vp, _vp, _vp, _vp],
     "jb_euler_flux_f32": [_u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_bfs": [_u64, _u64, _vp, _vp, _vp, _u32, _vp, _vp],

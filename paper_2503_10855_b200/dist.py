@@ -8,6 +8,10 @@ gloo in the CPU tests).  What shards and how:
   SRAD         row slabs with 1 halo row above / 2 below; per iteration an
                allreduce of the f64 (sum, sum^2) pair and a halo exchange of
                the image rows                                 (srad_distributed)
+  CFD/Euler    contiguous element ranges; the halo is every element an owned
+               element's neighbour list points outside the range (one mesh row
+               above and below on the structured mesh); per RK stage a halo
+               exchange of the 5 variables              (euler_plan, euler_distributed)
   BFS, BP      replicas only
 
 The SRAD driver is written against a small backend protocol so the same host
@@ -160,3 +164,109 @@ class CudaSradBackend:
 
     def cat_rows(self, parts):
         return self.torch.cat(parts, dim=0).contiguous()
+
+
+# ------------------------------------------------------------------- CFD
+def euler_plan(neighbors, world: int, rank: int) -> dict:
+    """Element-range slab of `rank` for euler<nelr> and its halo exchange.
+
+    `neighbors` is the global i32[4, nelr] array (ids, -1 wall, -2 far field).
+    Returns the owned range [e0, e1), the slab-local neighbour ids (own
+    elements 0..n_own-1, then the halo elements in global order), and per peer
+    rank the own elements to send and the halo positions to receive.  Computed
+    once per mesh on the host (numpy)."""
+    import numpy as np
+    nb = np.asarray(neighbors)
+    nelr = nb.shape[1]
+    bounds = [partition(nelr, world, r) for r in range(world)]
+
+    def halo_of(r):
+        e0, cnt = bounds[r]
+        own = nb[:, e0:e0 + cnt]
+        ext = own[(own >= 0) & ((own < e0) | (own >= e0 + cnt))]
+        return np.unique(ext)
+
+    e0, n_own = bounds[rank]
+    e1 = e0 + n_own
+    halo = halo_of(rank)
+    own = nb[:, e0:e1]
+    loc = own.astype(np.int64).copy()
+    inside = (own >= e0) & (own < e1)
+    outside = (own >= 0) & ~inside
+    loc[inside] -= e0
+    loc[outside] = n_own + np.searchsorted(halo, own[outside])
+    starts = np.array([b[0] for b in bounds] + [nelr])
+    owner = np.searchsorted(starts, halo, side="right") - 1
+    recv = {}
+    for r in np.unique(owner):
+        pos = np.nonzero(owner == r)[0]
+        recv[int(r)] = (int(pos[0]), int(pos.size))  # contiguous: halo is sorted by global id
+    send = {}
+    for s in range(world):
+        if s == rank:
+            continue
+        h = halo_of(s)
+        mine = h[(h >= e0) & (h < e1)]
+        if mine.size:
+            send[s] = (mine - e0).astype(np.int64)
+    return dict(e0=e0, e1=e1, n_own=n_own, n_loc=n_own + halo.size, halo=halo,
+                neighbors=np.ascontiguousarray(loc.astype(np.int32)), recv=recv, send=send)
+
+
+def euler_halo_exchange(cur, plan: dict, group=None, backend=None):
+    """Fill the halo columns of the SoA slab array cur[5, n_loc] from their
+    owners (batched point-to-point send/recv of the owned values they need)."""
+    import torch
+    import torch.distributed as dist
+    n_own = plan["n_own"]
+    ops, rbufs = [], []
+    for s, idx in plan["send"].items():
+        ids = torch.as_tensor(idx, device=cur.device)
+        buf = cur.index_select(1, ids).contiguous()
+        ops.append(dist.P2POp(dist.isend, buf, s, group))
+    for r, (st, cnt) in plan["recv"].items():
+        buf = torch.empty((cur.shape[0], cnt), dtype=cur.dtype, device=cur.device)
+        ops.append(dist.P2POp(dist.irecv, buf, r, group))
+        rbufs.append((st, cnt, buf))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for st, cnt, buf in rbufs:
+        cur[:, n_own + st:n_own + st + cnt] = buf
+
+
+def euler_distributed(plan: dict, areas_own, normals_own, ff, vars_loc, iterations: int, backend,
+                      group=None, exchange=None):
+    """Rodinia euler on the slab of `plan`: `vars_loc` is the SoA f32[5, n_loc]
+    slab state (own columns first; halo columns are filled here), updated in
+    place; returns its own columns.  Per iteration the three RK stages each
+    start with a halo exchange of the stage input (no reductions: the
+    result is bit-identical to the single-device run)."""
+    import torch
+    exchange = exchange or (lambda cur: euler_halo_exchange(cur, plan, group))
+    nbrs = backend.to_device(plan["neighbors"], like=vars_loc)
+    t1, t2 = torch.empty_like(vars_loc), torch.empty_like(vars_loc)
+    for _ in range(iterations):
+        for j, (cur, dst) in enumerate(((vars_loc, t1), (t1, t2), (t2, vars_loc))):
+            exchange(cur)
+            backend.stage(plan["n_own"], plan["n_loc"], j, areas_own, nbrs, normals_own, ff, cur, vars_loc, dst)
+    return vars_loc[:, :plan["n_own"]]
+
+
+class CudaEulerBackend:
+    """libjunob200's slab stage kernel on device tensors (NCCL exchanges)."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.lib = _lib.load()
+
+    def to_device(self, a, like):
+        return self.torch.as_tensor(a).to(like.device)
+
+    def stage(self, n_own, n_loc, j, areas, nbrs, normals, ff, cur, old, dst):
+        rc = self.lib.jb_euler_stage_f32(int(n_own), int(n_loc), int(j), areas.data_ptr(), nbrs.data_ptr(),
+                                         normals.data_ptr(), ff.data_ptr(), cur.data_ptr(), old.data_ptr(),
+                                         dst.data_ptr(), self.torch.cuda.current_stream().cuda_stream)
+        if rc:
+            raise RuntimeError(f"euler_stage: {_lib.last_error()}")

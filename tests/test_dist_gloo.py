@@ -139,3 +139,65 @@ def test_frame_sharding_gathers_the_batch():
     outs = _run(2, _frames_rank)
     for o in outs:
         assert np.array_equal(o.view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------------------ CFD
+class OracleEulerBackend:
+    """CPU stand-in for CudaEulerBackend: the slab stage from the C
+    restatement's flux / step-factor on the slab-local arrays (halo columns
+    padded as walls; only the own columns are kept)."""
+
+    def __init__(self):
+        from oracle import oracle
+        self.o = oracle
+
+    def to_device(self, a, like):
+        return torch.as_tensor(a)
+
+    def stage(self, n_own, n_loc, j, areas, nbrs, normals, ff, cur, old, dst):
+        nb = np.full((4, n_loc), -1, np.int32)
+        nb[:, :n_own] = nbrs.numpy()
+        nr = np.zeros((4, 3, n_loc), np.float32)
+        nr[:, :, :n_own] = normals.numpy()
+        fl = self.o.euler_flux(nb, nr, ff.numpy(), np.ascontiguousarray(cur.numpy()))[:, :n_own]
+        o = np.ascontiguousarray(old.numpy()[:, :n_own])
+        sf = self.o.euler_step_factor(o, areas.numpy())
+        factor = sf / np.float32(4 - j)  # RK + 1 - j
+        dst[:, :n_own] = torch.from_numpy((o + factor[None, :] * fl).astype(np.float32))
+
+
+MESH_W, MESH_H, CFD_ITERS = 12, 9, 2
+
+
+def _euler_rank(rank, world):
+    from paper_2503_10855_b200 import workloads as W
+    areas, nb, normals, ff, v = W.euler_mesh(MESH_W, MESH_H, seed=3)
+    plan = D.euler_plan(nb, world, rank)
+    e0, e1 = plan["e0"], plan["e1"]
+    vl = torch.zeros((5, plan["n_loc"]), dtype=torch.float32)
+    vl[:, :plan["n_own"]] = torch.from_numpy(v[:, e0:e1])
+    out = D.euler_distributed(plan, torch.from_numpy(np.ascontiguousarray(areas[e0:e1])),
+                              torch.from_numpy(np.ascontiguousarray(normals[:, :, e0:e1])),
+                              torch.from_numpy(ff), vl, CFD_ITERS, OracleEulerBackend())
+    return out.numpy().copy()
+
+
+def test_euler_plan_structured_mesh_halo_is_one_row():
+    from paper_2503_10855_b200 import workloads as W
+    _, nb, _, _, _ = W.euler_mesh(MESH_W, MESH_H)
+    p = D.euler_plan(nb, 3, 1)
+    assert p["n_loc"] - p["n_own"] == 2 * MESH_W  # one mesh row above and below
+    assert sorted(p["recv"]) == [0, 2] and sorted(p["send"]) == [0, 2]
+    assert all(len(ix) == MESH_W for ix in p["send"].values())
+    loc = p["neighbors"]
+    assert loc.min() >= -2 and loc.max() < p["n_loc"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_euler_element_slabs_match_single_device(world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    areas, nb, normals, ff, v = W.euler_mesh(MESH_W, MESH_H, seed=3)
+    ref = oracle.euler(areas, nb, normals, ff, v, CFD_ITERS)
+    got = np.concatenate(_run(world, _euler_rank), axis=1)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
