@@ -60,7 +60,7 @@ def test_euler_emulated_slabs_match_single_device(jb, oracle, nslab):
     from paper_2503_10855_b200 import dist as D
     areas, nb, normals, ff, v = W.euler_mesh(40, 23, seed=6)
     iters = 2
-    ref = jb.euler(areas, nb, normals, ff, v, iters)
+    ref = jb.euler(iters, areas, nb, normals, ff, v)
     be = D.CudaEulerBackend()
     plans = [D.euler_plan(nb, nslab, r) for r in range(nslab)]
     state = []
