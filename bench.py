@@ -370,29 +370,49 @@ class SradWorkload(_DeviceCall):
     niter = 10
 
     def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import dist as D
         from paper_2503_10855_b200 import workloads as W
         self.rows = self.cols = 4096 if args.small else 16384
-        self.host = {"image": W.srad_image(self.rows, self.cols)}
+        img = W.srad_image(self.rows, self.cols)
+        # N > 1: row slabs of one image (strong scaling), NCCL halo exchange
+        # of the J rows + allreduce of the f64 statistics per iteration
+        self.world = world
+        self.plan = D.srad_slab(self.rows, world, rank)
+        self.own_rows = self.plan["r1"] - self.plan["r0"]
+        if world > 1:
+            img = np.ascontiguousarray(img[self.plan["r0"]:self.plan["r1"]])
+            self.scaling = "strong"
+        self.host = {"image": img}
         self.inputs_e2e = ["image"]
 
     def alloc_outputs(self, torch):
-        self.out = torch.empty((self.rows, self.cols), dtype=torch.float32, device="cuda")
-        self.pin_out = {"out": torch.empty((self.rows, self.cols), dtype=torch.float32).pin_memory()}
+        self.out = torch.empty((self.own_rows, self.cols), dtype=torch.float32, device="cuda")
+        self.pin_out = {"out": torch.empty((self.own_rows, self.cols), dtype=torch.float32).pin_memory()}
+        if self.world > 1:
+            from paper_2503_10855_b200 import dist as D
+            self.be = D.CudaSradBackend()
 
     def outputs_e2e(self):
         return [("out", self.out)]
 
     def config(self, world):
+        par = "single GPU" if world == 1 else f"row slabs/{world}: NCCL halo rows + f64 allreduce per iteration"
         return {"workload": f"srad<{self.rows},{self.cols}> niter={self.niter} lambda=0.5 (Rodinia srad_v1)",
-                "parallelism": "single GPU", "l2": "1 GiB image >> 126 MB L2"}
+                "parallelism": par, "l2": "1 GiB image >> 126 MB L2"}
 
     def units_per_step(self):
         return self.niter
 
     def algorithmic_bytes_per_unit(self):
-        return 8 * self.rows * self.cols  # read J + write J' per iteration
+        # read J + write J' per iteration, of this rank's rows
+        return 8 * self.own_rows * self.cols
 
     def step_device(self):
+        if self.world > 1:
+            from paper_2503_10855_b200 import dist as D
+            res = D.srad_distributed(self.dev["image"], self.niter, 0.5, self.rows, self.cols, self.be)
+            self.out.copy_(res)
+            return
         self.check_rc(self.lib.jb_srad_f32(self.rows, self.cols, self.niter, 0.5, self.dev["image"].data_ptr(),
                                            self.out.data_ptr(), None, self.stream.cuda_stream))
 
@@ -427,22 +447,41 @@ class EulerWorkload(_DeviceCall):
     iters = 10
 
     def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import dist as D
         from paper_2503_10855_b200 import workloads as W
         self.w = self.h = 512 if args.small else 2048
         areas, nb, normals, ff, v = W.euler_mesh(self.w, self.h)
         self.nelr = areas.shape[0]
+        self.world = world
+        self.n_own = self.nelr
+        if world > 1:
+            # element-range slabs of one mesh (strong scaling): slab-local
+            # neighbour ids, NCCL halo exchange of the stage input per RK stage
+            self.plan = D.euler_plan(nb, world, rank)
+            e0, e1 = self.plan["e0"], self.plan["e1"]
+            self.n_own = e1 - e0
+            vl = np.zeros((5, self.plan["n_loc"]), np.float32)
+            vl[:, :self.n_own] = v[:, e0:e1]
+            areas, normals, v = (np.ascontiguousarray(areas[e0:e1]), np.ascontiguousarray(normals[:, :, e0:e1]), vl)
+            nb = self.plan["neighbors"]
+            self.scaling = "strong"
         self.host = {"areas": areas, "nb": nb, "normals": normals, "ff": ff, "v": v}
         self.inputs_e2e = ["areas", "nb", "normals", "ff", "v"]
 
     def alloc_outputs(self, torch):
-        self.pin_out = {"v": torch.empty((5, self.nelr), dtype=torch.float32).pin_memory()}
+        self.pin_out = {"v": torch.empty(self.host["v"].shape, dtype=torch.float32).pin_memory()}
+        if self.world > 1:
+            from paper_2503_10855_b200 import dist as D
+            self.be = D.CudaEulerBackend()
+            self.plan[("_nbrs", str(self.dev["nb"].device))] = self.dev["nb"]
 
     def outputs_e2e(self):
         return [("v", self.dev["v"])]
 
     def config(self, world):
+        par = "single GPU" if world == 1 else f"element slabs/{world}: NCCL halo exchange per RK stage"
         return {"workload": f"euler<{self.nelr}> {self.w}x{self.h} structured mesh, {self.iters} iterations x RK3",
-                "parallelism": "single GPU", "l2": f"{self.nelr * 128 / 1e6:.0f} MB streamed per stage > L2"}
+                "parallelism": par, "l2": f"{self.nelr * 128 / 1e6:.0f} MB streamed per stage > L2"}
 
     def units_per_step(self):
         return self.iters
@@ -450,10 +489,14 @@ class EulerWorkload(_DeviceCall):
     def algorithmic_bytes_per_unit(self):
         # per RK stage and element: own vars 20 + normals 48 + neighbour ids 16
         # + old vars 20 + area 4 + new vars 20 = 128 B (neighbour vars cached)
-        return 3 * 128 * self.nelr  # per iteration = 3 RK-stage launches
+        return 3 * 128 * self.n_own  # per iteration = 3 RK-stage launches (this rank's elements)
 
     def step_device(self):
         d = self.dev
+        if self.world > 1:
+            from paper_2503_10855_b200 import dist as D
+            D.euler_distributed(self.plan, d["areas"], d["normals"], d["ff"], d["v"], self.iters, self.be)
+            return
         self.check_rc(self.lib.jb_euler_f32(self.nelr, self.iters, d["areas"].data_ptr(), d["nb"].data_ptr(),
                                             d["normals"].data_ptr(), d["ff"].data_ptr(), d["v"].data_ptr(),
                                             self.stream.cuda_stream))

@@ -70,36 +70,74 @@ def srad_slab(rows: int, world: int, rank: int) -> dict:
 
 class SradBackend(Protocol):
     def extract(self, image_own, compress: bool): ...            # -> (J_own, sums f64[2])
-    def step(self, J_ext, own_lo: int, own_hi: int, q0, lam: float, compress: bool): ...  # -> (out_own, sums)
+    def step(self, J_ext, own_lo: int, own_hi: int, q0, lam: float, compress: bool, out=None): ...
+    # -> (out_own, sums); writes into `out` (own rows of the other slab buffer) when given
     def q0(self, sums, npx: int): ...                              # -> q0 (backend tensor)
+    def empty_rows(self, n: int, cols: int, like): ...             # -> uninitialised [n, cols]
     def cat_rows(self, parts): ...
 
 
-def _halo_exchange(J_own, rank: int, world: int, group, backend):
-    """Return the extended slab [north 1 | own | south 2] (edges trimmed)."""
-    import torch
+def _gloo(group) -> bool:
     import torch.distributed as dist
-    cols = J_own.shape[1]
-    ops, north, south = [], None, None
-    if rank > 0:
-        north = torch.empty((1, cols), dtype=J_own.dtype, device=J_own.device)
-        ops.append(dist.P2POp(dist.irecv, north, rank - 1, group))
-        ops.append(dist.P2POp(dist.isend, J_own[:2].contiguous(), rank - 1, group))
-    if rank < world - 1:
-        south = torch.empty((2, cols), dtype=J_own.dtype, device=J_own.device)
-        ops.append(dist.P2POp(dist.irecv, south, rank + 1, group))
-        ops.append(dist.P2POp(dist.isend, J_own[-1:].contiguous(), rank + 1, group))
+    return dist.get_backend(group) == "gloo"
+
+
+def _p2p(ops_spec, group):
+    """Batched isend/irecv of (kind, tensor, peer) triples.  NCCL moves the
+    device tensors directly; a gloo group (CPU tests, the shared-GPU bench
+    test mode) stages CUDA tensors through host copies."""
+    import torch.distributed as dist
+    staged, ops = [], []
+    for kind, t, peer in ops_spec:
+        x = t
+        if t.is_cuda and _gloo(group):
+            x = t.detach().cpu() if kind == "send" else torch_empty_cpu(t)
+            staged.append((kind, t, x))
+        ops.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, x.contiguous() if kind == "send" else x,
+                              peer, group))
     if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    parts = [p for p in (north, J_own, south) if p is not None]
-    return backend.cat_rows(parts)
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for kind, t, x in staged:
+        if kind == "recv":
+            t.copy_(x)
+
+
+def torch_empty_cpu(t):
+    import torch
+    return torch.empty(t.shape, dtype=t.dtype)
+
+
+def _all_reduce(t, group):
+    import torch.distributed as dist
+    if t.is_cuda and _gloo(group):
+        x = t.cpu()
+        dist.all_reduce(x, group=group)
+        t.copy_(x)
+    else:
+        dist.all_reduce(t, group=group)
+
+
+def _halo_exchange_rows(ext, lo: int, hi: int, rank: int, world: int, group):
+    """In place: ext = [north 1 | own rows lo..hi | south 2] of this rank's
+    slab (rows that exist); the halo rows are received straight into it."""
+    spec = []
+    if rank > 0:
+        spec.append(("recv", ext[0:1], rank - 1))
+        spec.append(("send", ext[lo:lo + 2], rank - 1))
+    if rank < world - 1:
+        spec.append(("recv", ext[hi:hi + 2], rank + 1))
+        spec.append(("send", ext[hi - 1:hi], rank + 1))
+    _p2p(spec, group)
 
 
 def srad_distributed(image_own, niter: int, lam: float, rows: int, cols: int, backend: SradBackend,
                      group=None):
     """Row-slab SRAD across the ranks of `group`.  `image_own` holds this
-    rank's rows (srad_slab(...)[r0:r1]); returns this rank's output rows."""
+    rank's rows (srad_slab(...)[r0:r1]); returns this rank's output rows.
+    Two extended slab buffers [north 1 | own | south 2] are reused: the step
+    kernel writes the new own rows into the other buffer and the halo rows
+    are received in place (no per-iteration slab copy)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -109,19 +147,25 @@ def srad_distributed(image_own, niter: int, lam: float, rows: int, cols: int, ba
     if niter == 0:
         out, _ = backend.extract(image_own, compress=True)
         return out
+    lo, hi, n_ext = plan["own_lo"], plan["own_hi"], plan["e1"] - plan["e0"]
     J, sums = backend.extract(image_own, compress=False)
+    ext = [backend.empty_rows(n_ext, cols, like=J) for _ in range(2)]
+    ext[0][lo:hi] = J
     if world > 1:
-        dist.all_reduce(sums, group=group)
+        _all_reduce(sums, group)
     q0 = backend.q0(sums, npx)
+    cur = 0
     for it in range(niter):
         last = it + 1 == niter
-        J_ext = _halo_exchange(J, rank, world, group, backend) if world > 1 else J
-        J, sums = backend.step(J_ext, plan["own_lo"], plan["own_hi"], q0, lam, compress=last)
+        if world > 1:
+            _halo_exchange_rows(ext[cur], lo, hi, rank, world, group)
+        _, sums = backend.step(ext[cur], lo, hi, q0, lam, compress=last, out=ext[cur ^ 1][lo:hi])
+        cur ^= 1
         if not last:
             if world > 1:
-                dist.all_reduce(sums, group=group)
+                _all_reduce(sums, group)
             q0 = backend.q0(sums, npx)
-    return J
+    return ext[cur][lo:hi]
 
 
 class CudaSradBackend:
@@ -148,9 +192,13 @@ class CudaSradBackend:
                                                self._s()), "srad_extract")
         return out, sums
 
-    def step(self, J_ext, own_lo, own_hi, q0, lam, compress):
+    def empty_rows(self, n, cols, like):
+        return self.torch.empty((n, cols), dtype=self.torch.float32, device=like.device)
+
+    def step(self, J_ext, own_lo, own_hi, q0, lam, compress, out=None):
         t = self.torch
-        out = t.empty((own_hi - own_lo, J_ext.shape[1]), dtype=t.float32, device=J_ext.device)
+        if out is None:
+            out = t.empty((own_hi - own_lo, J_ext.shape[1]), dtype=t.float32, device=J_ext.device)
         sums = t.zeros(2, dtype=t.float64, device=J_ext.device)
         self._chk(self.lib.jb_srad_slab_step_f32(J_ext.shape[0], J_ext.shape[1], own_lo, own_hi,
                                                  J_ext.data_ptr(), out.data_ptr(), q0.data_ptr(), float(lam),
@@ -217,20 +265,19 @@ def euler_halo_exchange(cur, plan: dict, group=None, backend=None):
     """Fill the halo columns of the SoA slab array cur[5, n_loc] from their
     owners (batched point-to-point send/recv of the owned values they need)."""
     import torch
-    import torch.distributed as dist
     n_own = plan["n_own"]
-    ops, rbufs = [], []
+    spec, rbufs = [], []
+    cache = plan.setdefault("_send_ids", {})  # device copies of the send lists, made once
     for s, idx in plan["send"].items():
-        ids = torch.as_tensor(idx, device=cur.device)
-        buf = cur.index_select(1, ids).contiguous()
-        ops.append(dist.P2POp(dist.isend, buf, s, group))
+        ids = cache.get((s, str(cur.device)))
+        if ids is None:
+            ids = cache[(s, str(cur.device))] = torch.as_tensor(idx, device=cur.device)
+        spec.append(("send", cur.index_select(1, ids), s))
     for r, (st, cnt) in plan["recv"].items():
         buf = torch.empty((cur.shape[0], cnt), dtype=cur.dtype, device=cur.device)
-        ops.append(dist.P2POp(dist.irecv, buf, r, group))
+        spec.append(("recv", buf, r))
         rbufs.append((st, cnt, buf))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+    _p2p(spec, group)
     for st, cnt, buf in rbufs:
         cur[:, n_own + st:n_own + st + cnt] = buf
 
@@ -244,7 +291,10 @@ def euler_distributed(plan: dict, areas_own, normals_own, ff, vars_loc, iteratio
     result is bit-identical to the single-device run)."""
     import torch
     exchange = exchange or (lambda cur: euler_halo_exchange(cur, plan, group))
-    nbrs = backend.to_device(plan["neighbors"], like=vars_loc)
+    key = ("_nbrs", str(getattr(vars_loc, "device", "cpu")))
+    if key not in plan:  # the slab-local neighbour ids move to the device once
+        plan[key] = backend.to_device(plan["neighbors"], like=vars_loc)
+    nbrs = plan[key]
     t1, t2 = torch.empty_like(vars_loc), torch.empty_like(vars_loc)
     for _ in range(iterations):
         for j, (cur, dst) in enumerate(((vars_loc, t1), (t1, t2), (t2, vars_loc))):

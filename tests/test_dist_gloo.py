@@ -45,11 +45,19 @@ class OracleSradBackend:
         J = self.o.srad_extract(a, compress=compress)
         return torch.from_numpy(J), torch.from_numpy(self.o.srad_sums(J))
 
-    def step(self, J_ext, own_lo, own_hi, q0, lam, compress):
+    def empty_rows(self, n, cols, like):
+        return torch.empty((n, cols), dtype=torch.float32)
+
+    def step(self, J_ext, own_lo, own_hi, q0, lam, compress, out=None):
         J = self.o.srad_iter(J_ext.numpy(), float(q0.item()), float(lam))[own_lo:own_hi]
         if compress:
-            return torch.from_numpy(self.o.srad_compress(J)), torch.zeros(2, dtype=torch.float64)
-        return torch.from_numpy(np.ascontiguousarray(J)), torch.from_numpy(self.o.srad_sums(J))
+            res, sums = torch.from_numpy(self.o.srad_compress(J)), torch.zeros(2, dtype=torch.float64)
+        else:
+            res, sums = torch.from_numpy(np.ascontiguousarray(J)), torch.from_numpy(self.o.srad_sums(J))
+        if out is not None:
+            out.copy_(res)
+            res = out
+        return res, sums
 
     def q0(self, sums, npx):
         s, s2 = float(sums[0]), float(sums[1])
