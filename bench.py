@@ -54,6 +54,17 @@ def load_traffic(workload):
         return None, None
 
 
+def load_issue(workload):
+    """the same capture's issue picture (what binds a kernel that is not at
+    its memory or tensor roof): issue-active %, FMA-pipe %, tensor-pipe %"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f)[workload]
+        return {k: e[k] for k in ("issue_active_pct", "fma_pipe_pct", "tensor_pipe_pct") if k in e} or None
+    except Exception:
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -792,6 +803,9 @@ def run_ours(args):
         roofline["traffic_source"] = traffic_src
         if hasattr(wl, "roofline_extra"):
             roofline.update(wl.roofline_extra(avg_ms, per_launch_units))
+        issue = load_issue(args.workload)
+        if issue:
+            roofline["ncu_issue"] = issue
     h2d, d2h = wl.e2e_bytes()
     res = {"metric": wl.metric, "value": round(value, 4 if not hib else 2), "unit": wl.unit, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),

@@ -66,8 +66,15 @@ def traffic(rep):
     def get(k):
         i = hdr.index(k)
         return float(vals[i].replace(',', '')) * scale.get(units[i], 1)
+    extra = {}
+    for k, name in (('smsp__issue_active.avg.pct_of_peak_sustained_active', 'issue_active_pct'),
+                    ('smsp__inst_executed.sum', 'warp_inst'),
+                    ('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', 'fma_pipe_pct'),
+                    ('sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active', 'tensor_pipe_pct')):
+        if k in hdr:
+            extra[name] = float(vals[hdr.index(k)].replace(',', ''))
     return (vals[hdr.index('Kernel Name')], get('dram__bytes_read.sum') + get('dram__bytes_write.sum'),
-            get('gpu__time_duration.sum'))
+            get('gpu__time_duration.sum'), extra)
 
 
 if __name__ == '__main__':
@@ -80,10 +87,10 @@ if __name__ == '__main__':
     for rep in args:
         print(summary(rep))
         if out_json:
-            k, b, t = traffic(rep)
+            k, b, t, extra = traffic(rep)
             w = rep.rsplit('/', 1)[-1].replace('prof_', '').replace('.ncu-rep', '')
             table[w] = {"kernel": k.split('(')[0], "dram_bytes_per_launch": b, "ncu_duration_ns": t,
-                        "source": rep.rsplit('/', 1)[-1]}
+                        "source": rep.rsplit('/', 1)[-1], **extra}
     if out_json:
         import json
         with open(out_json, 'w') as f:
