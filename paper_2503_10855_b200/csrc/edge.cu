@@ -740,6 +740,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
   }
   __syncthreads();
   int t1 = S.next_tile, f1 = S.nt_f, y1 = S.nt_y0, x1 = S.nt_x0;  // the next tile
+  __syncthreads();  // thread 0 rewrites the descriptor in the first tile (racecheck)
   uint32_t tma_phase = 0;
   EDGE_T0();
 
