@@ -49,11 +49,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 namespace jb {
 namespace mm {
 
-constexpr int BM = 128, BN = 128, BK = 32;  // BK fp32 = one 128-byte swizzle row
+#ifndef MM_BN
+#define MM_BN 128
+#endif
+constexpr int BM = 128, BN = MM_BN, BK = 32;  // BK fp32 = one 128-byte swizzle row
+constexpr int B_ATOM = BK * 32 * 4;           // one 32-column MN atom of B: 4 KiB
 constexpr int STAGES = 4;                   // raw tiles (TMA ring, also the hi operands)
 constexpr int LO_STAGES = 2;                // converted lo operands
 constexpr int A_TILE = BM * BK * 4;         // 16 KiB
-constexpr int B_TILE = BK * BN * 4;         // 16 KiB
+constexpr int B_TILE = BK * BN * 4;         // BN/32 atoms
 constexpr int THREADS = 320;
 constexpr int CONVERTERS = 256;             // warps 2..9 (warps 2..5 also run the epilogue)
 constexpr uint32_t TMEM_COLS = 128;
@@ -86,9 +90,9 @@ __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, 
 }
 
 // MN-major B descriptor: 128B swizzle with 32-byte atoms (layout type 1),
-// 32-column MN atoms B_TILE/4 apart (LBO), 4-row K groups 512 B apart (SBO)
+// 32-column MN atoms B_ATOM apart (LBO), 4-row K groups 512 B apart (SBO)
 __device__ __forceinline__ uint64_t desc_b_mn(uint32_t saddr) {
-  const uint64_t d = tc::smem_desc_sw128(saddr, B_TILE / 4, 512);
+  const uint64_t d = tc::smem_desc_sw128(saddr, B_ATOM, 512);
   return (d & ~(7ull << 61)) | (1ull << 61);
 }
 
@@ -145,7 +149,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
         tc::tma_load_2d(S.a_raw[s], &tm_a, &S.full[s], k0, m0);
 #pragma unroll
         for (int at = 0; at < BN / 32; at++)
-          tc::tma_load_2d(S.b_raw[s] + at * (B_TILE / 4), &tm_b, &S.full[s], n0 + 32 * at, k0);
+          tc::tma_load_2d(S.b_raw[s] + at * B_ATOM, &tm_b, &S.full[s], n0 + 32 * at, k0);
       }
     }
   } else if (warp == 1) {
