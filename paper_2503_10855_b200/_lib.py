@@ -40,6 +40,12 @@ SIGNATURES = {
     "jb_srad_extract_f32": [_u64, _vp, _vp, _vp, ctypes.c_int, _vp],
     "jb_srad_slab_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, _vp, ctypes.c_int, _vp],
     "jb_srad_q0_f32": [_vp, _u64, _vp, _vp],
+    "jb_srad_slab_p2p_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, ctypes.c_int, _vp, _vp],
+    "jb_p2p_alloc": [_u64, ctypes.POINTER(_vp)],
+    "jb_p2p_free": [_vp],
+    "jb_ipc_handle": [_vp, _vp],
+    "jb_ipc_open": [_vp, ctypes.POINTER(_vp)],
+    "jb_ipc_close": [_vp],
     "jb_euler_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_euler_stage_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_euler_step_factor_f32": [_u64, _vp, _vp, _vp, _vp],
@@ -112,3 +118,10 @@ def prof_read(name: str) -> tuple[float, int]:
     if st != JB_OK:
         raise RuntimeError(last_error())
     return ms.value, int(cnt.value)
+
+
+class SradP2P(ctypes.Structure):
+    """include/junob200.h: jb_srad_p2p"""
+    _fields_ = [("peer_north", _vp), ("peer_south", _vp), ("mbox", _vp), ("flag", _vp),
+                ("peer_mbox", _vp * 8), ("peer_flag", _vp * 8), ("world", ctypes.c_int),
+                ("rank", ctypes.c_int), ("iter", ctypes.c_int), ("npx_global", _u64), ("grid", ctypes.c_int)]

@@ -229,3 +229,34 @@ jb_status jb_release_workspace(void) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- peer memory (IPC)
+extern "C" jb_status jb_p2p_alloc(uint64_t bytes, void **ptr) {
+  JB_REQUIRE(ptr && bytes > 0, "p2p_alloc: bad arguments");
+  JB_CHECK_CUDA(cudaMalloc(ptr, bytes));
+  JB_CHECK_CUDA(cudaMemset(*ptr, 0, bytes));
+  return JB_OK;
+}
+extern "C" jb_status jb_p2p_free(void *ptr) {
+  if (ptr) JB_CHECK_CUDA(cudaFree(ptr));
+  return JB_OK;
+}
+extern "C" jb_status jb_ipc_handle(const void *ptr, void *handle64) {
+  JB_REQUIRE(ptr && handle64, "ipc_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  JB_CHECK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle64, &h, sizeof(h));
+  return JB_OK;
+}
+extern "C" jb_status jb_ipc_open(const void *handle64, void **ptr) {
+  JB_REQUIRE(ptr && handle64, "ipc_open: null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  JB_CHECK_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return JB_OK;
+}
+extern "C" jb_status jb_ipc_close(void *ptr) {
+  if (ptr) JB_CHECK_CUDA(cudaIpcCloseMemHandle(ptr));
+  return JB_OK;
+}

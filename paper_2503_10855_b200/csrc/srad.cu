@@ -53,7 +53,46 @@ struct Args {
   float ql;           // 0.25f * lambda
   int compress;       // write log(J')*255 instead of J'
   double *sums_out;   // slab mode: the last CTA writes (sum, sum2) here instead of q0
+  // ---- fused multi-GPU slab step (peer memory over NVLink; dist.py
+  // srad_distributed_p2p).  Null mbox: the NCCL-driven slab mode above.
+  float *peer_north;  // north neighbour's next slab: its 2 south-halo rows (our first 2 own rows)
+  float *peer_south;  // south neighbour's next slab: its north-halo row (our last own row)
+  double *mbox;       // this rank's mailbox [2][kMaxRanks][2] (peers write their sums here)
+  unsigned *flag;     // this rank's arrival counter (peers add 1 per iteration)
+  double *peer_mbox[8];
+  unsigned *peer_flag[8];
+  int world, rank, iter;  // iteration it: read mbox[(it-1)&1] after flag >= world*it; write mbox[it&1]
+  long long npx_global;
 };
+constexpr int kMaxRanks = 8;
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// fused P2P step: every CTA waits for all ranks' previous iteration (their
+// halo rows and sums have landed in this rank's buffers), then derives q0^2
+// from the rank-ordered sums (identical on every rank and CTA)
+__device__ float p2p_q0(const Args &a) {
+  __shared__ float q0s;
+  if (threadIdx.x == 0) {
+    const unsigned target = (unsigned)(a.world * a.iter);
+    while (ld_acquire_sys(a.flag) < target) __nanosleep(64);
+    const volatile double *mb = a.mbox + ((a.iter - 1) & 1) * kMaxRanks * 2;
+    double s = 0.0, s2 = 0.0;
+    for (int r = 0; r < a.world; r++) {
+      s += mb[2 * r];
+      s2 += mb[2 * r + 1];
+    }
+    const double mean = s / (double)a.npx_global;
+    const double var = s2 / (double)a.npx_global - mean * mean;
+    q0s = (float)(var / (mean * mean));
+  }
+  __syncthreads();
+  return q0s;
+}
 
 __device__ __forceinline__ void block_stats(double s, double s2, Stats *out) {
   __shared__ double sh[2][THREADS / 32];
@@ -73,7 +112,8 @@ __device__ __forceinline__ void block_stats(double s, double s2, Stats *out) {
 // last CTA of the grid: fixed-order f64 reduction of the partials -> q0^2
 __device__ void finish_stats(const Args &a, long long npx) {
   __shared__ bool last;
-  __threadfence();
+  if (a.mbox) __threadfence_system();  // this CTA's peer halo stores
+  else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
   __syncthreads();
@@ -89,7 +129,16 @@ __device__ void finish_stats(const Args &a, long long npx) {
     s = warp_sum(s);
     s2 = warp_sum(s2);
     if (threadIdx.x == 0) {
-      if (a.sums_out) {  // multi-GPU slab: the q0 comes after the allreduce
+      if (a.mbox) {  // fused P2P: the sums go to every rank's mailbox, then the arrival counts
+        const int slot = (a.iter & 1) * kMaxRanks * 2 + 2 * a.rank;
+        for (int r = 0; r < a.world; r++) {
+          double *mb = a.peer_mbox[r];
+          mb[slot] = s;
+          mb[slot + 1] = s2;
+        }
+        __threadfence_system();  // the sums and every CTA's halo stores precede the counts
+        for (int r = 0; r < a.world; r++) atomicAdd_system(a.peer_flag[r], 1u);
+      } else if (a.sums_out) {  // multi-GPU slab: the q0 comes after the allreduce
         a.sums_out[0] = s;
         a.sums_out[1] = s2;
       } else {
@@ -271,6 +320,20 @@ struct StripCtx {
   int rows, cols, row_lo, row_hi, compress;
   float ql, q0, q0den, q0y;
 };
+// fused P2P step: the neighbours' halo rows fed by our first 2 / last own rows
+// (both null in the single-GPU step)
+struct PeerRows {
+  float *pn, *ps;
+};
+
+// J' of own row `orow`, columns xl..xl+3 (non-compress iterations); the
+// slab's boundary rows also go straight into the neighbours' next slabs
+// (NVLink stores in the fused multi-GPU step)
+__device__ __forceinline__ void put_row(const StripCtx &k, const PeerRows &p, int orow, int xl, float4 v) {
+  *reinterpret_cast<float4 *>(k.dst + (size_t)orow * k.cols + xl) = v;
+  if (p.pn && orow < 2) *reinterpret_cast<float4 *>(p.pn + (size_t)orow * k.cols + xl) = v;
+  if (p.ps && orow == k.row_hi - k.row_lo - 1) *reinterpret_cast<float4 *>(p.ps + xl) = v;
+}
 
 __device__ __forceinline__ float4 ld_row(const float *src, int cols, int y, int xb) {
   return __ldg(reinterpret_cast<const float4 *>(src + (size_t)y * cols + xb));
@@ -313,7 +376,8 @@ __device__ __noinline__ float coef_exact(float Jc, float n_, float s_, float w_,
 
 // one strip; returns false (FAST only) when the strip fails the range guard
 template <bool FAST>
-__device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, int y1, double &s, double &s2) {
+__device__ __forceinline__ bool srad_strip(const StripCtx &k, const PeerRows &pr, int x0, int y0, int y1, double &s,
+                                           double &s2) {
   const int lane = threadIdx.x & 31;
   const int rows = k.rows, cols = k.cols;
   const int xl = x0 + 4 * lane;
@@ -398,7 +462,7 @@ __device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, in
               make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
                           mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
         } else {
-          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+          put_row(k, pr, r - 1 - k.row_lo, xl, make_float4(o[0], o[1], o[2], o[3]));
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             s += (double)o[q];
@@ -426,7 +490,7 @@ __device__ __forceinline__ bool srad_strip(const StripCtx &k, int x0, int y0, in
               make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
                           mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
         } else {
-          *reinterpret_cast<float4 *>(k.dst + off) = make_float4(o[0], o[1], o[2], o[3]);
+          put_row(k, pr, r - k.row_lo, xl, make_float4(o[0], o[1], o[2], o[3]));
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             s += (double)o[q];
@@ -495,7 +559,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // Interior strips only (rows y0-1 .. y1+1 exist, so no row clamping and no
 // bottom-row special case; the kernel sends the rest to srad_strip<true>).
 template <bool COMPRESS>
-__device__ __forceinline__ bool strip_fast(const StripCtx k, RowRing &R, int x0, int y0, int y1, double &s,
+__device__ __forceinline__ bool strip_fast(const StripCtx k, const PeerRows pr, RowRing &R, int x0, int y0, int y1, double &s,
                                            double &s2) {
   const int lane = threadIdx.x & 31;
   const int cols = k.cols;
@@ -594,7 +658,8 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, RowRing &R, int x0,
           *reinterpret_cast<float4 *>(po) = make_float4(mul_rn(log_ref(o[0]), 255.0f), mul_rn(log_ref(o[1]), 255.0f),
                                                         mul_rn(log_ref(o[2]), 255.0f), mul_rn(log_ref(o[3]), 255.0f));
         } else {
-          *reinterpret_cast<float4 *>(po) = make_float4(o[0], o[1], o[2], o[3]);
+          if (pr.pn || pr.ps) put_row(k, pr, (int)((po - k.dst) / cs), xl, make_float4(o[0], o[1], o[2], o[3]));
+          else *reinterpret_cast<float4 *>(po) = make_float4(o[0], o[1], o[2], o[3]);
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             const double v = (double)o[q];
@@ -623,24 +688,30 @@ struct StripRes {
   double s, s2;
   bool ok;
 };
-__device__ __noinline__ StripRes strip_edge(const StripCtx k, int x0, int y0, int y1) {
+__device__ __noinline__ StripRes strip_edge(const StripCtx k, const PeerRows pr, int x0, int y0, int y1) {
   StripRes r{0.0, 0.0, false};
-  r.ok = srad_strip<true>(k, x0, y0, y1, r.s, r.s2);
+  r.ok = srad_strip<true>(k, pr, x0, y0, y1, r.s, r.s2);
   return r;
 }
 
-__device__ __noinline__ StripRes strip_exact(const StripCtx k, int x0, int y0, int y1) {
+__device__ __noinline__ StripRes strip_exact(const StripCtx k, const PeerRows pr, int x0, int y0, int y1) {
   StripRes r{0.0, 0.0, true};
-  srad_strip<false>(k, x0, y0, y1, r.s, r.s2);
+  srad_strip<false>(k, pr, x0, y0, y1, r.s, r.s2);
   return r;
 }
 
+// P2P: the fused multi-GPU step (peer halo stores, mailbox q0); the
+// single-GPU instantiation compiles that code out (register pressure)
+template <bool P2P>
 __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args a) {
   const int warp = threadIdx.x >> 5;
   StripCtx k;
   k.src = a.src; k.dst = a.dst; k.rows = a.rows; k.cols = a.cols;
   k.row_lo = a.row_lo; k.row_hi = a.row_hi; k.compress = a.compress; k.ql = a.ql;
-  k.q0 = *a.q0;
+  PeerRows pr;
+  pr.pn = (P2P && !a.compress) ? a.peer_north : nullptr;
+  pr.ps = (P2P && !a.compress) ? a.peer_south : nullptr;
+  k.q0 = (P2P && a.iter > 0) ? p2p_q0(a) : *a.q0;
   k.q0den = mul_rn(k.q0, add_rn(1.0f, k.q0));
   k.q0y = recip_refined(k.q0den);
   const bool q0ok = k.q0 >= 9.5367431640625e-07f && k.q0 <= 1048576.0f;  // [2^-20, 2^20]
@@ -657,13 +728,13 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
     StripRes res{0.0, 0.0, false};
     if (q0ok) {
       if (y0 >= 1 && y1 + 1 <= a.rows - 1 && y1 - y0 == SH) {  // interior strip
-        res.ok = a.compress ? strip_fast<true>(k, rings[warp], x0, y0, y1, res.s, res.s2)
-                            : strip_fast<false>(k, rings[warp], x0, y0, y1, res.s, res.s2);
+        res.ok = a.compress ? strip_fast<true>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2)
+                            : strip_fast<false>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2);
       } else {
-        res = strip_edge(k, x0, y0, y1);
+        res = strip_edge(k, pr, x0, y0, y1);
       }
     }
-    if (!res.ok) res = strip_exact(k, x0, y0, y1);  // outside the fast-division guard
+    if (!res.ok) res = strip_exact(k, pr, x0, y0, y1);  // outside the fast-division guard
     s += res.s;
     s2 += res.s2;
   }
@@ -689,7 +760,7 @@ static bool strip_ok(uint64_t cols, const void *p0, const void *p1) {
 static int strip_grid() {
   static int per_sm = 0;
   if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_strip_kernel, SWARPS * 32, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_strip_kernel<false>, SWARPS * 32, 0) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
   }
@@ -748,7 +819,7 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
     a.q0_next = q0 + it + 1;
     a.compress = last;
     void *tok = prof_begin("srad_iter", s);
-    if (strips) srad_strip_kernel<<<sgrid, SWARPS * 32, 0, s>>>(a);
+    if (strips) srad_strip_kernel<false><<<sgrid, SWARPS * 32, 0, s>>>(a);
     else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
     prof_end(tok, s);
     JB_LAUNCHED("srad_iter");
@@ -822,10 +893,54 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
   a.sums_out = sums;
   JB_CHECK_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s));
   void *tok = prof_begin("srad_iter", s);
-  if (strips) srad_strip_kernel<<<sgrid, SWARPS * 32, 0, s>>>(a);
+  if (strips) srad_strip_kernel<false><<<sgrid, SWARPS * 32, 0, s>>>(a);
   else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
   prof_end(tok, s);
   JB_LAUNCHED("srad_slab_step");
+  return JB_OK;
+}
+
+// fused multi-GPU slab step (dist.py srad_distributed_p2p): the strip kernel
+// stores the slab's boundary rows straight into the neighbours' next slabs
+// and its (sum, sum^2) into every rank's mailbox over peer memory, and the
+// next iteration's kernel waits on the arrival counter -- no NCCL call and no
+// host round trip per iteration.
+extern "C" jb_status jb_srad_slab_p2p_step_f32(uint64_t rows_ext, uint64_t cols, uint64_t own_lo, uint64_t own_hi,
+                                               const float *J_ext, float *out_own, const float *q0, float lambda,
+                                               int compress, const jb_srad_p2p *p2p, void *stream) {
+  JB_REQUIRE(rows_ext >= 1 && cols >= 1 && own_lo < own_hi && own_hi <= rows_ext, "srad_p2p: bad slab");
+  JB_REQUIRE(p2p && J_ext && out_own && p2p->mbox && p2p->flag, "srad_p2p: null pointer");
+  JB_REQUIRE(p2p->world >= 1 && p2p->world <= kMaxRanks && p2p->rank >= 0 && p2p->rank < p2p->world,
+             "srad_p2p: world must be 1..8");
+  JB_REQUIRE(p2p->iter > 0 || q0, "srad_p2p: the first iteration needs q0 from the host");
+  JB_REQUIRE(strip_ok(cols, J_ext, out_own), "srad_p2p: rows must be float4-aligned (cols %% 4 == 0)");
+  for (int r = 0; r < p2p->world; r++) JB_REQUIRE(p2p->peer_mbox[r] && p2p->peer_flag[r], "srad_p2p: null peer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sgrid = p2p->grid > 0 ? p2p->grid : strip_grid();
+  const size_t pb = ((sgrid * sizeof(Stats) + 255) / 256) * 256;
+  char *ws = (char *)workspace(pb + 256, s);
+  if (!ws) return JB_ECUDA;
+  if (p2p->iter == 0) JB_CHECK_CUDA(cudaMemsetAsync(ws + pb, 0, 4, s));
+  Args a{};
+  a.src = J_ext; a.dst = out_own; a.q0 = q0; a.q0_next = nullptr;
+  a.partials = (Stats *)ws; a.ticket = (unsigned *)(ws + pb);
+  a.rows = (int)rows_ext; a.cols = (int)cols;
+  a.row_lo = (int)own_lo; a.row_hi = (int)own_hi;
+  a.ql = 0.25f * lambda;
+  a.compress = compress;
+  a.sums_out = nullptr;
+  a.peer_north = p2p->peer_north; a.peer_south = p2p->peer_south;
+  a.mbox = p2p->mbox; a.flag = p2p->flag;
+  for (int r = 0; r < kMaxRanks; r++) {
+    a.peer_mbox[r] = r < p2p->world ? p2p->peer_mbox[r] : nullptr;
+    a.peer_flag[r] = r < p2p->world ? p2p->peer_flag[r] : nullptr;
+  }
+  a.world = p2p->world; a.rank = p2p->rank; a.iter = p2p->iter;
+  a.npx_global = (long long)p2p->npx_global;
+  void *tok = prof_begin("srad_iter", s);
+  srad_strip_kernel<true><<<sgrid, SWARPS * 32, 0, s>>>(a);
+  prof_end(tok, s);
+  JB_LAUNCHED("srad_p2p_step");
   return JB_OK;
 }
 
