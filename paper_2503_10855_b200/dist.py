@@ -168,6 +168,149 @@ def srad_distributed(image_own, niter: int, lam: float, rows: int, cols: int, ba
     return ext[cur][lo:hi]
 
 
+class _Raw:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def _raw_tensor(ptr: int, shape, dtype="f4"):
+    import torch
+    return torch.as_tensor(_Raw(ptr, shape, "<" + dtype), device="cuda")
+
+
+class SradP2PSlabs:
+    """Peer-memory slab buffers of one rank for the fused multi-GPU SRAD step.
+
+    One IPC-exportable allocation per rank holds [ext 0 | ext 1 | mailbox |
+    counter]: two extended slabs [north 1 | own | south 2] and the mailbox the
+    other ranks write their (sum, sum^2) into.  The handles are exchanged once
+    (all_gather_object) and every peer allocation is mapped
+    (cudaIpcOpenMemHandle: NVLink P2P between GPUs; the same device in the
+    one-GPU tests)."""
+
+    MBOX = 256  # bytes: double[2][8][2]
+
+    def __init__(self, rows: int, cols: int, group=None, grid: int = 0):
+        import ctypes
+        import torch.distributed as dist
+        self.lib = _lib.load()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 8:
+            raise ValueError("the fused P2P step supports up to 8 ranks")
+        if cols % 4:
+            raise ValueError("the fused P2P step needs cols % 4 == 0")
+        self.rows, self.cols, self.group, self.grid = rows, cols, group, grid
+        self.plans = [srad_slab(rows, self.world, r) for r in range(self.world)]
+        self.ext_bytes = [(p["e1"] - p["e0"]) * cols * 4 for p in self.plans]
+        nbytes = 2 * self.ext_bytes[self.rank] + self.MBOX + 256
+        ptr = ctypes.c_void_p()
+        self._chk(self.lib.jb_p2p_alloc(nbytes, ctypes.byref(ptr)), "p2p_alloc")
+        self.base = ptr.value
+        h = ctypes.create_string_buffer(64)
+        self._chk(self.lib.jb_ipc_handle(self.base, h), "ipc_handle")
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, h.raw, group=group)
+        else:
+            handles = [h.raw]
+        self.peers, self.opened = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                self.peers.append(self.base)
+                continue
+            p = ctypes.c_void_p()
+            self._chk(self.lib.jb_ipc_open(ctypes.create_string_buffer(handles[r], 64), ctypes.byref(p)),
+                      f"ipc_open(rank {r})")
+            self.peers.append(p.value)
+            self.opened.append(p.value)
+
+    def _chk(self, rc, what):
+        if rc:
+            raise RuntimeError(f"{what}: {_lib.last_error()}")
+
+    def ext(self, b: int, r: int = None) -> int:  # device address of slab buffer b of rank r
+        r = self.rank if r is None else r
+        return self.peers[r] + b * self.ext_bytes[r]
+
+    def mbox(self, r: int) -> int:
+        return self.peers[r] + 2 * self.ext_bytes[r]
+
+    def flag(self, r: int) -> int:
+        return self.mbox(r) + self.MBOX
+
+    def ext_tensor(self, b: int):
+        p = self.plans[self.rank]
+        return _raw_tensor(self.ext(b), (p["e1"] - p["e0"], self.cols))
+
+    def close(self):
+        for p in self.opened:
+            self.lib.jb_ipc_close(p)
+        self.opened = []
+        if self.base:
+            self.lib.jb_p2p_free(self.base)
+            self.base = None
+
+
+def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs, backend=None):
+    """Row-slab SRAD where each iteration is ONE kernel per rank: it stores
+    the slab's boundary rows into the neighbours' next slabs and its sums into
+    every rank's mailbox over peer memory, and the next iteration's kernel
+    waits on the arrival counter (jb_srad_slab_p2p_step_f32).  The extract
+    prologue runs once through the collective path.  Returns this rank's
+    output rows (a copy)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    be = backend or CudaSradBackend()
+    lib, w, rank, group = slabs.lib, slabs.world, slabs.rank, slabs.group
+    plan = slabs.plans[rank]
+    lo, hi, cols = plan["own_lo"], plan["own_hi"], slabs.cols
+    npx = slabs.rows * cols
+    if niter == 0:
+        out, _ = be.extract(image_own, compress=True)
+        return out
+    # a fresh call: zero this rank's counter and mailbox once every rank is
+    # idle, so that no peer writes into them before they are reset
+    torch.cuda.synchronize()
+    if w > 1:
+        dist.barrier(group=group)
+    _raw_tensor(slabs.mbox(rank), (slabs.MBOX // 4 + 64,), "i4").zero_()
+    torch.cuda.synchronize()
+    if w > 1:
+        dist.barrier(group=group)
+    ext0 = slabs.ext_tensor(0)
+    J, sums = be.extract(image_own, compress=False)
+    ext0[lo:hi] = J
+    if w > 1:
+        _all_reduce(sums, group)
+        _halo_exchange_rows(ext0, lo, hi, rank, w, group)
+    q0 = be.q0(sums, npx)
+    a = _lib.SradP2P()
+    a.mbox, a.flag = slabs.mbox(rank), slabs.flag(rank)
+    for r in range(w):
+        a.peer_mbox[r] = slabs.mbox(r)
+        a.peer_flag[r] = slabs.flag(r)
+    a.world, a.rank, a.npx_global, a.grid = w, rank, npx, slabs.grid
+    stream = torch.cuda.current_stream().cuda_stream
+    n_ext = plan["e1"] - plan["e0"]
+    for it in range(niter):
+        cur, nxt = it & 1, (it & 1) ^ 1
+        last = it + 1 == niter
+        a.iter = it
+        a.peer_north = (slabs.ext(nxt, rank - 1) + slabs.plans[rank - 1]["own_hi"] * cols * 4) if rank > 0 else None
+        a.peer_south = slabs.ext(nxt, rank + 1) if rank < w - 1 else None
+        rc = lib.jb_srad_slab_p2p_step_f32(n_ext, cols, lo, hi, slabs.ext(cur), slabs.ext(nxt) + lo * cols * 4,
+                                            q0.data_ptr() if it == 0 else None, float(lam), int(last),
+                                            ctypes.byref(a), stream)
+        if rc:
+            raise RuntimeError(f"srad_p2p_step: {_lib.last_error()}")
+    return slabs.ext_tensor(niter & 1)[lo:hi].clone()
+
+
 class CudaSradBackend:
     """libjunob200 slab kernels on device tensors (NCCL collectives)."""
 
