@@ -402,12 +402,21 @@ class SradWorkload(_DeviceCall):
         if self.world > 1:
             from paper_2503_10855_b200 import dist as D
             self.be = D.CudaSradBackend()
+            # default: the fused peer-memory step (one kernel per iteration,
+            # boundary rows and sums stored into the peers over NVLink);
+            # JB_SRAD_NCCL=1 selects the NCCL halo + allreduce path
+            self.slabs = None
+            if os.environ.get("JB_SRAD_NCCL") != "1":
+                self.slabs = D.SradP2PSlabs(self.rows, self.cols, grid=int(os.environ.get("JB_SRAD_P2P_GRID", "0")))
 
     def outputs_e2e(self):
         return [("out", self.out)]
 
     def config(self, world):
-        par = "single GPU" if world == 1 else f"row slabs/{world}: NCCL halo rows + f64 allreduce per iteration"
+        fused = getattr(self, "slabs", None) is not None
+        par = "single GPU" if world == 1 else (
+            f"row slabs/{world}: " + ("fused P2P step (peer-memory halo rows + mailbox sums)" if fused
+                                      else "NCCL halo rows + f64 allreduce per iteration"))
         return {"workload": f"srad<{self.rows},{self.cols}> niter={self.niter} lambda=0.5 (Rodinia srad_v1)",
                 "parallelism": par, "l2": "1 GiB image >> 126 MB L2"}
 
@@ -421,7 +430,10 @@ class SradWorkload(_DeviceCall):
     def step_device(self):
         if self.world > 1:
             from paper_2503_10855_b200 import dist as D
-            res = D.srad_distributed(self.dev["image"], self.niter, 0.5, self.rows, self.cols, self.be)
+            if self.slabs is not None:
+                res = D.srad_distributed_p2p(self.dev["image"], self.niter, 0.5, self.slabs, self.be)
+            else:
+                res = D.srad_distributed(self.dev["image"], self.niter, 0.5, self.rows, self.cols, self.be)
             self.out.copy_(res)
             return
         self.check_rc(self.lib.jb_srad_f32(self.rows, self.cols, self.niter, 0.5, self.dev["image"].data_ptr(),

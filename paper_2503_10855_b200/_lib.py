@@ -124,4 +124,5 @@ class SradP2P(ctypes.Structure):
     """include/junob200.h: jb_srad_p2p"""
     _fields_ = [("peer_north", _vp), ("peer_south", _vp), ("mbox", _vp), ("flag", _vp),
                 ("peer_mbox", _vp * 8), ("peer_flag", _vp * 8), ("world", ctypes.c_int),
-                ("rank", ctypes.c_int), ("iter", ctypes.c_int), ("npx_global", _u64), ("grid", ctypes.c_int)]
+                ("rank", ctypes.c_int), ("iter", ctypes.c_int), ("flag_base", ctypes.c_uint32),
+                ("npx_global", _u64), ("grid", ctypes.c_int)]

@@ -61,7 +61,8 @@ struct Args {
   unsigned *flag;     // this rank's arrival counter (peers add 1 per iteration)
   double *peer_mbox[8];
   unsigned *peer_flag[8];
-  int world, rank, iter;  // iteration it: read mbox[(it-1)&1] after flag >= world*it; write mbox[it&1]
+  int world, rank, iter;  // iteration it: read mbox[(it-1)&1] after flag >= base+world*it; write mbox[it&1]
+  unsigned flag_base;     // the counter value when this call started (every iteration adds world)
   long long npx_global;
 };
 constexpr int kMaxRanks = 8;
@@ -78,8 +79,12 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
 __device__ float p2p_q0(const Args &a) {
   __shared__ float q0s;
   if (threadIdx.x == 0) {
-    const unsigned target = (unsigned)(a.world * a.iter);
+    const unsigned target = a.flag_base + (unsigned)(a.world * a.iter);
     while (ld_acquire_sys(a.flag) < target) __nanosleep(64);
+    if (a.iter == 0) {  // the previous call has finished on every rank; q0 comes from the host
+      q0s = *a.q0;
+      goto done;
+    }
     const volatile double *mb = a.mbox + ((a.iter - 1) & 1) * kMaxRanks * 2;
     double s = 0.0, s2 = 0.0;
     for (int r = 0; r < a.world; r++) {
@@ -90,6 +95,7 @@ __device__ float p2p_q0(const Args &a) {
     const double var = s2 / (double)a.npx_global - mean * mean;
     q0s = (float)(var / (mean * mean));
   }
+done:
   __syncthreads();
   return q0s;
 }
@@ -711,7 +717,7 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
   PeerRows pr;
   pr.pn = (P2P && !a.compress) ? a.peer_north : nullptr;
   pr.ps = (P2P && !a.compress) ? a.peer_south : nullptr;
-  k.q0 = (P2P && a.iter > 0) ? p2p_q0(a) : *a.q0;
+  k.q0 = P2P ? p2p_q0(a) : *a.q0;
   k.q0den = mul_rn(k.q0, add_rn(1.0f, k.q0));
   k.q0y = recip_refined(k.q0den);
   const bool q0ok = k.q0 >= 9.5367431640625e-07f && k.q0 <= 1048576.0f;  // [2^-20, 2^20]
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
     s += res.s;
     s2 += res.s2;
   }
-  if (a.compress) return;
+  if (a.compress && !P2P) return;  // (the fused step still counts its arrival)
   block_stats(s, s2, a.partials + blockIdx.x);
   finish_stats(a, (long long)nrows * a.cols);
 }
@@ -935,7 +941,7 @@ extern "C" jb_status jb_srad_slab_p2p_step_f32(uint64_t rows_ext, uint64_t cols,
     a.peer_mbox[r] = r < p2p->world ? p2p->peer_mbox[r] : nullptr;
     a.peer_flag[r] = r < p2p->world ? p2p->peer_flag[r] : nullptr;
   }
-  a.world = p2p->world; a.rank = p2p->rank; a.iter = p2p->iter;
+  a.world = p2p->world; a.rank = p2p->rank; a.iter = p2p->iter; a.flag_base = p2p->flag_base;
   a.npx_global = (long long)p2p->npx_global;
   void *tok = prof_begin("srad_iter", s);
   srad_strip_kernel<true><<<sgrid, SWARPS * 32, 0, s>>>(a);

@@ -204,6 +204,7 @@ class SradP2PSlabs:
         if cols % 4:
             raise ValueError("the fused P2P step needs cols % 4 == 0")
         self.rows, self.cols, self.group, self.grid = rows, cols, group, grid
+        self.epoch = 0  # this rank's arrival counter after the calls so far
         self.plans = [srad_slab(rows, self.world, r) for r in range(self.world)]
         self.ext_bytes = [(p["e1"] - p["e0"]) * cols * 4 for p in self.plans]
         nbytes = 2 * self.ext_bytes[self.rank] + self.MBOX + 256
@@ -273,15 +274,9 @@ def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs,
     if niter == 0:
         out, _ = be.extract(image_own, compress=True)
         return out
-    # a fresh call: zero this rank's counter and mailbox once every rank is
-    # idle, so that no peer writes into them before they are reset
-    torch.cuda.synchronize()
-    if w > 1:
-        dist.barrier(group=group)
-    _raw_tensor(slabs.mbox(rank), (slabs.MBOX // 4 + 64,), "i4").zero_()
-    torch.cuda.synchronize()
-    if w > 1:
-        dist.barrier(group=group)
+    # no host synchronisation between calls: the counters only grow (every
+    # iteration adds `world` on every rank), so this call's iteration 0 waits
+    # for the previous call to have finished everywhere (flag_base)
     ext0 = slabs.ext_tensor(0)
     J, sums = be.extract(image_own, compress=False)
     ext0[lo:hi] = J
@@ -295,6 +290,7 @@ def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs,
         a.peer_mbox[r] = slabs.mbox(r)
         a.peer_flag[r] = slabs.flag(r)
     a.world, a.rank, a.npx_global, a.grid = w, rank, npx, slabs.grid
+    a.flag_base = slabs.epoch
     stream = torch.cuda.current_stream().cuda_stream
     n_ext = plan["e1"] - plan["e0"]
     for it in range(niter):
@@ -308,6 +304,7 @@ def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs,
                                             ctypes.byref(a), stream)
         if rc:
             raise RuntimeError(f"srad_p2p_step: {_lib.last_error()}")
+    slabs.epoch += w * niter
     return slabs.ext_tensor(niter & 1)[lo:hi].clone()
 
 

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 for w in ${WORKLOADS:-edge cava matmul srad euler bfs backprop}; do
   for impl in ours reference; do
     echo "== $w $impl" >> gpurun_out/multi_rank.log
-    JB_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    JB_BENCH_SHARE_GPU=1 JB_SRAD_P2P_GRID=8 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
       --master-addr 127.0.0.1 --master-port 29517 bench.py --workload $w --impl $impl --gpus 2 --steps 2 --warmup 3 \
       --e2e-steps 1 >> gpurun_out/multi_rank.log 2>&1
     echo "rc=$?" >> gpurun_out/multi_rank.log
