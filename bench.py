@@ -653,7 +653,8 @@ class BackpropWorkload(_DeviceCall):
 
 
 class CavaWorkload(_DeviceCall):
-    """cava on a batch of 16 synthetic 1080x1920 raw frames, P=16."""
+    """cava on a batch of 64 synthetic 1080x1920 raw frames, P=16, sharded by
+    frame across ranks (strong scaling, no collective)."""
     name = "cava"
     metric = "cava_frames_per_s"
     unit = "frames/s"
@@ -663,16 +664,18 @@ class CavaWorkload(_DeviceCall):
     scaling = "strong"
 
     def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import dist as D
         from paper_2503_10855_b200 import workloads as W
-        self.batch = 4 if args.small else 16
+        self.batch = 4 if args.small else 64
         self.r, self.c = (270, 480) if args.small else (1080, 1920)
         self.P = 16
-        self.host = {"raw": W.cava_raw(self.batch, self.r, self.c)}
+        f0, self.local = D.shard_frames(self.batch, world, rank)
+        raw = W.cava_raw(self.batch, self.r, self.c)[f0:f0 + self.local]
+        self.host = {"raw": np.ascontiguousarray(raw)}
         self.params = W.cava_params(self.P)
         for k, v in zip(("tstw", "ctrl", "wts", "coefs", "tmap"), self.params):
             self.host[k] = v
         self.inputs_e2e = ["raw"]
-        self.local = self.batch
 
     def alloc_outputs(self, torch):
         self.out = torch.empty(self.host["raw"].shape, dtype=torch.uint8, device="cuda")
@@ -683,7 +686,8 @@ class CavaWorkload(_DeviceCall):
 
     def config(self, world):
         return {"workload": f"cava batch={self.batch} u8[3,{self.r},{self.c}] P={self.P} control points",
-                "parallelism": "frames", "l2": f"{self.batch * 6 * self.r * self.c / 1e6:.0f} MB in+out"}
+                "global_batch": self.batch, "parallelism": f"frames/{world}",
+                "l2": f"{self.batch * 6 * self.r * self.c / 1e6:.0f} MB in+out >> 126 MB L2"}
 
     def units_per_step(self):
         return self.batch
@@ -691,9 +695,19 @@ class CavaWorkload(_DeviceCall):
     def algorithmic_bytes_per_unit(self):
         return 6 * self.r * self.c  # u8 x3 in + u8 x3 out
 
+    e2e_api = "paper_2503_10855_b200.api.cava_pipelined (pinned host in/out, 2-frame chunks)"
+
+    def step_e2e(self):
+        """Public API on pinned host buffers, copies overlapped with the kernels."""
+        from paper_2503_10855_b200 import api
+        if self.local:
+            api.cava_pipelined(self.pin["raw"], *self.params, out=self.pin_out["out"])
+
     def step_device(self):
+        if not self.local:
+            return
         d = self.dev
-        self.check_rc(self.lib.jb_cava_u8(self.batch, self.r, self.c, self.P, d["raw"].data_ptr(),
+        self.check_rc(self.lib.jb_cava_u8(self.local, self.r, self.c, self.P, d["raw"].data_ptr(),
                                           d["tstw"].data_ptr(), d["ctrl"].data_ptr(), d["wts"].data_ptr(),
                                           d["coefs"].data_ptr(), d["tmap"].data_ptr(), self.out.data_ptr(),
                                           self.stream.cuda_stream))
@@ -791,7 +805,8 @@ def run_ours(args):
     roofline = None
     if kcount:
         avg_ms = kms / kcount
-        local_units = (wl.local if isinstance(wl, EdgeWorkload) else units) * args.steps
+        # units this rank's kernels processed (frame-sharded workloads: its share)
+        local_units = (wl.local if isinstance(wl, (EdgeWorkload, CavaWorkload)) else units) * args.steps
         per_launch_units = local_units / kcount
         if getattr(wl, "bound", "hbm") == "tensor":
             alg = wl.flops_per_unit() * per_launch_units

@@ -195,36 +195,25 @@ def edge_detection(input, gaussian_filter, structure, sx, sy, theta):
 _PIPE_CACHE: dict = {}
 
 
-def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 8):
-    """Host-buffer edge detection with copy/compute overlap.
+def _pipelined(x, out, chunk: int, key, launch):
+    """Host-buffer batch through the device with copy/compute overlap.
 
-    ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
-    memory gives full PCIe bandwidth).  Frames move in chunks through two
-    device slots on three streams -- H2D of chunk i+1 and D2H of chunk i-1
-    overlap the kernels of chunk i -- so the call is bound by the slower
-    PCIe direction instead of the sum of copy and compute time.  Returns
-    ``out`` (a host f32 tensor/array of the input's shape)."""
+    Frames of the host batch ``x`` move in chunks through two device slots on
+    three streams -- H2D of chunk i+1 and D2H of chunk i-1 overlap the kernel
+    of chunk i -- so a call is bound by the slower PCIe direction instead of
+    the sum of copy and compute time.  ``launch(k, din, dout, stream)`` runs
+    the entry on the first k frames of the slot buffers."""
     torch = _torch()
-    x = input if isinstance(input, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(input, np.float32))
-    _need(x.dtype == torch.float32 and x.dim() == 3 and not x.is_cuda,
-          "edge_detection_pipelined: input must be a host f32[batch,n,m]")
-    B, n, m = (int(v) for v in x.shape)
-    if out is None:
-        out = torch.empty_like(x, pin_memory=x.is_pinned())
-    gs, sz, sb = (_shape(f)[0] for f in (gaussian_filter, structure, sx))
     dev = torch.device("cuda", torch.cuda.current_device())
-    key = (dev.index, n, m, chunk)
+    B = int(x.shape[0])
+    key = (dev.index, x.dtype, tuple(x.shape[1:]), out.dtype, tuple(out.shape[1:]), chunk, key)
     st = _PIPE_CACHE.get(key)
     if st is None:
-        st = dict(inb=[torch.empty((chunk, n, m), dtype=torch.float32, device=dev) for _ in range(2)],
-                  outb=[torch.empty((chunk, n, m), dtype=torch.float32, device=dev) for _ in range(2)],
+        st = dict(inb=[torch.empty((chunk, *x.shape[1:]), dtype=x.dtype, device=dev) for _ in range(2)],
+                  outb=[torch.empty((chunk, *out.shape[1:]), dtype=out.dtype, device=dev) for _ in range(2)],
                   s_in=torch.cuda.Stream(dev), s_out=torch.cuda.Stream(dev))
         _PIPE_CACHE[key] = st
     comp = torch.cuda.current_stream(dev)
-    filt = [(f.to(dev) if isinstance(f, torch.Tensor) else
-             torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
-            for f in (gaussian_filter, structure, sx, sy)]
-    lib = _lib.load()
     s_in, s_out = st["s_in"], st["s_out"]
     c_done = [None, None]
     d_done = [None, None]
@@ -241,9 +230,7 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
         comp.wait_event(h_ev)
         if d_done[slot] is not None:
             comp.wait_event(d_done[slot])
-        _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
-                               filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(),
-                               comp.cuda_stream), "edge_detection")
+        launch(k, din, dout, comp.cuda_stream)
         c_ev = torch.cuda.Event()
         c_ev.record(comp)
         c_done[slot] = c_ev
@@ -256,6 +243,56 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
     s_out.synchronize()
     comp.wait_stream(s_out)
     return out
+
+
+def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 8):
+    """Host-buffer edge detection with copy/compute overlap (``_pipelined``).
+
+    ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
+    memory gives full PCIe bandwidth).  Returns ``out`` (a host f32 tensor of
+    the input's shape)."""
+    torch = _torch()
+    x = input if isinstance(input, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(input, np.float32))
+    _need(x.dtype == torch.float32 and x.dim() == 3 and not x.is_cuda,
+          "edge_detection_pipelined: input must be a host f32[batch,n,m]")
+    B, n, m = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty_like(x, pin_memory=x.is_pinned())
+    gs, sz, sb = (_shape(f)[0] for f in (gaussian_filter, structure, sx))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    filt = [(f.to(dev) if isinstance(f, torch.Tensor) else
+             torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
+            for f in (gaussian_filter, structure, sx, sy)]
+    lib = _lib.load()
+
+    def launch(k, din, dout, stream):
+        _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
+                               filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(), stream),
+               "edge_detection")
+    return _pipelined(x, out, chunk, "edge", launch)
+
+
+def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 2):
+    """Host-buffer CAVA over a batch u8[batch,3,r,c] with copy/compute overlap
+    (``_pipelined``); returns ``out`` (a host u8 tensor of the input's shape)."""
+    torch = _torch()
+    x = input if isinstance(input, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(input, np.uint8))
+    _need(x.dtype == torch.uint8 and x.dim() == 4 and x.shape[1] == 3 and not x.is_cuda,
+          "cava_pipelined: input must be a host u8[batch,3,r,c]")
+    B, _, r, c = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty_like(x, pin_memory=x.is_pinned())
+    P = _shape(ctrl_pts)[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    prm = [(f.to(dev) if isinstance(f, torch.Tensor) else
+            torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
+           for f in (tstw, ctrl_pts, weights, coefs, tonemap)]
+    lib = _lib.load()
+
+    def launch(k, din, dout, stream):
+        _check(lib.jb_cava_u8(k, r, c, P, din.data_ptr(), *(t.data_ptr() for t in prm), dout.data_ptr(), stream),
+               "cava")
+    return _pipelined(x, out, chunk, "cava", launch)
 
 
 def edge_detection_stages(input, gaussian_filter, structure, sx, sy, theta):

@@ -27,3 +27,16 @@ def test_cava_scale_transform_pinned(oracle):
     g = golden("cava_stages_6x8")
     sc = oracle.cava_stage("scale", g["raw"])
     assert np.array_equal(sc.view(np.uint32), g["scaled"].view(np.uint32))
+
+
+def test_cava_pipelined_matches_single_call(jb):
+    """The host-buffer pipelined entry (chunks through two device slots on
+    three streams) returns exactly the single-call result, including a
+    ragged last chunk."""
+    import torch
+    from paper_2503_10855_b200 import api
+    raw = W.cava_raw(5, 70, 132, seed=3)
+    params = W.cava_params(P=16)
+    ref = jb.cava(raw, *params)
+    got = api.cava_pipelined(torch.from_numpy(raw).pin_memory(), *params, chunk=2)
+    assert np.array_equal(got.numpy(), ref)

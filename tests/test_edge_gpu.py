@@ -89,3 +89,15 @@ def test_edge_threshold_cases(jb, oracle, theta):
     x = np.stack([W.edge_frame(130, 190, seed=s) for s in range(3)])
     th = np.float32(theta)
     _bits_equal(jb.edge_detection(x, g, st, sx, sy, th), oracle.edge(x, g, st, sx, sy, th))
+
+
+def test_edge_pipelined_matches_single_call(jb):
+    """The host-buffer pipelined entry returns exactly the single-call result
+    (ragged last chunk included)."""
+    import torch
+    from paper_2503_10855_b200 import api
+    g, st, sx, sy, th = W.edge_filters()
+    x = np.stack([W.edge_frame(121, 245, seed=s) for s in range(7)])
+    ref = jb.edge_detection(x, g, st, sx, sy, th)
+    got = api.edge_detection_pipelined(torch.from_numpy(x).pin_memory(), g, st, sx, sy, th, chunk=3)
+    _bits_equal(got.numpy(), ref)
