@@ -48,6 +48,9 @@ SIGNATURES = {
     "jb_ipc_close": [_vp],
     "jb_euler_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_euler_stage_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "jb_euler_stage_p2p_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32,
+                               ctypes.c_uint32, _vp],
+    "jb_euler_push_f32": [_vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp],
     "jb_euler_step_factor_f32": [_u64, _vp, _vp, _vp, _vp],
     "jb_euler_flux_f32": [_u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_bfs": [_u64, _u64, _vp, _vp, _vp, _u32, _vp, _vp],

@@ -401,6 +401,11 @@ def euler_plan(neighbors, world: int, rank: int) -> dict:
                 neighbors=np.ascontiguousarray(loc.astype(np.int32)), recv=recv, send=send)
 
 
+def euler_plans(neighbors, world: int) -> list:
+    """euler_plan for every rank (each rank's halo computed once)."""
+    return [euler_plan(neighbors, world, r) for r in range(world)]
+
+
 def euler_halo_exchange(cur, plan: dict, group=None, backend=None):
     """Fill the halo columns of the SoA slab array cur[5, n_loc] from their
     owners (batched point-to-point send/recv of the owned values they need)."""
@@ -441,6 +446,131 @@ def euler_distributed(plan: dict, areas_own, normals_own, ff, vars_loc, iteratio
             exchange(cur)
             backend.stage(plan["n_own"], plan["n_loc"], j, areas_own, nbrs, normals_own, ff, cur, vars_loc, dst)
     return vars_loc[:, :plan["n_own"]]
+
+
+class EulerP2PSlabs:
+    """Peer-memory slab arrays of one rank for the fused multi-GPU CFD step.
+
+    One IPC-exportable allocation per rank holds the three SoA stage arrays
+    [V | t1 | t2] ([5][n_loc] each: own columns, then halo columns) and an
+    arrival counter.  After each stage a push kernel stores the values the
+    peers need straight into the peers' array of the same role and counts one
+    arrival on each of them; the next stage waits on its own counter."""
+
+    def __init__(self, neighbors, group=None, plans=None):
+        import ctypes
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        self.lib = _lib.load()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 8:
+            raise ValueError("the fused P2P step supports up to 8 ranks")
+        self.group = group
+        self.plans = plans or euler_plans(neighbors, self.world)
+        me = self.plan = self.plans[self.rank]
+        self.arr_bytes = [5 * p["n_loc"] * 4 for p in self.plans]
+        ptr = ctypes.c_void_p()
+        self._chk(self.lib.jb_p2p_alloc(3 * self.arr_bytes[self.rank] + 256, ctypes.byref(ptr)), "p2p_alloc")
+        self.base = ptr.value
+        h = ctypes.create_string_buffer(64)
+        self._chk(self.lib.jb_ipc_handle(self.base, h), "ipc_handle")
+        handles = [h.raw]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, h.raw, group=group)
+        self.peers, self.opened = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                self.peers.append(self.base)
+                continue
+            p = ctypes.c_void_p()
+            self._chk(self.lib.jb_ipc_open(ctypes.create_string_buffer(handles[r], 64), ctypes.byref(p)),
+                      f"ipc_open(rank {r})")
+            self.peers.append(p.value)
+            self.opened.append(p.value)
+        # push list: (own element, destination rank, column in its arrays)
+        own, peer, col = [], [], []
+        for s, idx in me["send"].items():
+            ps = self.plans[s]
+            own.append(idx)
+            peer.append(np.full(idx.size, s))
+            col.append(ps["n_own"] + np.searchsorted(ps["halo"], me["e0"] + idx))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        cat = (lambda xs: np.concatenate(xs).astype(np.int32)) if own else (lambda xs: np.zeros(0, np.int32))
+        self.push_own = torch.from_numpy(cat(own)).to(dev)
+        self.push_peer = torch.from_numpy(cat(peer)).to(dev)
+        self.push_col = torch.from_numpy(cat(col)).to(dev)
+        self.receivers = sorted(me["send"])
+        self.srcmask = sum(1 << r for r in me["recv"])  # ranks that push into this one
+        self.epoch = 0
+
+    def _chk(self, rc, what):
+        if rc:
+            raise RuntimeError(f"{what}: {_lib.last_error()}")
+
+    def buf(self, b: int, r: int = None) -> int:  # array b (0: V, 1: t1, 2: t2) of rank r
+        r = self.rank if r is None else r
+        return self.peers[r] + b * self.arr_bytes[r]
+
+    def flags(self, r: int = None) -> int:  # rank r's counters, one u32 per source rank
+        r = self.rank if r is None else r
+        return self.peers[r] + 3 * self.arr_bytes[r]
+
+    def array(self, b: int):
+        return _raw_tensor(self.buf(b), (5, self.plan["n_loc"]))
+
+    def push(self, b: int, stream):
+        import ctypes
+        w = self.world
+        bufs = (ctypes.c_void_p * 8)(*[self.buf(b, r) for r in range(w)])
+        strides = (ctypes.c_uint64 * 8)(*[p["n_loc"] for p in self.plans])
+        flags = (ctypes.c_void_p * 8)(*[self.flags(r) + 4 * self.rank for r in self.receivers])
+        self._chk(self.lib.jb_euler_push_f32(self.buf(b), self.plan["n_loc"], self.push_own.data_ptr(),
+                                             self.push_peer.data_ptr(), self.push_col.data_ptr(),
+                                             self.push_own.numel(), bufs, strides, flags, len(self.receivers),
+                                             w, stream), "euler_push")
+
+    def close(self):
+        for p in self.opened:
+            self.lib.jb_ipc_close(p)
+        self.opened = []
+        if self.base:
+            self.lib.jb_p2p_free(self.base)
+            self.base = None
+
+
+def euler_distributed_p2p(slabs: EulerP2PSlabs, areas_own, normals_own, ff, vars_own, iterations: int):
+    """Rodinia euler on this rank's element slab with the fused peer-memory
+    exchange: per RK stage one stage kernel (waits on the arrival counter)
+    and one push kernel (stores the halo values into the peers' arrays, counts
+    an arrival on each) -- no NCCL call and no host round trip.  Returns this
+    rank's own columns (a copy).  Bit-identical to the single-device run."""
+    import torch
+    plan, lib = slabs.plan, slabs.lib
+    n_own, n_loc = plan["n_own"], plan["n_loc"]
+    stream = torch.cuda.current_stream().cuda_stream
+    key = ("_nbrs", str(vars_own.device))
+    if key not in plan:
+        plan[key] = torch.as_tensor(plan["neighbors"]).to(vars_own.device)
+    nbrs = plan[key]
+    V = slabs.array(0)
+    V[:, :n_own] = vars_own
+    slabs.push(0, stream)  # V's halo values into the peers' V arrays
+    pushes = 1
+    for _ in range(iterations):
+        for j, (cb, db) in enumerate(((0, 1), (1, 2), (2, 0))):
+            target = slabs.epoch + pushes  # every source has pushed `pushes` times this call
+            rc = lib.jb_euler_stage_p2p_f32(n_own, n_loc, j, areas_own.data_ptr(), nbrs.data_ptr(),
+                                            normals_own.data_ptr(), ff.data_ptr(), slabs.buf(cb), slabs.buf(0),
+                                            slabs.buf(db), slabs.flags(), slabs.srcmask, target, stream)
+            if rc:
+                raise RuntimeError(f"euler_stage_p2p: {_lib.last_error()}")
+            slabs.push(db, stream)
+            pushes += 1
+    slabs.epoch += pushes
+    return V[:, :n_own].clone()
 
 
 class CudaEulerBackend:

@@ -146,3 +146,62 @@ def test_srad_fused_p2p_slabs_match_oracle(oracle, world):
     assert np.array_equal(got.view(np.uint32), got2.view(np.uint32))
     assert np.count_nonzero(got.view(np.uint32) != ref.view(np.uint32)) <= got.size // 10000
     np.testing.assert_allclose(got, ref, rtol=1e-5)
+
+
+# -------------------------------------------------- fused P2P CFD, 2-3 ranks
+def _euler_p2p_rank(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)  # all ranks on the one GPU (small grids: the kernels co-reside)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2503_10855_b200 import dist as D
+        areas, nb, normals, ff, v = W.euler_mesh(40, 23, seed=6)
+        slabs = D.EulerP2PSlabs(nb)
+        p = slabs.plan
+        e0, e1 = p["e0"], p["e1"]
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        args = (dev(areas[e0:e1]), dev(normals[:, :, e0:e1]), dev(ff), dev(v[:, e0:e1]))
+        out = D.euler_distributed_p2p(slabs, *args, 2)
+        out2 = D.euler_distributed_p2p(slabs, *args, 2)  # counters carry over between calls
+        torch.cuda.synchronize()
+        dist.barrier()
+        slabs.close()
+        q.put((rank, out.cpu().numpy(), out2.cpu().numpy()))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, RuntimeError(traceback.format_exc()), None))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_euler_fused_p2p_slabs_match_single_device(jb, world):
+    """Element slabs in separate processes on the one GPU: per RK stage one
+    stage kernel waiting on its arrival counter and one push kernel storing
+    the halo values into the peers' arrays (CUDA IPC).  Bit-identical to the
+    single-device entry."""
+    import socket
+
+    import torch.multiprocessing as mp
+    areas, nb, normals, ff, v = W.euler_mesh(40, 23, seed=6)
+    ref = jb.euler(2, areas, nb, normals, ff, v)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_euler_p2p_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (a, b)) for r, a, b in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+    for r, (a, _) in res.items():
+        if isinstance(a, Exception):
+            raise a
+    got = np.concatenate([res[r][0] for r in range(world)], axis=1)
+    got2 = np.concatenate([res[r][1] for r in range(world)], axis=1)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(got2.view(np.uint32), ref.view(np.uint32))
