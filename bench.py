@@ -480,7 +480,9 @@ class EulerWorkload(_DeviceCall):
         if world > 1:
             # element-range slabs of one mesh (strong scaling): slab-local
             # neighbour ids, NCCL halo exchange of the stage input per RK stage
-            self.plan = D.euler_plan(nb, world, rank)
+            self.plans = D.euler_plans(nb, world)
+            self.plan = self.plans[rank]
+            self.mesh_nb = nb
             e0, e1 = self.plan["e0"], self.plan["e1"]
             self.n_own = e1 - e0
             vl = np.zeros((5, self.plan["n_loc"]), np.float32)
@@ -497,12 +499,21 @@ class EulerWorkload(_DeviceCall):
             from paper_2503_10855_b200 import dist as D
             self.be = D.CudaEulerBackend()
             self.plan[("_nbrs", str(self.dev["nb"].device))] = self.dev["nb"]
+            # default: the fused peer-memory exchange (stage kernel + push
+            # kernel per RK stage); JB_EULER_NCCL=1 selects the NCCL path
+            self.slabs = None
+            if os.environ.get("JB_EULER_NCCL") != "1":
+                self.slabs = D.EulerP2PSlabs(self.mesh_nb, plans=self.plans)
+                self.slabs.plan[("_nbrs", str(self.dev["nb"].device))] = self.dev["nb"]
 
     def outputs_e2e(self):
         return [("v", self.dev["v"])]
 
     def config(self, world):
-        par = "single GPU" if world == 1 else f"element slabs/{world}: NCCL halo exchange per RK stage"
+        fused = getattr(self, "slabs", None) is not None
+        par = "single GPU" if world == 1 else (
+            f"element slabs/{world}: " + ("fused P2P (push kernel into peer memory + arrival counters) per RK stage"
+                                          if fused else "NCCL halo exchange per RK stage"))
         return {"workload": f"euler<{self.nelr}> {self.w}x{self.h} structured mesh, {self.iters} iterations x RK3",
                 "parallelism": par, "l2": f"{self.nelr * 128 / 1e6:.0f} MB streamed per stage > L2"}
 
@@ -518,7 +529,12 @@ class EulerWorkload(_DeviceCall):
         d = self.dev
         if self.world > 1:
             from paper_2503_10855_b200 import dist as D
-            D.euler_distributed(self.plan, d["areas"], d["normals"], d["ff"], d["v"], self.iters, self.be)
+            if self.slabs is not None:
+                res = D.euler_distributed_p2p(self.slabs, d["areas"], d["normals"], d["ff"],
+                                              d["v"][:, :self.n_own], self.iters)
+                d["v"][:, :self.n_own].copy_(res)
+            else:
+                D.euler_distributed(self.plan, d["areas"], d["normals"], d["ff"], d["v"], self.iters, self.be)
             return
         self.check_rc(self.lib.jb_euler_f32(self.nelr, self.iters, d["areas"].data_ptr(), d["nb"].data_ptr(),
                                             d["normals"].data_ptr(), d["ff"].data_ptr(), d["v"].data_ptr(),
@@ -861,6 +877,9 @@ def run_reference(args):
         return
     from oracle import oracle
     wl = WORKLOADS[args.workload](args, 0, 1) if not args.small else WORKLOADS[args.workload](args, 0, 1)
+    # every host thread: torch.distributed.run exports OMP_NUM_THREADS=1 to
+    # its workers, which would time a single-threaded reference at N > 1
+    oracle.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     threads = oracle.max_threads()
     vals = []
     for i in range(args.warmup + args.steps):
