@@ -13,7 +13,7 @@ from paper_2503_10855_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
 
-SETTINGS = settings(max_examples=12, deadline=None, derandomize=True,
+SETTINGS = settings(max_examples=40, deadline=None, derandomize=True,
                     suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
 
 
