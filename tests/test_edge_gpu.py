@@ -29,7 +29,9 @@ def test_edge_matches_golden(jb, name):
                                    (2, 1080, 1920), (4, 121, 245),
                                    # more frames than packed-ring slots (slot reuse), and an odd
                                    # width (no TMA, scalar reject units)
-                                   (12, 1080, 1920), (7, 1080, 1918)])
+                                   (12, 1080, 1920), (7, 1080, 1918),
+                                   # 4K frames: the packed ring holds only 2 slots (reject lag 1)
+                                   (3, 2160, 3840)])
 def test_edge_fused_vs_oracle(jb, oracle, shape):
     b, n, m = shape
     g, st, sx, sy, th = W.edge_filters()
