@@ -100,6 +100,10 @@ struct alignas(128) Smem {
   // are read from here, the ones with x - x0 even from the copy inA
   alignas(128) float raw[IR][RP];
   alignas(128) float inA[IR][IP];  // inA[r][c] = input(y0-5+r, x0-5+c)
+  // the packed tile, read by the async proxy (bulk tensor store) until
+  // thread 0's bulk_wait_read at the next tile's top; its own buffer, so the
+  // next tile's stage 0 may refill inA while the store is still reading
+  alignas(128) uint32_t P[TH][TW];
   float sm[SR][SR];       // smoothed tile (out-of-frame = clamped replica)
   uint32_t lapbits[LR][2];// laplacian > 0, bit = column within 32-col chunk
   uint32_t zcw[TH][2];    // zero crossing, bit = column within 32-col chunk
@@ -437,10 +441,11 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
     const bool col_ok = oc < TW && (!BORDER || x0 + oc < m);
     const int scol = min(oc, TW - 1);
     const int orow0 = rb * 15;
-    uint32_t *prow = a.packed + (size_t)(f % a.ring) * a.slot_px + (size_t)(y0 + orow0) * m + x0 + scol;
-    // TMA path: the packed tile goes to smem (aliasing inA, dead after the
-    // gaussian) and leaves with one bulk tensor store; the box clips borders
-    uint32_t(*P)[TW] = reinterpret_cast<uint32_t(*)[TW]>(&S.inA[0][0]);
+    uint32_t *prow = a.use_tma ? nullptr
+                               : a.packed + (size_t)(f % a.ring) * a.slot_px + (size_t)(y0 + orow0) * m + x0 + scol;
+    // TMA path: the packed tile goes to smem (S.P) and leaves with one bulk
+    // tensor store; the box clips borders
+    uint32_t(*P)[TW] = S.P;
     float sx[9], sy[9];
 #pragma unroll
     for (int q = 0; q < 9; q++) { sx[q] = c_sx[q]; sy[q] = c_sy[q]; }
@@ -500,7 +505,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   __syncthreads();
   if (tid == 0) {
     if (a.use_tma) {
-      tc::tma_store_3d_hint(&a.pmap, &S.inA[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
+      tc::tma_store_3d_hint(&a.pmap, &S.P[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
       tc::bulk_commit();
     }
     float v = S.wmax[0];
@@ -564,6 +569,10 @@ __device__ __forceinline__ void flush_done(const FusedArgs &a, Sched &q, unsigne
   if (newest_pending) tc::bulk_wait<1>();
   else tc::bulk_wait<0>();
   if (pd_max == 0xffffffffu) red_add(a.done + q.pd, 0u);  // never true: orders the red after the atom
+  // release the tile's bulk-stored lines (async proxy) to the generic loads
+  // of the reject units on other SMs
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  fence_acq_rel();
   red_add(a.done + q.pd, 1u);
   q.pd = -1;
 }
@@ -602,6 +611,7 @@ __device__ int publish_threshold(const FusedArgs &a, int f) {
 __device__ bool frame_bound(const FusedArgs &a, int f, unsigned long long r, unsigned d, int &A) {
   if (r >> 32) {
     A = (int)(unsigned)r;
+    fence_acq_rel();  // acquire: the frame's packed lines before the unit's loads
     return true;
   }
   const unsigned tpf = (unsigned)(a.tiles_x * a.tiles_y);
@@ -627,7 +637,7 @@ __device__ __forceinline__ float reject_px(uint32_t p, int A) {
 }
 
 // the whole CTA: reject unit `unit` with compare bound `A` (from thread 0)
-__device__ void reject_unit(const FusedArgs &a, int unit, int A) {
+__device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   const int f = unit / a.units, u = unit - f * a.units;
   const long long b0 = (long long)u * a.unit_px;
   const long long cnt = min((long long)a.unit_px, a.frame_px - b0);
@@ -637,16 +647,35 @@ __device__ void reject_unit(const FusedArgs &a, int unit, int A) {
     const int n4 = (int)(cnt >> 2);
     const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
     float4 *d4 = reinterpret_cast<float4 *>(dst);
-    for (int base = 0; base < n4; base += THREADS) {
-      const int i = base + threadIdx.x;
-      if (i < n4) {
-        const uint4 p = __ldcg(s4 + i);
-        __stcs(d4 + i, make_float4(reject_px(p.x, A), reject_px(p.y, A), reject_px(p.z, A), reject_px(p.w, A)));
+    // RB passes' loads in flight at once (one L2 round trip per RB passes,
+    // not one per pass), then the compares and streaming stores
+    constexpr int RB = 4;
+    for (int base = 0; base < n4; base += RB * THREADS) {
+      uint4 p[RB];
+#pragma unroll
+      for (int k = 0; k < RB; k++) {
+        const int i = base + k * THREADS + threadIdx.x;
+        if (i < n4) p[k] = __ldcg(s4 + i);
+      }
+#pragma unroll
+      for (int k = 0; k < RB; k++) {
+        const int i = base + k * THREADS + threadIdx.x;
+        if (i < n4)
+          __stcs(d4 + i, make_float4(reject_px(p[k].x, A), reject_px(p[k].y, A), reject_px(p[k].z, A),
+                                     reject_px(p[k].w, A)));
       }
       __syncwarp();
       // the slot base and unit start are 4 KB aligned: lane 8k starts a line
-      if (!(a.opts & 1) && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
+#pragma unroll
+      for (int k = 0; k < RB; k++) {
+        const int i = base + k * THREADS + threadIdx.x;
+        if (!(a.opts & 1) && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
+      }
     }
+    // the discards must be performed before the unit is counted: a discard
+    // still in flight when the slot's next frame is stored would drop the
+    // new lines
+    if (!(a.opts & 1) && (threadIdx.x & 7) == 0) fence_acq_rel();
   } else {
     for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), A);
   }
@@ -748,7 +777,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     // ---- the ring slot of frame f must be rejected; probe this tile's
     // reject frame (consumed at the tile's end)
     if (tid == 0) {
-      tc::bulk_wait_read<0>();  // the last packed tile has left smem
+      tc::bulk_wait_read<0>();  // the last packed tile has left S.P (the stage-0 barrier orders this before the sobel stage refills it)
       if (!slot_free(a, q, rf_, f)) {
         flush_done(a, q, pd_max, false);  // someone may be waiting on it
         while (ld_relaxed(a.rdone + f - a.ring) < (unsigned)a.units) __nanosleep(128);
