@@ -60,7 +60,8 @@ def load_issue(workload):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             e = json.load(f)[workload]
-        return {k: e[k] for k in ("issue_active_pct", "fma_pipe_pct", "tensor_pipe_pct") if k in e} or None
+        out = {k: e[k] for k in ("issue_active_pct", "fma_pipe_pct", "tensor_pipe_pct", "warp_inst") if k in e}
+        return out or None
     except Exception:
         return None
 
@@ -193,6 +194,7 @@ class EdgeWorkload:
         self.frames_host = W.edge_batch(self.local, self.n, self.m, seed=1000 + self.first) \
             if self.local else np.zeros((0, self.n, self.m), np.float32)
         self.frame_bytes = self.n * self.m * 4
+        self.inst_unit = ("px", self.n * self.m)
 
     def config(self, world):
         return {"workload": f"edge_detection batch={self.batch} frames {self.n}x{self.m} f32, gs=7 sz=3 sb=3",
@@ -685,6 +687,7 @@ class CavaWorkload(_DeviceCall):
         self.batch = 4 if args.small else 64
         self.r, self.c = (270, 480) if args.small else (1080, 1920)
         self.P = 16
+        self.inst_unit = ("px", self.r * self.c)
         f0, self.local = D.shard_frames(self.batch, world, rank)
         raw = W.cava_raw(self.batch, self.r, self.c)[f0:f0 + self.local]
         self.host = {"raw": np.ascontiguousarray(raw)}
@@ -848,6 +851,13 @@ def run_ours(args):
             roofline.update(wl.roofline_extra(avg_ms, per_launch_units))
         issue = load_issue(args.workload)
         if issue:
+            # thread-instructions per unit (instr/px vs FP32
+            # issue for the compute-bound stencils); the capture ran this
+            # same default configuration, one launch
+            wi = issue.pop("warp_inst", None)
+            iu = getattr(wl, "inst_unit", None)
+            if wi and iu and world == 1 and not args.small:
+                issue[f"thread_inst_per_{iu[0]}"] = round(wi * 32 / (per_launch_units * iu[1]), 1)
             roofline["ncu_issue"] = issue
     h2d, d2h = wl.e2e_bytes()
     res = {"metric": wl.metric, "value": round(value, 4 if not hib else 2), "unit": wl.unit, "n_gpus": world,
