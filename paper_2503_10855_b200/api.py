@@ -514,10 +514,17 @@ def oracle_execute(module, entry: str, dyn_consts, args, max_steps: int = 50_000
     """Drop-in for skiff.runtime.oracle.oracle_execute (oracle.py:28-32).
 
     ``module`` may be a skiff ``Module`` (its function table must contain
-    ``entry``) or None.  ``max_steps`` is accepted for signature parity; the
+    ``entry``; an entry under another name is matched to a B200 kernel by
+    its signature, see planner.py) or None.  ``max_steps`` is accepted for signature parity; the
     device path has no interpreter budget."""
     del max_steps
     fns = getattr(module, "functions", None)
-    if fns is not None and entry not in fns:
-        raise KeyError(entry)
+    if fns is not None:
+        if entry not in fns:
+            raise KeyError(entry)
+        if entry not in ENTRIES:
+            # a renamed / scheduled entry: pick the kernel by signature and
+            # extents (planner.select_kernel, SURVEY §8(f)1)
+            from .planner import select_kernel
+            entry = select_kernel(module, entry, [int(x) for x in dyn_consts]).entry
     return execute(entry, dyn_consts, args)
