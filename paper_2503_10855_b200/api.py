@@ -488,6 +488,14 @@ ENTRIES: dict[str, Entry] = {
 
 def execute(entry: str, dyn_consts, args):
     """Run Juno ``entry`` on the B200: ``oracle_execute`` without the module."""
+    dcs, args = validate(entry, dyn_consts, args)
+    return ENTRIES[entry].run(dcs, args)
+
+
+def validate(entry: str, dyn_consts, args):
+    """The invocation checks of ``execute``: entry known, dynamic constants
+    counted and non-negative (dynconst.py:179-204), argument extents equal to
+    the ones the dynamic constants give.  Returns (dcs, args)."""
     if entry not in ENTRIES:
         raise RuntimeError_(f"no B200 kernel for entry {entry!r}; known: {sorted(ENTRIES)}")
     spec = ENTRIES[entry]
@@ -507,7 +515,7 @@ def execute(entry: str, dyn_consts, args):
         if got != tuple(want) and got[1:] != tuple(want):
             raise RuntimeError_(f"{entry}: argument {idx} has shape {got}, expected {tuple(want)} "
                                 f"under dyn-consts {dict(zip(spec.dyn_consts, dcs))}")
-    return spec.run(dcs, args)
+    return dcs, args
 
 
 def oracle_execute(module, entry: str, dyn_consts, args, max_steps: int = 50_000_000):
