@@ -714,7 +714,7 @@ class CavaWorkload(_DeviceCall):
     def algorithmic_bytes_per_unit(self):
         return 6 * self.r * self.c  # u8 x3 in + u8 x3 out
 
-    e2e_api = "paper_2503_10855_b200.api.cava_pipelined (pinned host in/out, 2-frame chunks)"
+    e2e_api = "paper_2503_10855_b200.api.cava_pipelined (pinned host in/out, 8-frame chunks)"
 
     def step_e2e(self):
         """Public API on pinned host buffers, copies overlapped with the kernels."""

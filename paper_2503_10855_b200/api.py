@@ -245,7 +245,7 @@ def _pipelined(x, out, chunk: int, key, launch):
     return out
 
 
-def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 8):
+def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 16):
     """Host-buffer edge detection with copy/compute overlap (``_pipelined``).
 
     ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
@@ -272,7 +272,7 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
     return _pipelined(x, out, chunk, "edge", launch)
 
 
-def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 2):
+def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 8):
     """Host-buffer CAVA over a batch u8[batch,3,r,c] with copy/compute overlap
     (``_pipelined``); returns ``out`` (a host u8 tensor of the input's shape)."""
     torch = _torch()
