@@ -30,8 +30,15 @@ namespace bfs {
 
 constexpr int THREADS = 512;
 constexpr int LQ = 4096;  // block-local queue capacity
-constexpr int EB = 8;     // edges per batch
-constexpr int VPT = 2;    // frontier vertices per thread per round
+#ifndef BFS_EB
+#define BFS_EB 8
+#endif
+#ifndef BFS_VPT
+#define BFS_VPT 2
+#endif
+constexpr int EB = BFS_EB;       // edges per lane per batch
+constexpr int CAP = 32 * EB;     // per-warp edge-id buffer (one batch)
+constexpr int VPT = BFS_VPT;  // frontier vertices per thread per round
 constexpr uint8_t kUnseen = 0xFF, kDeep = 0xFE;  // level byte codes
 
 struct Args {
@@ -63,6 +70,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t lq[LQ];
   __shared__ uint32_t lcount, lbase;
+  __shared__ uint32_t ebuf[THREADS / 32][CAP];
   const uint32_t gtid = blockIdx.x * THREADS + threadIdx.x;
   const uint32_t gsize = gridDim.x * THREADS;
 
@@ -104,27 +112,60 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
           }
         }
       }
+      // warp-cooperative expansion: the warp's adjacency ranges are laid out
+      // back to back in a per-warp buffer of edge ids (a warp scan gives each
+      // range its offset), then all 32 lanes walk the buffer together --
+      // balanced across lanes whatever the degrees, and consecutive lanes
+      // read consecutive edges.  Ranges longer than the buffer continue in
+      // the next pass.
+      uint32_t *eb = ebuf[threadIdx.x >> 5];
+      const int lane = threadIdx.x & 31;
 #pragma unroll
       for (int k = 0; k < VPT; k++) {
-        for (uint32_t b = 0; b < ne[k]; b += EB) {
-          uint32_t v[EB], w[EB];
+        uint32_t cur = e0[k];
+        const uint32_t end = e0[k] + ne[k];
+#pragma unroll 1
+        for (;;) {
+          const uint32_t rem = min(end - cur, (uint32_t)CAP);
+          uint32_t inc = rem;
 #pragma unroll
-          for (int j = 0; j < EB; j++) v[j] = b + j < ne[k] ? __ldg(a.edges + e0[k] + b + j) : 0xffffffffu;
-          // probes may come from L1 (stale only towards "unseen": the
-          // atomicOr below re-checks)
-#pragma unroll
-          for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
-#pragma unroll
-          for (int j = 0; j < EB; j++) {
-            if (v[j] == 0xffffffffu) continue;
-            const uint32_t bit = 1u << (v[j] & 31);
-            if (w[j] & bit) continue;
-            const uint32_t old = atomicOr(a.visited + (v[j] >> 5), bit);
-            if (old & bit) continue;  // someone else claimed v
-            a.level[v[j]] = nb;
-            if (nb == kDeep) a.cost[v[j]] = nl;
-            enqueue(a, v[j], nxt, lq, lcount, nq);
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += t;
           }
+          const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+          if (total == 0) break;
+          const uint32_t off = inc - rem;
+          const uint32_t take = off >= (uint32_t)CAP ? 0u : min(rem, (uint32_t)CAP - off);
+          for (uint32_t j = 0; j < take; j++) eb[off + j] = cur + j;
+          cur += take;
+          __syncwarp();
+          const uint32_t cnt = min(total, (uint32_t)CAP);
+#pragma unroll 1
+          for (uint32_t b = 0; b < cnt; b += 32 * EB) {
+            uint32_t v[EB], w[EB];
+#pragma unroll
+            for (int j = 0; j < EB; j++) {
+              const uint32_t i = b + j * 32 + lane;
+              v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
+            }
+            // probes may come from L1 (stale only towards "unseen": the
+            // atomicOr below re-checks)
+#pragma unroll
+            for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
+#pragma unroll
+            for (int j = 0; j < EB; j++) {
+              if (v[j] == 0xffffffffu) continue;
+              const uint32_t bit = 1u << (v[j] & 31);
+              if (w[j] & bit) continue;
+              const uint32_t old = atomicOr(a.visited + (v[j] >> 5), bit);
+              if (old & bit) continue;  // someone else claimed v
+              a.level[v[j]] = nb;
+              if (nb == kDeep) a.cost[v[j]] = nl;
+              enqueue(a, v[j], nxt, lq, lcount, nq);
+            }
+          }
+          __syncwarp();
         }
       }
       __syncthreads();
