@@ -64,6 +64,26 @@ def test_euler_matches_oracle_bitwise(jb, oracle, wh, iters):
     assert not np.array_equal(got, v)  # the state actually evolved
 
 
+def test_euler_fast_path_fallback_bitwise(jb, oracle):
+    """Elements outside the fast division/sqrt range (tiny and huge states,
+    zero velocity, zero and negative pressure) take the IEEE recompute in
+    euler_rk_kernel; the whole result must stay bit-identical."""
+    areas, nb, normals, ff, v = _mesh(64, 48, seed=9)
+    v = v.copy()
+    n = v.shape[1]
+    rng = np.random.default_rng(9)
+    idx = rng.choice(n, size=n // 8, replace=False)
+    k = len(idx) // 5
+    v[0, idx[:k]] *= np.float32(1e-9)                        # tiny density
+    v[1:4, idx[k:2 * k]] = 0.0                               # zero velocity: ssq = 0
+    v[:, idx[2 * k:3 * k]] *= np.float32(3e7)                # huge state
+    v[4, idx[3 * k:4 * k]] = 0.5 * v[0, idx[3 * k:4 * k]] * 1e-3  # pressure below zero
+    v[1, idx[4 * k:]] = np.float32(2.0 ** -30)               # subnormal-ish velocity squares
+    got = jb.euler(2, areas, nb, normals, ff, v)
+    ref = oracle.euler(areas, nb, normals, ff, v, 2)
+    _exact(got, ref)
+
+
 def test_euler_stages_bitwise(jb, oracle):
     areas, nb, normals, ff, v = _mesh(80, 60, seed=3)
     _exact(jb.euler_step_factor(v, areas), oracle.euler_step_factor(v, areas))
