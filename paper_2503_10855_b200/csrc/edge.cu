@@ -118,7 +118,8 @@ struct alignas(128) Smem {
   Sched q;                // thread 0 only
 };
 
-// flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair
+// flags[0]: 1 if the filters admit the fast path; flags[1]: standard sobel pair;
+// flags[2]: the gaussian is mirror-symmetric top to bottom (bitwise)
 __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__restrict__ st,
                                   const float *__restrict__ sx, const float *__restrict__ sy,
                                   int *flags) {
@@ -139,8 +140,15 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
     ok &= (b == 0.f || b == 1.f || b == 2.f || b == 4.f);
     std_sobel &= (sx[k] == SX[k]) && (sy[k] == SY[k]);
   }
+  // vertical mirror symmetry of the gaussian, bit for bit: then the product
+  // of an input pixel with w[i][j] equals its product with w[6-i][j], and
+  // the fast gaussian computes it once for both output rows
+  int vsym = 1;
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 7; j++) vsym &= __float_as_uint(gf[i * 7 + j]) == __float_as_uint(gf[(6 - i) * 7 + j]);
   flags[0] = ok;
   flags[1] = ok && std_sobel;
+  flags[2] = ok && vsym;
 }
 
 struct FusedArgs {
@@ -223,6 +231,11 @@ __device__ __forceinline__ Smem &smem_tile() {
 // stage 1, fast path: packed gaussian of 8 smoothed rows x 2 columns per
 // lane.  Not inlined: one copy is shared by every tile variant, which keeps
 // the hot code inside the instruction cache.
+// VSYM: w[i][j] == w[6-i][j] bitwise; the weight is read from the canonical
+// row min(i, 6-i), so the two products of an input pair with mirrored taps are
+// one expression (computed once: the rounded product is the same value for
+// both output rows, and each output still adds its 49 terms in tap order).
+template <bool VSYM>
 __device__ __noinline__ void gauss_fast(int warp, int lane) {
   Smem &S = smem_tile();
   const int r0 = warp * 8;
@@ -242,7 +255,8 @@ __device__ __noinline__ void gauss_fast(int warp, int lane) {
       const int i = iy - o;
       if (i >= 0 && i < 7) {
 #pragma unroll
-        for (int j = 0; j < 7; j++) acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[i * 7 + j]));
+        for (int j = 0; j < 7; j++)
+          acc[o] = f2_add_ftz(acc[o], f2_mul(v[j], c_gauss[(VSYM ? (i < 6 - i ? i : 6 - i) : i) * 7 + j]));
       }
     }
   }
@@ -262,7 +276,8 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   {
     const int r0 = warp * 8;  // 8 smoothed rows per warp, 2 columns per lane
     if (FAST) {
-      gauss_fast(warp, lane);
+      if (a.flags[2]) gauss_fast<true>(warp, lane);
+      else gauss_fast<false>(warp, lane);
     } else {
       float2 acc[8];
 #pragma unroll

@@ -41,6 +41,25 @@ def test_edge_fused_vs_oracle(jb, oracle, shape):
     _bits_equal(out, ref)
 
 
+@pytest.mark.parametrize("kind", ["random", "vsym_only", "perturbed_one_tap"])
+def test_edge_gaussian_variants(jb, oracle, kind):
+    """The packed gaussian shares mirrored products only when the filter is
+    bitwise symmetric top to bottom; other 7x7 filters take the plain packed
+    path.  Both must be bit-exact."""
+    g, st, sx, sy, th = W.edge_filters()
+    rng = np.random.default_rng(11)
+    if kind == "random":
+        g = (rng.random((7, 7), dtype=np.float32) / np.float32(49.0)).astype(np.float32)
+    elif kind == "vsym_only":
+        top = rng.random((4, 7), dtype=np.float32) / np.float32(49.0)
+        g = np.concatenate([top, top[2::-1]]).astype(np.float32)   # rows i and 6-i equal
+    else:
+        g = g.copy()
+        g[6, 3] = np.nextafter(g[6, 3], np.float32(1))              # breaks the symmetry by 1 ulp
+    x = np.stack([W.edge_frame(200, 300, seed=s) for s in range(2)])
+    _bits_equal(jb.edge_detection(x, g, st, sx, sy, th), oracle.edge(x, g, st, sx, sy, th))
+
+
 def test_edge_exact_fallback_paths(jb, oracle):
     """Tiles whose data or filters violate the fast-path guard run the exact
     scalar path: negative pixels, subnormals, a non-unit structure and a
