@@ -125,10 +125,15 @@ def _max(a, b):
     return ("max", a, b)
 
 
+def _lit(x):
+    """A reference DcLiteral as a plain int (so sizes fold), else as is."""
+    return int(x.value) if type(x).__name__ == "DcLiteral" else x
+
+
 def _product(factors):
     out = 1
     for f in factors:
-        out = _mul(out, f)
+        out = _mul(out, _lit(f))
     return out
 
 

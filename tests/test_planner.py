@@ -192,6 +192,28 @@ fn twice<n: usize>(x: f32[n]) -> f32[n] {
         P.select_kernel(mod, "nope")
 
 
+def test_plans_of_every_golden_fixture_program():
+    """Every Juno fixture program of oracle/gen_golden.py plans after the
+    reference's own forkify + infer-attributes passes."""
+    import re
+    src = open(os.path.join(ROOT, "oracle", "gen_golden.py")).read()
+    progs = dict(re.findall(r'^([A-Z_]+) = """(.*?)"""', src, re.S | re.M))
+    assert len(progs) >= 8
+    planned = 0
+    for name, text in progs.items():
+        mod = _module(text, "forkify(*); infer-attributes(*);")
+        for fname, fn in mod.functions.items():
+            plan = P.launch_plan(fn)
+            assert plan.describe().startswith(fname)
+            for f in plan.forks():
+                assert f.role in (P.BLOCK, P.THREAD, P.SEQUENTIAL)
+            dcs = [7] * fn.num_dyn_consts
+            ev = plan.evaluate(dcs)
+            assert ev["blocks"] * ev["threads"] == ev["size"] >= 1
+            planned += 1
+    assert planned >= 14
+
+
 @pytest.mark.gpu
 def test_execute_module_runs_the_selected_kernel(jb, oracle):
     """A scheduled module runs end to end: plan -> select -> B200 kernel,
