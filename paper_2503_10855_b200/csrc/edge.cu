@@ -689,7 +689,10 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
     float4 *d4 = reinterpret_cast<float4 *>(dst);
     // RB passes' loads in flight at once (one L2 round trip per RB passes,
     // not one per pass), then the compares and streaming stores
-    constexpr int RB = 4;
+#ifndef EDGE_RB
+#define EDGE_RB 4
+#endif
+    constexpr int RB = EDGE_RB;
     for (int base = 0; base < n4; base += RB * THREADS) {
       uint4 p[RB];
 #pragma unroll
@@ -1124,7 +1127,10 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   JB_REQUIRE((uint64_t)tpf * batch < (1ull << 31), "edge_detection: batch too large");
   // packed-gradient ring: as many frame slots as fit ~64 MB of L2 (>= 2)
   const size_t slot_px = (frame_px + 1023) / 1024 * 1024;
-  size_t ring = (64ull << 20) / (slot_px * 4);
+#ifndef EDGE_RING_MB
+#define EDGE_RING_MB 64
+#endif
+  size_t ring = ((size_t)EDGE_RING_MB << 20) / (slot_px * 4);
   if (ring < 2) ring = 2;
   if (ring > batch) ring = batch;
   // reject units: one per ~two compute tiles, whole 4 KB blocks of lines
