@@ -118,7 +118,7 @@ class Dist:
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML during the timed region."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.005):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
