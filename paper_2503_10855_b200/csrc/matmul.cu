@@ -389,10 +389,13 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   const long long tiles = (long long)((l + BN - 1) / BN) * (long long)((n + BM - 1) / BM);
   const int kblocks = (int)((m + BK - 1) / BK);
-  // split K so that at least ~one CTA per SM runs; the partial tiles meet in
-  // C through f32 vector reductions (2 addends: order independent)
+  // split K in two when that still fits one CTA per SM; the partial tiles
+  // meet in C through f32 vector reductions onto zero.  Two addends only:
+  // 0 + p0 + p1 rounds the same in either order, so the result is
+  // deterministic run to run (more slices would make it depend on the order
+  // the reductions land)
   int splitk = 1;
-  while (splitk < 4 && tiles * splitk * 2 <= sm_count() && kblocks >= splitk * 2 * 4) splitk *= 2;
+  if (tiles * 2 <= sm_count() && kblocks >= 8) splitk = 2;
   if (splitk > 1) JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
   dim3 grid((unsigned)((l + BN - 1) / BN), (unsigned)((n + BM - 1) / BM), (unsigned)splitk);
   void *tok = prof_begin("matmul_tcgen05", s);

@@ -57,3 +57,15 @@ def test_matmul_identity_and_zero_k(jb):
     np.testing.assert_allclose(jb.matmul(eye, a), a, rtol=1e-6, atol=0)  # truncated-hi 3xTF32: ~2^-21
     z = jb.execute("matmul", [3, 0, 5], [np.zeros((3, 0), np.float32), np.zeros((0, 5), np.float32)])
     assert z.shape == (3, 5) and not z.any()
+
+
+@pytest.mark.parametrize("shape", [(256, 2048, 256), (1024, 1024, 1024), (128, 4096, 128)])
+def test_matmul_deterministic_run_to_run(jb, shape):
+    """Split-K slices meet through reductions; with two addends per element
+    the result cannot depend on their arrival order: repeated calls are
+    bit-identical."""
+    n, m, l = shape
+    a, b = W.matmul_inputs(n, m, l, seed=7)
+    first = jb.matmul(a, b)
+    for _ in range(4):
+        assert np.array_equal(jb.matmul(a, b).view(np.uint32), first.view(np.uint32))
