@@ -858,6 +858,17 @@ def run_ours(args):
             iu = getattr(wl, "inst_unit", None)
             if wi and iu and world == 1 and not args.small:
                 issue[f"thread_inst_per_{iu[0]}"] = round(wi * 32 / (per_launch_units * iu[1]), 1)
+            if wi and world == 1 and not args.small:
+                # the SM issue roofline for the compute-bound kernels: thread
+                # instructions per second of this run's launches against one
+                # instruction per lane per clock on every SM
+                mhz = clk.summary().get("sm_mhz") or 1965.0
+                peak_ti = torch.cuda.get_device_properties(0).multi_processor_count * 128 * mhz * 1e6
+                ach_ti = wi * 32 / (avg_ms / 1e3)
+                issue["issue_roofline"] = {"achieved_tinst_per_s": float(f"{ach_ti:.4g}"),
+                                           "peak_tinst_per_s": float(f"{peak_ti:.4g}"),
+                                           "frac": round(ach_ti / peak_ti, 3),
+                                           "note": "warp instructions from the ncu capture x 32 / live avg launch time"}
             roofline["ncu_issue"] = issue
     h2d, d2h = wl.e2e_bytes()
     res = {"metric": wl.metric, "value": round(value, 4 if not hib else 2), "unit": wl.unit, "n_gpus": world,
