@@ -6,10 +6,13 @@
 //
 // B200 design: one persistent cooperative kernel runs every
 // level (no host round trip per level):
-//  * top-down frontier-queue expansion, thread per frontier vertex; its
-//    edges are processed in batches of 8 whose edge-id loads, visited probes
-//    and claiming atomics are each issued back to back (memory-level
-//    parallelism instead of three dependent round trips per edge);
+//  * top-down frontier-queue expansion, two frontier vertices per thread
+//    per round; a warp lays its vertices' adjacency ranges back to back in a
+//    shared edge-id buffer (warp scan) and all 32 lanes walk it together,
+//    8 edges per lane per batch whose edge-id loads, visited probes and
+//    claiming atomics are each issued back to back (balanced lanes whatever
+//    the degrees; memory-level parallelism instead of three dependent round
+//    trips per edge);
 //  * a visited bitmap (n/8 bytes: 2 MiB at n = 2^24, L2-resident) filters
 //    the random neighbour probes before the claiming atomicOr;
 //  * levels go to a byte array (n bytes, L2-resident) instead of random
