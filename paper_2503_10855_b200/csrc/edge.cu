@@ -15,13 +15,16 @@
 // B200 design:
 //  * edge_fused_kernel: one persistent kernel for the whole batch. A CTA owns
 //    a 60x60 output tile; it stages the 70x70 clamped input tile in shared
-//    memory (twice: aligned and shifted by one column so every gaussian tap
-//    is one conflict-free 64-bit LDS of two adjacent pixels), computes the
-//    64x64 smoothed tile with packed FMUL2/FADD2 (bit-exact, see the tile
-//    guard), the 62x62 laplacian with separable min/max, packs its sign
+//    memory (twice: the 16-byte-aligned TMA box and a copy shifted by three
+//    columns, so every gaussian tap is one conflict-free 64-bit LDS of two
+//    adjacent pixels), computes the 64x64 smoothed tile with packed
+//    FMUL2/FADD2 (bit-exact, see the tile guard; a product shared by the two
+//    mirrored taps of a top-bottom symmetric filter is computed once), the
+//    62x62 laplacian with separable min/max, packs its sign
 //    bits with warp ballots, derives zero crossings with 64-bit mask logic,
-//    computes the sobel gx^2+gy^2, and stores it | zc<<31 (4 B/px) plus a
-//    warp->block->grid max (atomicMax on the float bits, per frame).
+//    computes the sobel gx^2+gy^2, and stores it | zc<<31 (4 B/px, one TMA
+//    bulk tensor store from its own shared buffer) plus a warp->block->grid
+//    max (atomicMax on the float bits, per frame).
 //  * the reject runs inside the same kernel as a second work queue: a frame
 //    whose tiles are done publishes its threshold (sqrt.rn is monotone, so
 //    zc && sqrt(g) > theta*sqrt(max g) becomes an integer compare on the
