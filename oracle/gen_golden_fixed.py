@@ -1,0 +1,168 @@
+"""TEST INFRASTRUCTURE: golden vectors for Juno programs in their natural
+(scalar-accumulator) form, from the reference interpreter with its
+dependents defect fixed.  SURVEY.md §8(f)3, Appendix A.
+
+skiff's ``_Eval.dependents`` (/root/reference/pkg/src/skiff/runtime/
+oracle.py:55-70) walks through phi and reduce nodes, so entering an inner
+loop invalidates the *current* value of an enclosing loop's phi and the
+interpreter raises "cannot evaluate node kind phi" (Appendix A.2: every
+stencil tap loop with a scalar accumulator, e.g. Appendix C's gaussian).
+The fix named in SURVEY Appendix A: stop the walk at phi/reduce nodes other
+than the roots themselves -- their values are owned by the control walk,
+which re-roots an invalidation whenever it updates them.
+
+This script (run in the build container, where /root/reference exists):
+  1. shows the unpatched interpreter fails on the accumulator programs;
+  2. checks the patched interpreter reproduces committed golden fixtures of
+     programs the unpatched one runs (matmul, gaussian in += form, BFS):
+     the patch changes nothing where the original works;
+  3. writes tests/golden/fixed_interp.npz: the gaussian and the max fold in
+     scalar-accumulator form on the edge_12x16_g7 inputs, and an abs-sum
+     with an if inside the loop (Appendix A.2 (i)).
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
+"""
+import contextlib
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import gen_golden as G  # noqa: E402  (imports skiff from /root/reference)
+
+from skiff.runtime import oracle as O  # noqa: E402
+
+GAUSS_ACC = """
+#[entry]
+fn gaussian_acc<n, m, gs: usize>(input: f32[n, m], filter: f32[gs, gs],
+                                 ri: u64[n, gs], ci: u64[m, gs]) -> f32[n, m] {
+  let res : f32[n, m];
+  for r in 0..n {
+    for c in 0..m {
+      let s : f32 = 0.0;
+      for i in 0..gs {
+        for j in 0..gs {
+          s = s + input[ri[r, i], ci[c, j]] * filter[i, j];
+        }
+      }
+      res[r, c] = s;
+    }
+  }
+  return res;
+}
+"""
+
+MAX_ACC = """
+#[entry]
+fn max_acc<n, m: usize>(g: f32[n, m]) -> f32[n] {
+  let rowmax : f32[n];
+  for i in 0..n {
+    let mx : f32 = g[i, 0];
+    for j in 0..m {
+      if g[i, j] > mx { mx = g[i, j]; }
+    }
+    rowmax[i] = mx;
+  }
+  return rowmax;
+}
+"""
+
+ABS_SUM = """
+#[entry]
+fn abs_sum<n, m: usize>(x: f32[n, m]) -> f32[n] {
+  let out : f32[n];
+  for i in 0..n {
+    let acc : f32 = 0.0;
+    for j in 0..m {
+      let v : f32 = x[i, j];
+      if v < 0.0 { v = -v; }
+      acc = acc + v;
+    }
+    out[i] = acc;
+  }
+  return out;
+}
+"""
+
+
+def _fixed_dependents(self, roots):
+    """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
+    phi / reduce nodes that are not roots."""
+    got = self._dependents_cache.get(roots)
+    if got is not None:
+        return got
+    rootset = set(roots)
+    out = set()
+    stack = list(roots)
+    while stack:
+        x = stack.pop()
+        for u in self.users.get(x, ()):
+            node = self.fn.node(u)
+            if u in out or node.is_control:
+                continue
+            if node.kind in ("phi", "reduce") and u not in rootset:
+                continue
+            out.add(u)
+            stack.append(u)
+    out |= rootset
+    self._dependents_cache[roots] = out
+    return out
+
+
+@contextlib.contextmanager
+def fixed_interpreter():
+    orig = O._Eval.dependents
+    O._Eval.dependents = _fixed_dependents
+    try:
+        yield
+    finally:
+        O._Eval.dependents = orig
+
+
+def run_fixed(src, entry, dcs, args):
+    with fixed_interpreter():
+        return G.run(src, entry, dcs, args)
+
+
+def main():
+    golden = os.path.join(G.OUT)
+    e = np.load(os.path.join(golden, "edge_12x16_g7.npz"))
+    n, m = e["input"].shape
+    gs = e["gaussian"].shape[0]
+    ri, ci = G.clamp_idx(n, gs), G.clamp_idx(m, gs)
+    # 1. the defect
+    for src, entry, dcs, args in [(GAUSS_ACC, "gaussian_acc", [n, m, gs], [e["input"], e["gaussian"], ri, ci]),
+                                  (ABS_SUM, "abs_sum", [2, 3], [np.ones((2, 3), np.float32)])]:
+        try:
+            G.run(src, entry, dcs, args)
+            print(f"{entry}: unpatched interpreter ran (defect not reproduced)")
+        except Exception as ex:  # the reference's RuntimeError_
+            print(f"{entry}: unpatched interpreter fails as in Appendix A: {type(ex).__name__}: {ex}")
+    # 2. the patch is transparent where the original works
+    mm = np.load(os.path.join(golden, "matmul.npz"))
+    got = run_fixed(G.MATMUL, "matmul", [8, 8, 8], [mm["8x8x8_a"], mm["8x8x8_b"]])
+    assert np.array_equal(got.view(np.uint32), mm["8x8x8_res"].view(np.uint32)), "matmul changed"
+    sm = run_fixed(G.GAUSS, "gaussian_smoothing", [n, m, gs], [e["input"], e["gaussian"], ri, ci])
+    assert np.array_equal(sm.view(np.uint32), e["smoothed"].view(np.uint32)), "gaussian (+= form) changed"
+    b = np.load(os.path.join(golden, "bfs_60.npz"))
+    cost = run_fixed(G.BFS, "bfs", [60, len(b["edges"])],
+                     [b["starting"].astype(np.uint64), b["no_of_edges"].astype(np.uint64),
+                      b["edges"].astype(np.uint64), np.uint64(int(b["source"]))])
+    assert np.array_equal(cost, b["cost"]), "bfs changed"
+    print("patched interpreter reproduces matmul, gaussian (+= form) and bfs golden vectors")
+    # 3. accumulator-form programs
+    acc = run_fixed(GAUSS_ACC, "gaussian_acc", [n, m, gs], [e["input"], e["gaussian"], ri, ci])
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((5, 9)).astype(np.float32)
+    rowmax = run_fixed(MAX_ACC, "max_acc", [5, 9], [x])
+    absum = run_fixed(ABS_SUM, "abs_sum", [5, 9], [x])
+    out = os.path.join(golden, "fixed_interp.npz")
+    np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
+                        x=x, rowmax=rowmax, abs_sum=absum)
+    print(f"wrote {out}; gaussian_acc == committed smoothed: "
+          f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
+
+
+if __name__ == "__main__":
+    main()

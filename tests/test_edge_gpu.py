@@ -25,6 +25,16 @@ def test_edge_matches_golden(jb, name):
         _bits_equal(st[k], g[k])
 
 
+def test_edge_gaussian_matches_fixed_interpreter_accumulator_form(jb):
+    """The smoothed stage against skiff's interpreter (Appendix A defect
+    fixed, oracle/gen_golden_fixed.py) running the gaussian in its natural
+    scalar-accumulator form."""
+    g = golden("fixed_interp")
+    e = golden("edge_12x16_g7")
+    st = jb.edge_detection_stages(g["edge_input"], g["gaussian"], e["structure"], e["sx"], e["sy"], e["theta"])
+    _bits_equal(st["smoothed"], g["gaussian_acc"])
+
+
 @pytest.mark.parametrize("shape", [(1, 60, 60), (2, 61, 59), (3, 128, 200), (1, 7, 5), (1, 1, 1),
                                    (2, 1080, 1920), (4, 121, 245),
                                    # more frames than packed-ring slots (slot reuse), and an odd

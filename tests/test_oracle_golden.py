@@ -77,3 +77,32 @@ def test_spec_known_answers(oracle):
     for n, want in ((8, 36.0), (1000, 500500.0)):
         v = np.arange(1, n + 1, dtype=np.float32)[:, None]
         assert oracle.matmul(np.ones((1, n), np.float32), v)[0, 0] == want
+
+
+def test_fixed_interpreter_accumulator_programs(oracle):
+    """tests/golden/fixed_interp.npz comes from skiff's own interpreter with
+    the Appendix A dependents defect fixed (oracle/gen_golden_fixed.py):
+    the gaussian in its scalar-accumulator form (which the unpatched
+    interpreter cannot run) must equal the restatement's smoothed stage, and
+    the per-row max fold / abs-sum must equal sequential f32 folds."""
+    g = golden("fixed_interp")
+    e = golden("edge_12x16_g7")
+    st = oracle.edge_frame(g["edge_input"], g["gaussian"], e["structure"], e["sx"], e["sy"], e["theta"],
+                           stages=True)
+    _eq(st["smoothed"], g["gaussian_acc"])
+    x = g["x"]
+    rowmax = []
+    for r in x:
+        mx = r[0]
+        for v in r:
+            if v > mx:
+                mx = v
+        rowmax.append(mx)
+    _eq(np.asarray(g["rowmax"]), np.array(rowmax, np.float32))
+    sums = []
+    for r in x:
+        acc = np.float32(0.0)
+        for v in r:
+            acc = np.float32(acc + np.float32(abs(v)))
+        sums.append(acc)
+    _eq(np.asarray(g["abs_sum"]), np.array(sums, np.float32))
