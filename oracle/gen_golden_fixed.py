@@ -17,8 +17,9 @@ This script (run in the build container, where /root/reference exists):
      programs the unpatched one runs (matmul, gaussian in += form, BFS):
      the patch changes nothing where the original works;
   3. writes tests/golden/fixed_interp.npz: the gaussian and the max fold in
-     scalar-accumulator form on the edge_12x16_g7 inputs, and an abs-sum
-     with an if inside the loop (Appendix A.2 (i)).
+     scalar-accumulator form on the edge_12x16_g7 inputs, an abs-sum with
+     an if inside the loop (Appendix A.2 (i)), and CAVA's demosaic and
+     3x3-median denoise on the cava_stages_6x8 frame.
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -82,6 +83,89 @@ fn abs_sum<n, m: usize>(x: f32[n, m]) -> f32[n] {
     out[i] = acc;
   }
   return out;
+}
+"""
+
+# CAVA demosaic (bilinear RGGB, border 0) and denoise (3x3 median by
+# insertion sort, border copied), written as oracle/juno_oracle.c's
+# jo_cava_demosaic / jo_cava_denoise restate them
+CAVA_DM_DN = """
+#[entry]
+fn demosaic<r, c: usize>(sc: f32[3, r, c]) -> f32[3, r, c] {
+  let dm : f32[3, r, c];
+  for y in 1..r - 1 {
+    for x in 1..c - 1 {
+      let rr : f32 = 0.0;
+      let gg : f32 = 0.0;
+      let bb : f32 = 0.0;
+      if y % 2 == 0 {
+        if x % 2 == 0 {
+          rr = sc[0, y, x];
+          gg = (((sc[1, y - 1, x] + sc[1, y + 1, x]) + sc[1, y, x - 1]) + sc[1, y, x + 1]) / 4.0;
+          bb = (((sc[2, y - 1, x - 1] + sc[2, y - 1, x + 1]) + sc[2, y + 1, x - 1]) + sc[2, y + 1, x + 1]) / 4.0;
+        } else {
+          rr = (sc[0, y, x - 1] + sc[0, y, x + 1]) / 2.0;
+          gg = sc[1, y, x];
+          bb = (sc[2, y - 1, x] + sc[2, y + 1, x]) / 2.0;
+        }
+      } else {
+        if x % 2 == 0 {
+          rr = (sc[0, y - 1, x] + sc[0, y + 1, x]) / 2.0;
+          gg = sc[1, y, x];
+          bb = (sc[2, y, x - 1] + sc[2, y, x + 1]) / 2.0;
+        } else {
+          rr = (((sc[0, y - 1, x - 1] + sc[0, y - 1, x + 1]) + sc[0, y + 1, x - 1]) + sc[0, y + 1, x + 1]) / 4.0;
+          gg = (((sc[1, y - 1, x] + sc[1, y + 1, x]) + sc[1, y, x - 1]) + sc[1, y, x + 1]) / 4.0;
+          bb = sc[2, y, x];
+        }
+      }
+      dm[0, y, x] = rr;
+      dm[1, y, x] = gg;
+      dm[2, y, x] = bb;
+    }
+  }
+  return dm;
+}
+
+#[entry]
+fn denoise<r, c: usize>(dm: f32[3, r, c]) -> f32[3, r, c] {
+  let dn : f32[3, r, c];
+  for y in 0..r {
+    for x in 0..c {
+      for ch in 0..3 {
+        if y == 0 || x == 0 || y == r - 1 || x == c - 1 {
+          dn[ch, y, x] = dm[ch, y, x];
+        } else {
+          let w : f32[9];
+          for i in 0..3 {
+            for j in 0..3 {
+              w[i * 3 + j] = dm[ch, y + i - 1, x + j - 1];
+            }
+          }
+          for i in 1..9 {
+            let v : f32 = w[i];
+            let k : u64 = i;
+            let moving : bool = true;
+            while moving {
+              if k > 0 {
+                if w[k - 1] > v {
+                  w[k] = w[k - 1];
+                  k = k - 1;
+                } else {
+                  moving = false;
+                }
+              } else {
+                moving = false;
+              }
+            }
+            w[k] = v;
+          }
+          dn[ch, y, x] = w[4];
+        }
+      }
+    }
+  }
+  return dn;
 }
 """
 
@@ -157,9 +241,14 @@ def main():
     x = rng.standard_normal((5, 9)).astype(np.float32)
     rowmax = run_fixed(MAX_ACC, "max_acc", [5, 9], [x])
     absum = run_fixed(ABS_SUM, "abs_sum", [5, 9], [x])
+    cv = np.load(os.path.join(golden, "cava_stages_6x8.npz"))
+    r, c = cv["scaled"].shape[1:]
+    dm = run_fixed(CAVA_DM_DN, "demosaic", [r, c], [cv["scaled"]])
+    dn = run_fixed(CAVA_DM_DN, "denoise", [r, c], [dm])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
-                        x=x, rowmax=rowmax, abs_sum=absum)
+                        x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
+                        cava_denoise=dn)
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

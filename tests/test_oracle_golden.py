@@ -106,3 +106,14 @@ def test_fixed_interpreter_accumulator_programs(oracle):
             acc = np.float32(acc + np.float32(abs(v)))
         sums.append(acc)
     _eq(np.asarray(g["abs_sum"]), np.array(sums, np.float32))
+
+
+def test_fixed_interpreter_cava_demosaic_denoise(oracle):
+    """CAVA's demosaic and 3x3-median denoise as Juno programs (if/else on
+    the Bayer site, insertion-sort median with a while loop), run by the
+    reference interpreter with the Appendix A fix, against the restatement."""
+    from paper_2503_10855_b200 import workloads as W
+    g = golden("fixed_interp")
+    st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
+    _eq(st["demosaic"], g["cava_demosaic"])
+    _eq(st["denoise"], g["cava_denoise"])
