@@ -18,8 +18,9 @@ This script (run in the build container, where /root/reference exists):
      the patch changes nothing where the original works;
   3. writes tests/golden/fixed_interp.npz: the gaussian and the max fold in
      scalar-accumulator form on the edge_12x16_g7 inputs, an abs-sum with
-     an if inside the loop (Appendix A.2 (i)), and CAVA's demosaic and
-     3x3-median denoise on the cava_stages_6x8 frame.
+     an if inside the loop (Appendix A.2 (i)), CAVA's demosaic and
+     3x3-median denoise on the cava_stages_6x8 frame, and SRAD's f64 q0^2
+     statistics on the srad_iter_10x13 image.
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -169,6 +170,27 @@ fn denoise<r, c: usize>(dm: f32[3, r, c]) -> f32[3, r, c] {
 }
 """
 
+# SRAD's q0^2 statistics as oracle/juno_oracle.c:jo_srad_q0sqr restates
+# them: f64 sums in row-major order, rounded once to f32
+SRAD_Q0 = """
+#[entry]
+fn srad_q0<rows, cols: usize>(J: f32[rows, cols]) -> f32 {
+  let sum : f64 = 0.0;
+  let sum2 : f64 = 0.0;
+  for i in 0..rows {
+    for j in 0..cols {
+      let t : f64 = f64(J[i, j]);
+      sum = sum + t;
+      sum2 = sum2 + t * t;
+    }
+  }
+  let nn : f64 = f64(rows * cols);
+  let mean : f64 = sum / nn;
+  let var : f64 = sum2 / nn - mean * mean;
+  return f32(var / (mean * mean));
+}
+"""
+
 
 def _fixed_dependents(self, roots):
     """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
@@ -245,10 +267,12 @@ def main():
     r, c = cv["scaled"].shape[1:]
     dm = run_fixed(CAVA_DM_DN, "demosaic", [r, c], [cv["scaled"]])
     dn = run_fixed(CAVA_DM_DN, "denoise", [r, c], [dm])
+    sr = np.load(os.path.join(golden, "srad_iter_10x13.npz"))
+    q0 = run_fixed(SRAD_Q0, "srad_q0", list(sr["J"].shape), [sr["J"]])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
                         x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
-                        cava_denoise=dn)
+                        cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0))
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

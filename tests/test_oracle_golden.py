@@ -117,3 +117,11 @@ def test_fixed_interpreter_cava_demosaic_denoise(oracle):
     st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
     _eq(st["demosaic"], g["cava_demosaic"])
     _eq(st["denoise"], g["cava_denoise"])
+
+
+def test_fixed_interpreter_srad_q0sqr(oracle):
+    """SRAD's q0^2 (f64 sums, one rounding to f32) as a Juno program on the
+    fixed reference interpreter, against the restatement."""
+    g = golden("fixed_interp")
+    got = np.float32(oracle.srad_q0sqr(g["srad_J"]))
+    assert got.view(np.uint32) == np.float32(g["srad_q0sqr"]).view(np.uint32), (got, g["srad_q0sqr"])
