@@ -19,8 +19,9 @@ This script (run in the build container, where /root/reference exists):
   3. writes tests/golden/fixed_interp.npz: the gaussian and the max fold in
      scalar-accumulator form on the edge_12x16_g7 inputs, an abs-sum with
      an if inside the loop (Appendix A.2 (i)), CAVA's demosaic and
-     3x3-median denoise on the cava_stages_6x8 frame, and SRAD's f64 q0^2
-     statistics on the srad_iter_10x13 image.
+     3x3-median denoise on the cava_stages_6x8 frame, SRAD's f64 q0^2
+     statistics on the srad_iter_10x13 image, and backprop's output and
+     hidden error stages (given the restatement's forward pass).
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -191,6 +192,46 @@ fn srad_q0<rows, cols: usize>(J: f32[rows, cols]) -> f32 {
 }
 """
 
+# backprop's output / hidden error stages (bpnn_output_error,
+# bpnn_hidden_error as oracle/juno_oracle.c:jo_bp_train restates them);
+# their inputs (hidden, output) come from squash, which needs exp
+BP_ERR = """
+#[entry]
+fn output_delta<no: usize>(output: f32[no], target: f32[no]) -> f32[no] {
+  let d : f32[no];
+  for j in 1..no {
+    let o : f32 = output[j];
+    d[j] = (o * (1.0 - o)) * (target[j] - o);
+  }
+  return d;
+}
+
+#[entry]
+fn abs_err<no: usize>(d: f32[no]) -> f32 {
+  let e : f32 = 0.0;
+  for j in 1..no {
+    let v : f32 = d[j];
+    if v < 0.0 { v = -v; }
+    e = e + v;
+  }
+  return e;
+}
+
+#[entry]
+fn hidden_delta<nh, no: usize>(hidden: f32[nh], d_o: f32[no], hw: f32[nh, no]) -> f32[nh] {
+  let d : f32[nh];
+  for j in 1..nh {
+    let h : f32 = hidden[j];
+    let s : f32 = 0.0;
+    for k in 1..no {
+      s = s + d_o[k] * hw[j, k];
+    }
+    d[j] = (h * (1.0 - h)) * s;
+  }
+  return d;
+}
+"""
+
 
 def _fixed_dependents(self, roots):
     """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
@@ -269,10 +310,23 @@ def main():
     dn = run_fixed(CAVA_DM_DN, "denoise", [r, c], [dm])
     sr = np.load(os.path.join(golden, "srad_iter_10x13.npz"))
     q0 = run_fixed(SRAD_Q0, "srad_q0", list(sr["J"].shape), [sr["J"]])
+    # backprop errors: hidden/output from the restatement's forward pass
+    # (squash needs exp), the error stages from the interpreter
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle as OR
+    from paper_2503_10855_b200.workloads import bp_inputs
+    bx, biw, bhw, bt, bipw, bhpw = bp_inputs(40, 6, 3, seed=5)
+    fw = OR.bp_train(bx, biw, bhw, bt, bipw, bhpw)
+    d_o = run_fixed(BP_ERR, "output_delta", [4], [fw["output"], bt])
+    e_o = run_fixed(BP_ERR, "abs_err", [4], [d_o])
+    d_h = run_fixed(BP_ERR, "hidden_delta", [7, 4], [fw["hidden"], d_o, bhw])
+    e_h = run_fixed(BP_ERR, "abs_err", [7], [d_h])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
                         x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
-                        cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0))
+                        cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0),
+                        bp_x=bx, bp_iw=biw, bp_hw=bhw, bp_t=bt, bp_ipw=bipw, bp_hpw=bhpw,
+                        bp_delta_o=d_o, bp_delta_h=d_h, bp_out_err=np.float32(e_o), bp_hid_err=np.float32(e_h))
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

@@ -125,3 +125,15 @@ def test_fixed_interpreter_srad_q0sqr(oracle):
     g = golden("fixed_interp")
     got = np.float32(oracle.srad_q0sqr(g["srad_J"]))
     assert got.view(np.uint32) == np.float32(g["srad_q0sqr"]).view(np.uint32), (got, g["srad_q0sqr"])
+
+
+def test_fixed_interpreter_backprop_errors(oracle):
+    """bpnn_output_error / bpnn_hidden_error as Juno programs on the fixed
+    reference interpreter (fed the restatement's forward pass: squash needs
+    exp), against the restatement's deltas and error sums."""
+    g = golden("fixed_interp")
+    fw = oracle.bp_train(g["bp_x"], g["bp_iw"], g["bp_hw"], g["bp_t"], g["bp_ipw"], g["bp_hpw"])
+    _eq(fw["delta_o"][1:], g["bp_delta_o"][1:])
+    _eq(fw["delta_h"][1:], g["bp_delta_h"][1:])
+    _eq(np.float32(fw["out_err"]), np.float32(g["bp_out_err"]))
+    _eq(np.float32(fw["hid_err"]), np.float32(g["bp_hid_err"]))
