@@ -20,8 +20,9 @@ This script (run in the build container, where /root/reference exists):
      scalar-accumulator form on the edge_12x16_g7 inputs, an abs-sum with
      an if inside the loop (Appendix A.2 (i)), CAVA's demosaic and
      3x3-median denoise on the cava_stages_6x8 frame, SRAD's f64 q0^2
-     statistics on the srad_iter_10x13 image, and backprop's output and
-     hidden error stages (given the restatement's forward pass).
+     statistics on the srad_iter_10x13 image, backprop's output and hidden
+     error stages (given the restatement's forward pass), and CAVA's tone
+     map + descale (given the restatement's gamut stage, which needs sqrt).
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -232,6 +233,30 @@ fn hidden_delta<nh, no: usize>(hidden: f32[nh], d_o: f32[no], hw: f32[nh, no]) -
 }
 """
 
+# CAVA's tone map + descale (jo_cava_tonemap_descale): clamp with the
+# reference's Python-builtin max/min order, truncating casts
+CAVA_TM = """
+#[entry]
+fn tonemap_descale<r, c: usize>(gm: f32[3, r, c], tmap: f32[256, 3]) -> u8[3, r, c] {
+  let out : u8[3, r, c];
+  for ch in 0..3 {
+    for y in 0..r {
+      for x in 0..c {
+        let t : f32 = gm[ch, y, x] * 255.0;
+        if 0.0 > t { t = 0.0; }
+        if t > 255.0 { t = 255.0; }
+        let idx : u64 = u64(t);
+        let v : f32 = tmap[idx, ch] * 255.0;
+        if 0.0 > v { v = 0.0; }
+        if v > 255.0 { v = 255.0; }
+        out[ch, y, x] = u8(v);
+      }
+    }
+  }
+  return out;
+}
+"""
+
 
 def _fixed_dependents(self, roots):
     """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
@@ -321,12 +346,16 @@ def main():
     e_o = run_fixed(BP_ERR, "abs_err", [4], [d_o])
     d_h = run_fixed(BP_ERR, "hidden_delta", [7, 4], [fw["hidden"], d_o, bhw])
     e_h = run_fixed(BP_ERR, "abs_err", [7], [d_h])
+    from paper_2503_10855_b200.workloads import cava_params
+    cst = OR.cava_frame(cv["raw"], *cava_params(16), stages=True)
+    tm_out = run_fixed(CAVA_TM, "tonemap_descale", [r, c], [cst["gamut"], cava_params(16)[4]])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
                         x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
                         cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0),
                         bp_x=bx, bp_iw=biw, bp_hw=bhw, bp_t=bt, bp_ipw=bipw, bp_hpw=bhpw,
-                        bp_delta_o=d_o, bp_delta_h=d_h, bp_out_err=np.float32(e_o), bp_hid_err=np.float32(e_h))
+                        bp_delta_o=d_o, bp_delta_h=d_h, bp_out_err=np.float32(e_o), bp_hid_err=np.float32(e_h),
+                        cava_gamut=cst["gamut"], cava_out=tm_out)
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

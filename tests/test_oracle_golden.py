@@ -137,3 +137,13 @@ def test_fixed_interpreter_backprop_errors(oracle):
     _eq(fw["delta_h"][1:], g["bp_delta_h"][1:])
     _eq(np.float32(fw["out_err"]), np.float32(g["bp_out_err"]))
     _eq(np.float32(fw["hid_err"]), np.float32(g["bp_hid_err"]))
+
+
+def test_fixed_interpreter_cava_tonemap_descale(oracle):
+    """CAVA's tone map + descale as a Juno program on the fixed reference
+    interpreter (fed the restatement's gamut stage: it needs sqrt)."""
+    from paper_2503_10855_b200 import workloads as W
+    g = golden("fixed_interp")
+    st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
+    _eq(st["gamut"], g["cava_gamut"])
+    _eq(st["out"], g["cava_out"])
