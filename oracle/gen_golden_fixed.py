@@ -21,8 +21,9 @@ This script (run in the build container, where /root/reference exists):
      an if inside the loop (Appendix A.2 (i)), CAVA's demosaic and
      3x3-median denoise on the cava_stages_6x8 frame, SRAD's f64 q0^2
      statistics on the srad_iter_10x13 image, backprop's output and hidden
-     error stages (given the restatement's forward pass), and CAVA's tone
-     map + descale (given the restatement's gamut stage, which needs sqrt).
+     error stages (given the restatement's forward pass), CAVA's tone map +
+     descale (given the restatement's gamut stage), and the gamut stage
+     itself around its sqrt (radicands and sums in Juno, IEEE sqrt between).
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -257,6 +258,46 @@ fn tonemap_descale<r, c: usize>(gm: f32[3, r, c], tmap: f32[256, 3]) -> u8[3, r,
 }
 """
 
+# CAVA's gamut map around its one sqrt: the radicands (Juno), their IEEE
+# sqrt (numpy: correctly rounded, like sqrtf), then the RBF + affine sums
+# (Juno), as jo_cava_gamut orders them
+CAVA_GAMUT = """
+#[entry]
+fn gamut_radicands<np, r, c: usize>(tr: f32[3, r, c], ctrl: f32[np, 3]) -> f32[np, r, c] {
+  let rad : f32[np, r, c];
+  for y in 0..r {
+    for x in 0..c {
+      for p in 0..np {
+        let d0 : f32 = tr[0, y, x] - ctrl[p, 0];
+        let d1 : f32 = tr[1, y, x] - ctrl[p, 1];
+        let d2 : f32 = tr[2, y, x] - ctrl[p, 2];
+        rad[p, y, x] = (d0 * d0 + d1 * d1) + d2 * d2;
+      }
+    }
+  }
+  return rad;
+}
+
+#[entry]
+fn gamut_sums<np, r, c: usize>(tr: f32[3, r, c], dist: f32[np, r, c], wts: f32[np, 3],
+                               coefs: f32[4, 3]) -> f32[3, r, c] {
+  let gm : f32[3, r, c];
+  for y in 0..r {
+    for x in 0..c {
+      for ch in 0..3 {
+        let g : f32 = 0.0;
+        for p in 0..np {
+          g = g + dist[p, y, x] * wts[p, ch];
+        }
+        let aff : f32 = ((coefs[0, ch] + coefs[1, ch] * tr[0, y, x]) + coefs[2, ch] * tr[1, y, x]) + coefs[3, ch] * tr[2, y, x];
+        gm[ch, y, x] = g + aff;
+      }
+    }
+  }
+  return gm;
+}
+"""
+
 
 def _fixed_dependents(self, roots):
     """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
@@ -349,13 +390,18 @@ def main():
     from paper_2503_10855_b200.workloads import cava_params
     cst = OR.cava_frame(cv["raw"], *cava_params(16), stages=True)
     tm_out = run_fixed(CAVA_TM, "tonemap_descale", [r, c], [cst["gamut"], cava_params(16)[4]])
+    tstw, ctrl, wts, coefs, _ = cava_params(16)
+    tr = G.run(G.CAVA_SCALE, "transform", [r, c], [cst["denoise"], tstw])
+    rad = run_fixed(CAVA_GAMUT, "gamut_radicands", [ctrl.shape[0], r, c], [tr, ctrl])
+    dist = np.sqrt(rad).astype(np.float32)
+    gm = run_fixed(CAVA_GAMUT, "gamut_sums", [ctrl.shape[0], r, c], [tr, dist, wts, coefs])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
                         x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
                         cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0),
                         bp_x=bx, bp_iw=biw, bp_hw=bhw, bp_t=bt, bp_ipw=bipw, bp_hpw=bhpw,
                         bp_delta_o=d_o, bp_delta_h=d_h, bp_out_err=np.float32(e_o), bp_hid_err=np.float32(e_h),
-                        cava_gamut=cst["gamut"], cava_out=tm_out)
+                        cava_gamut=cst["gamut"], cava_out=tm_out, cava_gamut_juno=gm)
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

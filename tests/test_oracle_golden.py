@@ -147,3 +147,14 @@ def test_fixed_interpreter_cava_tonemap_descale(oracle):
     st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
     _eq(st["gamut"], g["cava_gamut"])
     _eq(st["out"], g["cava_out"])
+
+
+def test_fixed_interpreter_cava_gamut_around_sqrt(oracle):
+    """CAVA's gamut map: radicands and the RBF + affine sums as Juno programs
+    on the fixed reference interpreter, IEEE sqrt between them (numpy's f32
+    sqrt is correctly rounded, like sqrtf): bit-identical to the
+    restatement's gamut stage."""
+    from paper_2503_10855_b200 import workloads as W
+    g = golden("fixed_interp")
+    st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
+    _eq(st["gamut"], g["cava_gamut_juno"])
