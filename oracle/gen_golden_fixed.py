@@ -22,8 +22,9 @@ This script (run in the build container, where /root/reference exists):
      3x3-median denoise on the cava_stages_6x8 frame, SRAD's f64 q0^2
      statistics on the srad_iter_10x13 image, backprop's output and hidden
      error stages (given the restatement's forward pass), CAVA's tone map +
-     descale (given the restatement's gamut stage), and the gamut stage
-     itself around its sqrt (radicands and sums in Juno, IEEE sqrt between).
+     descale (given the restatement's gamut stage), the gamut stage itself
+     around its sqrt (radicands and sums in Juno, IEEE sqrt between), and the
+     same for CFD/Euler's step factor and flux.
 
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_fixed.py
 """
@@ -298,6 +299,177 @@ fn gamut_sums<np, r, c: usize>(tr: f32[3, r, c], dist: f32[np, r, c], wts: f32[n
 }
 """
 
+# CFD/Euler step factor and flux around their square roots: primitives and
+# radicands in Juno, IEEE sqrt (numpy) between, then the flux sums in Juno,
+# in jo_euler_step_factor / jo_euler_flux's operation order.  (GAMMA - 1 is
+# written 1.4 - 1.0: the f32 difference, as the restatement computes it.)
+EULER = """
+#[entry]
+fn euler_radicands<nelr: usize>(vars: f32[5, nelr], normals: f32[4, 3, nelr]) -> f32[6, nelr] {
+  let out : f32[6, nelr];
+  for i in 0..nelr {
+    let rho : f32 = vars[0, i];
+    let vx : f32 = vars[1, i] / rho;
+    let vy : f32 = vars[2, i] / rho;
+    let vz : f32 = vars[3, i] / rho;
+    let ssq : f32 = (vx * vx + vy * vy) + vz * vz;
+    let p : f32 = (1.4 - 1.0) * (vars[4, i] - (0.5 * rho) * ssq);
+    out[0, i] = ssq;
+    out[1, i] = (1.4 * p) / rho;
+    for j in 0..4 {
+      out[2 + j, i] = (normals[j, 0, i] * normals[j, 0, i] + normals[j, 1, i] * normals[j, 1, i]) + normals[j, 2, i] * normals[j, 2, i];
+    }
+  }
+  return out;
+}
+
+#[entry]
+fn euler_step_factor_c<nelr: usize>(sqrt_area: f32[nelr], sqrts: f32[6, nelr]) -> f32[nelr] {
+  let sf : f32[nelr];
+  for i in 0..nelr {
+    sf[i] = 0.5 / (sqrt_area[i] * (sqrts[0, i] + sqrts[1, i]));
+  }
+  return sf;
+}
+
+#[entry]
+fn euler_flux_c<nelr: usize>(nbrs: i32[4, nelr], normals: f32[4, 3, nelr], ff: f32[5], vars: f32[5, nelr],
+                             sqrts: f32[6, nelr]) -> f32[5, nelr] {
+  let out : f32[5, nelr];
+  let fvx : f32 = ff[1] / ff[0];
+  let fvy : f32 = ff[2] / ff[0];
+  let fvz : f32 = ff[3] / ff[0];
+  let fp : f32 = (1.4 - 1.0) * (ff[4] - (0.5 * ff[0]) * ((fvx * fvx + fvy * fvy) + fvz * fvz));
+  let ffxx : f32 = fvx * ff[1] + fp;
+  let ffxy : f32 = fvx * ff[2];
+  let ffxz : f32 = fvx * ff[3];
+  let ffyy : f32 = fvy * ff[2] + fp;
+  let ffyz : f32 = fvy * ff[3];
+  let ffzz : f32 = fvz * ff[3] + fp;
+  let fdep : f32 = ff[4] + fp;
+  let ffex : f32 = fvx * fdep;
+  let ffey : f32 = fvy * fdep;
+  let ffez : f32 = fvz * fdep;
+  for i in 0..nelr {
+    let rho_i : f32 = vars[0, i];
+    let mx_i : f32 = vars[1, i];
+    let my_i : f32 = vars[2, i];
+    let mz_i : f32 = vars[3, i];
+    let rhoE_i : f32 = vars[4, i];
+    let vx_i : f32 = mx_i / rho_i;
+    let vy_i : f32 = my_i / rho_i;
+    let vz_i : f32 = mz_i / rho_i;
+    let ssq_i : f32 = (vx_i * vx_i + vy_i * vy_i) + vz_i * vz_i;
+    let p_i : f32 = (1.4 - 1.0) * (rhoE_i - (0.5 * rho_i) * ssq_i);
+    let sp_i : f32 = sqrts[0, i];
+    let a_i : f32 = sqrts[1, i];
+    let fxx_i : f32 = vx_i * mx_i + p_i;
+    let fxy_i : f32 = vx_i * my_i;
+    let fxz_i : f32 = vx_i * mz_i;
+    let fyy_i : f32 = vy_i * my_i + p_i;
+    let fyz_i : f32 = vy_i * mz_i;
+    let fzz_i : f32 = vz_i * mz_i + p_i;
+    let dep_i : f32 = rhoE_i + p_i;
+    let fex_i : f32 = vx_i * dep_i;
+    let fey_i : f32 = vy_i * dep_i;
+    let fez_i : f32 = vz_i * dep_i;
+    let f_rho : f32 = 0.0;
+    let f_rhoE : f32 = 0.0;
+    let f_mx : f32 = 0.0;
+    let f_my : f32 = 0.0;
+    let f_mz : f32 = 0.0;
+    for j in 0..4 {
+      let nb : i32 = nbrs[j, i];
+      let nx : f32 = normals[j, 0, i];
+      let ny : f32 = normals[j, 1, i];
+      let nz : f32 = normals[j, 2, i];
+      let nlen : f32 = sqrts[2 + j, i];
+      if nb >= 0 {
+        let k : u64 = u64(nb);
+        let rho_n : f32 = vars[0, k];
+        let mx_n : f32 = vars[1, k];
+        let my_n : f32 = vars[2, k];
+        let mz_n : f32 = vars[3, k];
+        let rhoE_n : f32 = vars[4, k];
+        let vx_n : f32 = mx_n / rho_n;
+        let vy_n : f32 = my_n / rho_n;
+        let vz_n : f32 = mz_n / rho_n;
+        let ssq_n : f32 = (vx_n * vx_n + vy_n * vy_n) + vz_n * vz_n;
+        let p_n : f32 = (1.4 - 1.0) * (rhoE_n - (0.5 * rho_n) * ssq_n);
+        let a_n : f32 = sqrts[1, k];
+        let fxx_n : f32 = vx_n * mx_n + p_n;
+        let fxy_n : f32 = vx_n * my_n;
+        let fxz_n : f32 = vx_n * mz_n;
+        let fyy_n : f32 = vy_n * my_n + p_n;
+        let fyz_n : f32 = vy_n * mz_n;
+        let fzz_n : f32 = vz_n * mz_n + p_n;
+        let dep_n : f32 = rhoE_n + p_n;
+        let fex_n : f32 = vx_n * dep_n;
+        let fey_n : f32 = vy_n * dep_n;
+        let fez_n : f32 = vz_n * dep_n;
+        let factor : f32 = (((-nlen) * 0.2) * 0.5) * (((sp_i + sqrts[0, k]) + a_i) + a_n);
+        f_rho = f_rho + factor * (rho_i - rho_n);
+        f_rhoE = f_rhoE + factor * (rhoE_i - rhoE_n);
+        f_mx = f_mx + factor * (mx_i - mx_n);
+        f_my = f_my + factor * (my_i - my_n);
+        f_mz = f_mz + factor * (mz_i - mz_n);
+        factor = 0.5 * nx;
+        f_rho = f_rho + factor * (mx_n + mx_i);
+        f_rhoE = f_rhoE + factor * (fex_n + fex_i);
+        f_mx = f_mx + factor * (fxx_n + fxx_i);
+        f_my = f_my + factor * (fxy_n + fxy_i);
+        f_mz = f_mz + factor * (fxz_n + fxz_i);
+        factor = 0.5 * ny;
+        f_rho = f_rho + factor * (my_n + my_i);
+        f_rhoE = f_rhoE + factor * (fey_n + fey_i);
+        f_mx = f_mx + factor * (fxy_n + fxy_i);
+        f_my = f_my + factor * (fyy_n + fyy_i);
+        f_mz = f_mz + factor * (fyz_n + fyz_i);
+        factor = 0.5 * nz;
+        f_rho = f_rho + factor * (mz_n + mz_i);
+        f_rhoE = f_rhoE + factor * (fez_n + fez_i);
+        f_mx = f_mx + factor * (fxz_n + fxz_i);
+        f_my = f_my + factor * (fyz_n + fyz_i);
+        f_mz = f_mz + factor * (fzz_n + fzz_i);
+      } else {
+        if nb + 1 == 0 {
+          f_mx = f_mx + nx * p_i;
+          f_my = f_my + ny * p_i;
+          f_mz = f_mz + nz * p_i;
+        } else {
+          if nb + 2 == 0 {
+            let factor : f32 = 0.5 * nx;
+            f_rho = f_rho + factor * (ff[1] + mx_i);
+            f_rhoE = f_rhoE + factor * (ffex + fex_i);
+            f_mx = f_mx + factor * (ffxx + fxx_i);
+            f_my = f_my + factor * (ffxy + fxy_i);
+            f_mz = f_mz + factor * (ffxz + fxz_i);
+            factor = 0.5 * ny;
+            f_rho = f_rho + factor * (ff[2] + my_i);
+            f_rhoE = f_rhoE + factor * (ffey + fey_i);
+            f_mx = f_mx + factor * (ffxy + fxy_i);
+            f_my = f_my + factor * (ffyy + fyy_i);
+            f_mz = f_mz + factor * (ffyz + fyz_i);
+            factor = 0.5 * nz;
+            f_rho = f_rho + factor * (ff[3] + mz_i);
+            f_rhoE = f_rhoE + factor * (ffez + fez_i);
+            f_mx = f_mx + factor * (ffxz + fxz_i);
+            f_my = f_my + factor * (ffyz + fyz_i);
+            f_mz = f_mz + factor * (ffzz + fzz_i);
+          }
+        }
+      }
+    }
+    out[0, i] = f_rho;
+    out[1, i] = f_mx;
+    out[2, i] = f_my;
+    out[3, i] = f_mz;
+    out[4, i] = f_rhoE;
+  }
+  return out;
+}
+"""
+
 
 def _fixed_dependents(self, roots):
     """oracle.py:55-70 with the Appendix A fix: do not walk into (or through)
@@ -395,13 +567,23 @@ def main():
     rad = run_fixed(CAVA_GAMUT, "gamut_radicands", [ctrl.shape[0], r, c], [tr, ctrl])
     dist = np.sqrt(rad).astype(np.float32)
     gm = run_fixed(CAVA_GAMUT, "gamut_sums", [ctrl.shape[0], r, c], [tr, dist, wts, coefs])
+    # CFD: a small structured mesh with walls and far-field faces
+    from paper_2503_10855_b200.workloads import euler_mesh, euler_ff_variable
+    areas, nbr, nrm, ffv, ev = euler_mesh(6, 5, seed=3)
+    ne = areas.shape[0]
+    rad = run_fixed(EULER, "euler_radicands", [ne], [ev, nrm])
+    sq = np.sqrt(rad).astype(np.float32)
+    sfc = run_fixed(EULER, "euler_step_factor_c", [ne], [np.sqrt(areas).astype(np.float32), sq])
+    flc = run_fixed(EULER, "euler_flux_c", [ne], [nbr, nrm, ffv, ev, sq])
     out = os.path.join(golden, "fixed_interp.npz")
     np.savez_compressed(out, edge_input=e["input"], gaussian=e["gaussian"], gaussian_acc=acc,
                         x=x, rowmax=rowmax, abs_sum=absum, cava_raw=cv["raw"], cava_demosaic=dm,
                         cava_denoise=dn, srad_J=sr["J"], srad_q0sqr=np.float32(q0),
                         bp_x=bx, bp_iw=biw, bp_hw=bhw, bp_t=bt, bp_ipw=bipw, bp_hpw=bhpw,
                         bp_delta_o=d_o, bp_delta_h=d_h, bp_out_err=np.float32(e_o), bp_hid_err=np.float32(e_h),
-                        cava_gamut=cst["gamut"], cava_out=tm_out, cava_gamut_juno=gm)
+                        cava_gamut=cst["gamut"], cava_out=tm_out, cava_gamut_juno=gm,
+                        eu_areas=areas, eu_nbrs=nbr, eu_normals=nrm, eu_ff=ffv, eu_vars=ev,
+                        eu_step_factor=sfc, eu_flux=flc)
     print(f"wrote {out}; gaussian_acc == committed smoothed: "
           f"{np.array_equal(acc.view(np.uint32), e['smoothed'].view(np.uint32))}")
 

@@ -158,3 +158,13 @@ def test_fixed_interpreter_cava_gamut_around_sqrt(oracle):
     g = golden("fixed_interp")
     st = oracle.cava_frame(g["cava_raw"], *W.cava_params(16), stages=True)
     _eq(st["gamut"], g["cava_gamut_juno"])
+
+
+def test_fixed_interpreter_euler_around_sqrt(oracle):
+    """CFD/Euler step factor and flux (walls, far field, interior faces) as
+    Juno programs on the fixed reference interpreter, with IEEE sqrt between
+    the radicand and sum programs: bit-identical to the restatement."""
+    g = golden("fixed_interp")
+    _eq(oracle.euler_step_factor(g["eu_vars"], g["eu_areas"]), g["eu_step_factor"])
+    _eq(oracle.euler_flux(g["eu_nbrs"], g["eu_normals"], g["eu_ff"], g["eu_vars"]), g["eu_flux"])
+    assert (g["eu_nbrs"] == -1).any() and (g["eu_nbrs"] == -2).any()  # both boundary kinds covered
