@@ -12,8 +12,14 @@ interpreter ``oracle_execute`` (runtime/oracle.py:28-32) through
 tests/golden/*.npz (made by oracle/gen_golden.py); the gaussian, laplacian,
 reject, max-gradient, SRAD-coefficient, CAVA scale/transform and BP
 adjust-weights stages are pinned the same way with oracle-friendly Juno
-fixtures.  sqrt/exp/log stages are inexpressible in the reference frontend
- and are "parity unpinned" beyond IEEE sqrt.
+fixtures.  oracle/gen_golden_fixed.py runs the same interpreter with its
+Appendix A dependents defect fixed and pins the accumulator-form programs
+and the stages around sqrt (CAVA demosaic, median, gamut, tone map; CFD step
+factor and flux; SRAD q0 statistics; BP error stages): radicands and sums
+are Juno programs, the IEEE sqrt between them numpy's.  What stays unpinned
+is the transcendental itself (sqrt/exp/log: IEEE or f64-rounded on both
+sides) and the f64 exp/log of SRAD's extract/compress and
+BP's squash.
 """
 
 from __future__ import annotations
