@@ -149,3 +149,12 @@ def test_backprop_adjust_pinned(oracle):
     g = golden("bp_33x5")
     w, _ = oracle.bp_adjust_weights(g["delta"], g["ly"], g["w"], g["oldw"])
     _exact(w[:, 1:], g["adjusted"][:, 1:])
+
+
+def test_euler_stages_match_fixed_interpreter(jb):
+    """The GPU step-factor and flux kernels against skiff's interpreter
+    (Appendix A defect fixed, oracle/gen_golden_fixed.py) running the Juno
+    step factor and flux around their square roots."""
+    g = golden("fixed_interp")
+    _exact(jb.euler_step_factor(g["eu_vars"], g["eu_areas"]), g["eu_step_factor"])
+    _exact(jb.euler_flux(g["eu_nbrs"], g["eu_normals"], g["eu_ff"], g["eu_vars"]), g["eu_flux"])
