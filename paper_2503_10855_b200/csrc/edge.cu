@@ -550,20 +550,24 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
 // assumption, no deadlock.
 //
 // Memory ordering.  The packed lines leave by bulk tensor store; a tile is
-// counted (red.relaxed on done[f]) only after cp.async.bulk.wait_group (not
-// .read) reports the store complete, i.e. its writes performed in global
-// memory, and after a fence.proxy.async.global.  Readers observe ready[f]
-// with a relaxed load and then read the lines with ld.global.cg, which
-// bypasses L1 and is served by the line's home L2 slice -- the one point of
-// coherence for every SM (cross-die accesses go to the home slice: 262 vs
-// 234 cycles, B300_MICROARCH.md "L2 cache"; there is no far-side copy).  So
-// no MEMBAR-class fence sits on the per-tile path: the two gpu-scope
-// acq_rel fences the PTX model would ask for (writer release before the
-// count, reader acquire after the flag) cost 3.4% of the kernel
-// (tools/ab_edge.sh: 63.5 k vs 65.7 k frames/s) and are compiled in with
-// -DEDGE_STRICT_FENCES.  The publisher of a frame's threshold does run an
-// acquire fence (once per frame), and the L2 discards are fenced before
-// their unit is counted (their lines are rewritten by the next frame).
+// counted (red.relaxed on done[f]) after cp.async.bulk.wait_group (not
+// .read) reports the store complete and after fence.proxy.async.global plus
+// a gpu-scope acq_rel fence (the release the PTX model asks for).  Readers
+// observe ready[f] with a relaxed load followed by an acquire fence (once
+// per frame and CTA) before reading the lines with ld.global.cg.  The
+// publisher of a frame's threshold runs an acquire fence, and the L2
+// discards are fenced before their unit is counted (their lines are
+// rewritten by a later frame).
+//
+// -DEDGE_RELAXED_ORDERING drops the writer and reader fences: the store is
+// complete at its home L2 slice before the count is sent and ld.cg reads
+// that slice (cross-die accesses go to the home slice, 262 vs 234 cycles,
+// B300_MICROARCH.md "L2 cache"), so it is safe on this hardware but outside
+// the PTX model; it measures 4.3% faster (tools/ab_edge.sh: 68.1 k vs 65.3 k
+// frames/s).
+#ifndef EDGE_RELAXED_ORDERING
+#define EDGE_STRICT_FENCES 1
+#endif
 //
 // All scheduling is done by thread 0 with as few L2 round trips as possible
 // (each one stalls the CTA at its next barrier): releases are one-thread
