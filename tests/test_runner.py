@@ -70,3 +70,15 @@ def test_runner_validates_like_execute(jb):
         r.run(8, 5, 2, a, b)
     with pytest.raises(DynConstError):
         r.run(8, 4)
+
+
+@pytest.mark.gpu
+def test_edge_runner_batch_matches_api(jb):
+    g, st, sx, sy, th = W.edge_filters()
+    x = np.stack([W.edge_frame(135, 240, seed=s) for s in range(3)])
+    r = Runner("edge_detection")
+    got = r.run(135, 240, 7, 3, 3, x, g, st, sx, sy, th)
+    np.testing.assert_array_equal(got, jb.edge_detection(x, g, st, sx, sy, th))
+    allocs = r.stats.allocations
+    r.run(135, 240, 7, 3, 3, x, g, st, sx, sy, th)
+    assert r.stats.allocations == allocs
