@@ -429,7 +429,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     }
     cudaGetLastError();  // a failed capture falls back to plain launches
   }
-  if (repeat && gc.exec) {
+  if (repeat && gc.exec && cap == cudaStreamCaptureStatusNone) {  // (a caller's capture records plain launches)
     void *tok = prof_begin("matmul_tcgen05", s);
     JB_CHECK_CUDA(cudaGraphLaunch(gc.exec, s));
     prof_end(tok, s);
