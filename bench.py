@@ -231,27 +231,29 @@ class EdgeWorkload:
             raise RuntimeError(_lib.last_error())
 
     def step_e2e(self):
-        """Public API on pinned host buffers: H2D, edge_detection, D2H."""
+        """The public entry on numpy host arrays: api.execute copies the batch
+        in, runs the kernel and returns a fresh numpy result every step."""
         if not self.local:
             return
         from paper_2503_10855_b200 import api
-        api.edge_detection_pipelined(self.pin_in, *self.filters[:4], self.theta, out=self.pin_out)
+        self.e2e_out = api.execute("edge_detection", [self.n, self.m, 7, 3, 3],
+                                   [self.frames_host, *self.filters[:4], self.theta])
 
     def e2e_bytes(self):
         return self.local * self.frame_bytes, self.local * self.frame_bytes
 
-    e2e_api = "paper_2503_10855_b200.api.edge_detection_pipelined (pinned host in/out)"
+    e2e_api = ("paper_2503_10855_b200.api.execute('edge_detection', ...) on numpy in/out "
+               "(input page-locked in place on first use, chunks of 16 frames overlap H2D/kernel/D2H)")
 
-    def cpu_sample(self, oracle):
-        """Oracle restatement on `k` frames with all host threads."""
-        k = 2
+    def ref_step(self, oracle, sample=False):
+        """The step on the host: the oracle restatement over the whole batch
+        (threads split the frames), or a 32-frame sample of it."""
+        k = min(32, self.batch) if sample else self.batch
         g, st, sx, sy, th = self.filters
         x = self.frames_host[:k] if self.local >= k else \
             __import__("paper_2503_10855_b200.workloads", fromlist=["x"]).edge_batch(k, self.n, self.m)
-        t = time.perf_counter()
         oracle.edge(x, g, st, sx, sy, th)
-        dt = time.perf_counter() - t
-        return k / dt, f"{k} frames {self.n}x{self.m} through oracle/juno_oracle.c (OpenMP)"
+        return k, f"{k} frames {self.n}x{self.m} through oracle/juno_oracle.c (OpenMP over frames)"
 
     def check(self, oracle):
         """Bit-exact spot check of one output frame against the oracle."""
@@ -310,22 +312,17 @@ class MatmulWorkload:
             raise RuntimeError(_lib.last_error())
 
     def step_e2e(self):
-        self.da.copy_(self.pa, non_blocking=True)
-        self.db.copy_(self.pb, non_blocking=True)
-        self.step_device()
-        self.pc.copy_(self.dc, non_blocking=True)
-        self.stream.synchronize()
+        from paper_2503_10855_b200 import api
+        self.e2e_out = api.execute("matmul", [self.n, self.m, self.l], [self.a, self.b])
+
+    e2e_api = "paper_2503_10855_b200.api.execute('matmul', ...) on numpy in/out"
 
     def e2e_bytes(self):
         return 8 * self.n * self.m, 4 * self.n * self.l
 
-    def cpu_sample(self, oracle):
-        n = 256
-        t = time.perf_counter()
-        oracle.matmul(self.a[:n], self.b)
-        dt = time.perf_counter() - t
-        # scale the 256-row slab to the full 1024-row call
-        return dt * (self.n / n) * 1e3, f"256x1024x1024 slab of the call (x4), oracle/juno_oracle.c"
+    def ref_step(self, oracle, sample=False):
+        oracle.matmul(self.a, self.b)
+        return 1, "the full 1024x1024x1024 call, oracle/juno_oracle.c (OpenMP over rows)"
 
     def check(self, oracle):
         ref = oracle.matmul(self.a, self.b)
@@ -359,12 +356,24 @@ class _DeviceCall:
             raise RuntimeError(_lib.last_error())
 
     def step_e2e(self):
+        if getattr(self, "world", 1) == 1 and hasattr(self, "execute_args"):
+            # the public entry on numpy host arrays (fresh numpy results)
+            from paper_2503_10855_b200 import api
+            entry, dcs, args = self.execute_args()
+            self.e2e_out = api.execute(entry, dcs, args)
+            return
         for k in self.inputs_e2e:
             self.dev[k].copy_(self.pin[k], non_blocking=True)
         self.step_device()
         for k, t in self.outputs_e2e():
             self.pin_out[k].copy_(t, non_blocking=True)
         self.stream.synchronize()
+
+    @property
+    def e2e_api(self):
+        if getattr(self, "world", 1) == 1 and hasattr(self, "execute_args"):
+            return f"paper_2503_10855_b200.api.execute('{self.execute_args()[0]}', ...) on numpy in/out"
+        return "pinned host buffers around the sharded step"
 
     def e2e_bytes(self):
         h2d = sum(self.host[k].nbytes for k in self.inputs_e2e)
@@ -444,13 +453,12 @@ class SradWorkload(_DeviceCall):
     def value_from(self, ms_per_step):
         return ms_per_step / self.niter
 
-    def cpu_sample(self, oracle):
-        crop = self.host["image"][:2048, :2048]
-        t = time.perf_counter()
-        oracle.srad(crop, 2, 0.5)
-        dt = time.perf_counter() - t
-        scale = (self.rows * self.cols) / crop.size
-        return dt / 2 * scale * 1e3, "2048x2048 crop, 2 iterations, scaled to ms/iteration at full size"
+    def execute_args(self):
+        return "srad", [self.rows, self.cols], [self.niter, 0.5, self.host["image"]]
+
+    def ref_step(self, oracle, sample=False):
+        oracle.srad(self.host["image"], 1, 0.5)
+        return 1, f"1 iteration (with extract + compress) of the full {self.rows}x{self.cols} image"
 
     def check(self, oracle):
         crop = np.ascontiguousarray(self.host["image"][:512, :512])
@@ -545,11 +553,14 @@ class EulerWorkload(_DeviceCall):
     def value_from(self, ms_per_step):
         return ms_per_step / self.iters
 
-    def cpu_sample(self, oracle):
+    def execute_args(self):
         h = self.host
-        t = time.perf_counter()
+        return "euler", [self.nelr], [self.iters, h["areas"], h["nb"], h["normals"], h["ff"], h["v"]]
+
+    def ref_step(self, oracle, sample=False):
+        h = self.host
         oracle.euler(h["areas"], h["nb"], h["normals"], h["ff"], h["v"], 1)
-        return (time.perf_counter() - t) * 1e3, "1 iteration at full size, oracle/juno_oracle.c (OpenMP)"
+        return 1, "1 iteration (3 RK stages) of the full mesh, oracle/juno_oracle.c (OpenMP)"
 
     def check(self, oracle):
         from paper_2503_10855_b200 import workloads as W
@@ -575,6 +586,10 @@ class BfsWorkload(_DeviceCall):
         self.host = {"s": s, "d": d, "e": e}
         self.inputs_e2e = ["s", "d", "e"]
 
+    def execute_args(self):
+        h = self.host
+        return "bfs", [self.n, self.m], [h["s"], h["d"], h["e"], 0]
+
     def alloc_outputs(self, torch):
         self.cost = torch.empty(self.n, dtype=torch.int32, device="cuda")
         self.pin_out = {"cost": torch.empty(self.n, dtype=torch.int32).pin_memory()}
@@ -599,11 +614,10 @@ class BfsWorkload(_DeviceCall):
         self.check_rc(self.lib.jb_bfs(self.n, self.m, d["s"].data_ptr(), d["d"].data_ptr(), d["e"].data_ptr(), 0,
                                       self.cost.data_ptr(), self.stream.cuda_stream))
 
-    def cpu_sample(self, oracle):
+    def ref_step(self, oracle, sample=False):
         h = self.host
-        t = time.perf_counter()
         oracle.bfs(h["s"], h["d"], h["e"], 0)
-        return self.m / 1e9 / (time.perf_counter() - t), "full traversal, oracle/juno_oracle.c (1 thread)"
+        return self.m / 1e9, "the full traversal, oracle/juno_oracle.c (sequential level loop)"
 
     def check(self, oracle):
         h = self.host
@@ -625,6 +639,10 @@ class BackpropWorkload(_DeviceCall):
         x, iw, hw, t, ipw, hpw = W.bp_inputs(self.n_in, 16, 1)
         self.host = {"x": x, "iw": iw, "hw": hw, "t": t, "ipw": ipw, "hpw": hpw}
         self.inputs_e2e = ["x", "iw", "hw", "t", "ipw", "hpw"]
+
+    def execute_args(self):
+        h = self.host
+        return "backprop", [self.n_in, 16, 1], [h["x"], h["iw"], h["hw"], h["t"], h["ipw"], h["hpw"]]
 
     def alloc_outputs(self, torch):
         self.hidden = torch.empty(17, dtype=torch.float32, device="cuda")
@@ -654,12 +672,10 @@ class BackpropWorkload(_DeviceCall):
                                                d["hpw"].data_ptr(), self.hidden.data_ptr(), self.output.data_ptr(),
                                                self.errs.data_ptr(), self.stream.cuda_stream))
 
-    def cpu_sample(self, oracle):
+    def ref_step(self, oracle, sample=False):
         h = self.host
-        n = 1 << 20
-        t = time.perf_counter()
-        oracle.bp_train(h["x"][:n + 1], h["iw"][:n + 1], h["hw"], h["t"], h["ipw"][:n + 1], h["hpw"])
-        return (time.perf_counter() - t) * (self.n_in / n) * 1e3, "2^20-input slab, scaled to 2^24"
+        oracle.bp_train(h["x"], h["iw"], h["hw"], h["t"], h["ipw"], h["hpw"])
+        return 1, f"the full bpnn_train step at n_in={self.n_in}, oracle/juno_oracle.c (OpenMP)"
 
     def check(self, oracle):
         from paper_2503_10855_b200 import workloads as W
@@ -714,13 +730,14 @@ class CavaWorkload(_DeviceCall):
     def algorithmic_bytes_per_unit(self):
         return 6 * self.r * self.c  # u8 x3 in + u8 x3 out
 
-    e2e_api = "paper_2503_10855_b200.api.cava_pipelined (pinned host in/out, 8-frame chunks)"
+    e2e_api = ("paper_2503_10855_b200.api.execute('cava', ...) on numpy in/out "
+               "(input page-locked in place on first use, 8-frame chunks overlap copies and kernels)")
 
     def step_e2e(self):
-        """Public API on pinned host buffers, copies overlapped with the kernels."""
+        """The public entry on numpy host arrays."""
         from paper_2503_10855_b200 import api
         if self.local:
-            api.cava_pipelined(self.pin["raw"], *self.params, out=self.pin_out["out"])
+            self.e2e_out = api.execute("cava", [self.r, self.c, self.P], [self.host["raw"], *self.params])
 
     def step_device(self):
         if not self.local:
@@ -731,10 +748,10 @@ class CavaWorkload(_DeviceCall):
                                           d["coefs"].data_ptr(), d["tmap"].data_ptr(), self.out.data_ptr(),
                                           self.stream.cuda_stream))
 
-    def cpu_sample(self, oracle):
-        t = time.perf_counter()
-        oracle.cava(self.host["raw"][:1], *self.params)
-        return 1.0 / (time.perf_counter() - t), "1 frame, oracle/juno_oracle.c (OpenMP)"
+    def ref_step(self, oracle, sample=False):
+        k = min(16, self.local) if sample else self.local
+        oracle.cava(self.host["raw"][:k], *self.params)
+        return k, f"{k} frames, oracle/juno_oracle.c (OpenMP over frames)"
 
     def check(self, oracle):
         return bool(np.array_equal(self.out[:1].cpu().numpy(), oracle.cava(self.host["raw"][:1], *self.params)))
@@ -883,13 +900,29 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle
         threads = oracle.max_threads()
-        v, sample = wl.cpu_sample(oracle)
+        v, _, sample = ref_timed(wl, oracle, warmup=1, steps=3, sample=True)
         res["cpu_baseline"] = {"value": round(v, 4), "unit": wl.unit, "cores": threads, "kind": "port",
-                               "sample": sample}
+                               "sample": sample + "; median of 3 after 1 warm-up"}
         res["parity_spot_check"] = "pass" if wl.check(oracle) else "MISMATCH"
     if rank == 0:
         print(json.dumps(res), flush=True)
     d.close()
+
+
+def ref_timed(wl, oracle, warmup, steps, sample=False):
+    """Time ``steps`` host steps of the workload (after ``warmup``): returns
+    (metric value of the median step, median step ms, description)."""
+    hib = getattr(wl, "higher_is_better", True)
+    times, units, desc = [], 1, ""
+    for i in range(warmup + steps):
+        t = time.perf_counter()
+        units, desc = wl.ref_step(oracle, sample=sample)
+        dt = time.perf_counter() - t
+        if i >= warmup:
+            times.append(dt)
+    med = statistics.median(times)
+    value = units / med if hib else med * 1e3 / units
+    return value, med * 1e3, desc
 
 
 def run_reference(args):
@@ -897,30 +930,27 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import oracle
-    wl = WORKLOADS[args.workload](args, 0, 1) if not args.small else WORKLOADS[args.workload](args, 0, 1)
+    wl = WORKLOADS[args.workload](args, 0, 1)
     # every host thread: torch.distributed.run exports OMP_NUM_THREADS=1 to
     # its workers, which would time a single-threaded reference at N > 1
     oracle.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     threads = oracle.max_threads()
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, sample = wl.cpu_sample(oracle)
-        if i >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+    # each step is one real host step (ref_step), timed as it runs: the
+    # full batch for edge/CAVA/matmul/BFS/backprop, one iteration of the
+    # full grid for SRAD/CFD (their metric is per iteration)
+    value, step_ms, desc = ref_timed(wl, oracle, args.warmup, args.steps)
     hib = getattr(wl, "higher_is_better", True)
     res = {"impl": "reference", "metric": wl.metric, "value": round(value, 4), "unit": wl.unit,
-           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(1e3 / value * wl.units_per_step(), 2) if hib else round(value, 2),
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 2),
            "higher_is_better": hib,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": wl.config(world),
+           "config": dict(wl.config(world), reference_step=desc),
            "cpu_baseline": {"value": round(value, 4), "unit": wl.unit, "cores": threads, "kind": "port",
-                            "sample": sample},
+                            "sample": desc + f"; median of {args.steps} timed steps"},
            "e2e": {"value": round(value, 4), "unit": wl.unit, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "note": "reference CPU path = oracle/juno_oracle.c (C restatement of the Juno program, "
-                   "OpenMP over the outer fork); the reference's own interpreter (skiff oracle_execute) "
+                   "OpenMP); the reference's own interpreter (skiff oracle_execute) "
                    "cannot run these sizes and is pinned to the port by tests/golden"}
     print(json.dumps(res), flush=True)
 

@@ -200,6 +200,11 @@ EXPORT void jo_edge_f32(int64_t batch, int64_t n, int64_t m, int64_t gs,
                         int64_t sz, int64_t sb, const float *in,
                         const float *gf, const float *st, const float *sx,
                         const float *sy, float theta, float *out) {
+  /* frames are independent: with at least two frames the threads split the
+   * batch (the paper's multicore macro chunks the outermost parallel fork,
+   * PAPER.md:626-630); each frame then runs its stages on one thread (the
+   * per-stage parallel loops are nested regions, inactive by default) */
+#pragma omp parallel for schedule(dynamic, 1) if (batch > 1)
   for (int64_t f = 0; f < batch; f++)
     jo_edge_frame_f32(n, m, gs, sz, sb, in + f * n * m, gf, st, sx, sy, theta,
                       out + f * n * m, NULL, NULL, NULL, NULL, NULL);
@@ -361,6 +366,7 @@ EXPORT void jo_cava_u8(int64_t batch, int64_t R, int64_t C, int64_t P,
                        const uint8_t *in, const float *tstw, const float *ctrl,
                        const float *wts, const float *coefs,
                        const float *tmap, uint8_t *out) {
+#pragma omp parallel for schedule(dynamic, 1) if (batch > 1)
   for (int64_t f = 0; f < batch; f++)
     jo_cava_frame_u8(R, C, P, in + f * 3 * R * C, tstw, ctrl, wts, coefs, tmap,
                      out + f * 3 * R * C, NULL, NULL, NULL);

@@ -28,15 +28,15 @@ from typing import Any, Callable, Sequence
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostmem
 
 
 class RuntimeError_(Exception):
-    """Mirror of skiff.runtime.values.RuntimeError_."""
+    """Mirror of skiff.runtime.values.RuntimeError_ (values.py:20)."""
 
 
 class DynConstError(Exception):
-    """Mirror of skiff.dynconst.DynConstError."""
+    """Mirror of skiff.dynconst.DynConstError (dynconst.py:16-17)."""
 
 
 class OracleLimitError(RuntimeError_):
@@ -45,7 +45,38 @@ class OracleLimitError(RuntimeError_):
 
 
 class UnsupportedError(RuntimeError_):
-    """The entry/config has no kernel in this build (JB_ENOTSUP)."""
+    """The entry/config has no kernel in this build (JB_ENOTSUP), or the
+    module's function is not a computation any kernel implements."""
+
+
+# The reference classes each of ours stands for.  Callers written against
+# skiff catch skiff's classes; whenever skiff is loaded in this process the
+# drop-in raises a class deriving from BOTH ours and the reference's, so
+# ``except skiff.dynconst.DynConstError`` and ``except api.DynConstError``
+# both work.  (If skiff is not loaded no caller can name its classes.)
+_REF_CLASS = {
+    RuntimeError_: ("skiff.runtime.values", "RuntimeError_"),
+    DynConstError: ("skiff.dynconst", "DynConstError"),
+    OracleLimitError: ("skiff.runtime.oracle", "OracleLimitError"),
+    UnsupportedError: ("skiff.runtime.values", "RuntimeError_"),
+}
+_DUAL: dict = {}
+
+
+def _err(cls, msg: str) -> Exception:
+    """An instance of ``cls`` that is also the reference's class of the same
+    role when skiff is loaded."""
+    import sys
+    mod, name = _REF_CLASS.get(cls, (None, None))
+    ref = getattr(sys.modules.get(mod), name, None) if mod else None
+    if ref is None or issubclass(cls, ref):
+        return cls(msg)
+    key = (cls, ref)
+    dual = _DUAL.get(key)
+    if dual is None:
+        dual = type(cls.__name__, (cls, ref), {"__module__": cls.__module__, "__doc__": cls.__doc__})
+        _DUAL[key] = dual
+    return dual(msg)
 
 
 def _torch():
@@ -58,9 +89,9 @@ def _check(status: int, what: str) -> None:
         return
     msg = f"{what}: {_lib.last_error()}"
     if status == _lib.JB_EINVAL:
-        raise RuntimeError_(msg)
+        raise _err(RuntimeError_, msg)
     if status == _lib.JB_ENOTSUP:
-        raise UnsupportedError(msg)
+        raise _err(UnsupportedError, msg)
     raise RuntimeError(msg)
 
 
@@ -79,7 +110,14 @@ def _torch_dtype(np_dtype):
 
 class _Call:
     """Collects device buffers for one call; remembers whether results must
-    be copied back to the host (numpy in -> numpy out)."""
+    be copied back to the host (numpy in -> numpy out).
+
+    The call's device is the device of its CUDA tensor arguments (else the
+    current one); ``on_device()`` makes it current around the library call,
+    since the C library resolves scratch, caches and attributes against the
+    current device.  Host (numpy) inputs are page-locked in place and copied
+    asynchronously (hostmem.py); host results come back through pinned
+    memory, with one stream synchronisation before they are returned."""
 
     def __init__(self, args, device=None):
         torch = _torch()
@@ -89,41 +127,58 @@ class _Call:
             device = dev if dev is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         if self.device.type != "cuda":
-            raise RuntimeError_("libjunob200 computes on CUDA devices only (no CPU fallback)")
+            raise _err(RuntimeError_, "libjunob200 computes on CUDA devices only (no CPU fallback)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.current_stream(self.device)
+        self._synced = False
+
+    def on_device(self):
+        return _torch().cuda.device(self.device)
+
+    def host_array(self, x, np_dtype, name: str):
+        a = np.asarray(x)
+        if a.dtype != np.dtype(np_dtype):
+            if a.dtype.kind != np.dtype(np_dtype).kind and not (a.dtype.kind in "iu" and
+                                                                np.dtype(np_dtype).kind in "iu"):
+                raise _err(RuntimeError_, f"{name}: expected {np.dtype(np_dtype).name}, got {a.dtype}")
+            a = a.astype(np_dtype)
+        a = np.ascontiguousarray(a)
+        # uint32 has limited torch support: move the raw bytes as int32
+        return a.view(np.int32) if a.dtype == np.uint32 else a
 
     def dev(self, x, np_dtype, name: str, copy: bool = False):
         torch = _torch()
         want = _torch_dtype(np_dtype)
         if isinstance(x, torch.Tensor):
             if x.dtype != want:
-                raise RuntimeError_(f"{name}: expected {np.dtype(np_dtype).name}, got {x.dtype}")
+                raise _err(RuntimeError_, f"{name}: expected {np.dtype(np_dtype).name}, got {x.dtype}")
             t = x.to(self.device, non_blocking=True)
             if not t.is_contiguous():
                 t = t.contiguous()
             elif copy and t.data_ptr() == x.data_ptr():
                 t = t.clone()
             return t
-        a = np.asarray(x)
-        if a.dtype != np.dtype(np_dtype):
-            if a.dtype.kind != np.dtype(np_dtype).kind and not (a.dtype.kind in "iu" and
-                                                                np.dtype(np_dtype).kind in "iu"):
-                raise RuntimeError_(f"{name}: expected {np.dtype(np_dtype).name}, got {a.dtype}")
-            a = a.astype(np_dtype)
-        a = np.ascontiguousarray(a)
-        # uint32 has limited torch support: move the raw bytes as int32
-        if a.dtype == np.uint32:
-            return torch.from_numpy(a.view(np.int32)).to(self.device, non_blocking=False)
-        return torch.from_numpy(a).to(self.device, non_blocking=False)
+        h = hostmem.pinned_view(self.host_array(x, np_dtype, name))
+        with torch.cuda.stream(self.stream):
+            return h.to(self.device, non_blocking=True)
 
     def empty(self, shape, np_dtype):
         torch = _torch()
         return torch.empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype), device=self.device)
 
     def out(self, t):
-        if self.host:
-            return t.cpu().numpy()
-        return t
+        if not self.host:
+            return t
+        torch = _torch()
+        if t.numel() * t.element_size() < hostmem.MIN_BYTES:
+            with torch.cuda.stream(self.stream):
+                return t.cpu().numpy()
+        h = hostmem.pinned_empty(t.shape, t.dtype)
+        with torch.cuda.stream(self.stream):
+            h.copy_(t, non_blocking=True)
+        self.stream.synchronize()
+        return h.numpy()
 
     @property
     def s(self):
@@ -140,7 +195,7 @@ def _shape(x) -> tuple:
 
 def _need(cond: bool, msg: str):
     if not cond:
-        raise RuntimeError_(msg)
+        raise _err(RuntimeError_, msg)
 
 
 def _scalar(x, ty=float):
@@ -164,7 +219,8 @@ def matmul(a, b, exact: bool = False):
     da, db = c.dev(a, np.float32, "a"), c.dev(b, np.float32, "b")
     out = c.empty((n, l), np.float32)
     fn = _lib.load().jb_matmul_exact_f32 if exact else _lib.load().jb_matmul_f32
-    _check(fn(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+    with c.on_device():
+        _check(fn(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
     return c.out(out)
 
 
@@ -182,20 +238,27 @@ def edge_detection(input, gaussian_filter, structure, sx, sy, theta):
     _need(_shape(structure) == (sz, sz), "edge_detection: structure must be square")
     _need(_shape(sx) == (sb, sb) and _shape(sy) == (sb, sb), "edge_detection: sx/sy must be sb x sb")
     c = _Call([input, gaussian_filter, structure, sx, sy])
+    if c.host and len(shp) == 3 and batch > 1:
+        # a host batch streams through the device: copies overlap kernels
+        x = hostmem.pinned_view(c.host_array(input, np.float32, "input"))
+        out = hostmem.pinned_empty(shp, _torch().float32)
+        edge_detection_pipelined(x, gaussian_filter, structure, sx, sy, theta, out=out, device=c.device)
+        return out.numpy()
     din = c.dev(input, np.float32, "input")
     dg, dst, dsx, dsy = (c.dev(x, np.float32, nm) for x, nm in
                          ((gaussian_filter, "gaussian_filter"), (structure, "structure"), (sx, "sx"),
                           (sy, "sy")))
     out = c.empty(shp, np.float32)
-    _check(_lib.load().jb_edge_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst), _ptr(dsx),
-                                   _ptr(dsy), _scalar(theta), _ptr(out), c.s), "edge_detection")
+    with c.on_device():
+        _check(_lib.load().jb_edge_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst), _ptr(dsx),
+                                       _ptr(dsy), _scalar(theta), _ptr(out), c.s), "edge_detection")
     return c.out(out)
 
 
 _PIPE_CACHE: dict = {}
 
 
-def _pipelined(x, out, chunk: int, key, launch):
+def _pipelined(x, out, chunk: int, key, launch, dev):
     """Host-buffer batch through the device with copy/compute overlap.
 
     Frames of the host batch ``x`` move in chunks through two device slots on
@@ -204,7 +267,6 @@ def _pipelined(x, out, chunk: int, key, launch):
     the sum of copy and compute time.  ``launch(k, din, dout, stream)`` runs
     the entry on the first k frames of the slot buffers."""
     torch = _torch()
-    dev = torch.device("cuda", torch.cuda.current_device())
     B = int(x.shape[0])
     key = (dev.index, x.dtype, tuple(x.shape[1:]), out.dtype, tuple(out.shape[1:]), chunk, key)
     st = _PIPE_CACHE.get(key)
@@ -245,7 +307,8 @@ def _pipelined(x, out, chunk: int, key, launch):
     return out
 
 
-def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 16):
+def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 16,
+                             device=None):
     """Host-buffer edge detection with copy/compute overlap (``_pipelined``).
 
     ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
@@ -259,7 +322,7 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
     if out is None:
         out = torch.empty_like(x, pin_memory=x.is_pinned())
     gs, sz, sb = (_shape(f)[0] for f in (gaussian_filter, structure, sx))
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     filt = [(f.to(dev) if isinstance(f, torch.Tensor) else
              torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
             for f in (gaussian_filter, structure, sx, sy)]
@@ -269,10 +332,11 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
         _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
                                filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(), stream),
                "edge_detection")
-    return _pipelined(x, out, chunk, "edge", launch)
+    with torch.cuda.device(dev):
+        return _pipelined(x, out, chunk, "edge", launch, dev)
 
 
-def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 8):
+def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 8, device=None):
     """Host-buffer CAVA over a batch u8[batch,3,r,c] with copy/compute overlap
     (``_pipelined``); returns ``out`` (a host u8 tensor of the input's shape)."""
     torch = _torch()
@@ -283,7 +347,7 @@ def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chu
     if out is None:
         out = torch.empty_like(x, pin_memory=x.is_pinned())
     P = _shape(ctrl_pts)[0]
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     prm = [(f.to(dev) if isinstance(f, torch.Tensor) else
             torch.from_numpy(np.ascontiguousarray(f, np.float32)).to(dev))
            for f in (tstw, ctrl_pts, weights, coefs, tonemap)]
@@ -292,7 +356,8 @@ def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chu
     def launch(k, din, dout, stream):
         _check(lib.jb_cava_u8(k, r, c, P, din.data_ptr(), *(t.data_ptr() for t in prm), dout.data_ptr(), stream),
                "cava")
-    return _pipelined(x, out, chunk, "cava", launch)
+    with torch.cuda.device(dev):
+        return _pipelined(x, out, chunk, "cava", launch, dev)
 
 
 def edge_detection_stages(input, gaussian_filter, structure, sx, sy, theta):
@@ -305,10 +370,11 @@ def edge_detection_stages(input, gaussian_filter, structure, sx, sy, theta):
     dg, dst, dsx, dsy = (c.dev(x, np.float32, "filter") for x in (gaussian_filter, structure, sx, sy))
     out, sm, lp, zc, gr = (c.empty(shp, np.float32) for _ in range(5))
     mx = c.empty((batch,), np.float32)
-    _check(_lib.load().jb_edge_stages_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst),
-                                          _ptr(dsx), _ptr(dsy), _scalar(theta), _ptr(out), _ptr(sm),
-                                          _ptr(lp), _ptr(zc), _ptr(gr), _ptr(mx), c.s),
-           "edge_detection_stages")
+    with c.on_device():
+        _check(_lib.load().jb_edge_stages_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst),
+                                              _ptr(dsx), _ptr(dsy), _scalar(theta), _ptr(out), _ptr(sm),
+                                              _ptr(lp), _ptr(zc), _ptr(gr), _ptr(mx), c.s),
+               "edge_detection_stages")
     return dict(out=c.out(out), smoothed=c.out(sm), laplacian=c.out(lp), zero_crossings=c.out(zc),
                 gradient=c.out(gr), max_gradient=c.out(mx))
 
@@ -327,13 +393,19 @@ def cava(input, tstw, ctrl_pts, weights, coefs, tonemap):
     _need(_shape(coefs) == (4, 3), "cava: coefs must be f32[4,3]")
     _need(_shape(tonemap) == (256, 3), "cava: tonemap must be f32[256,3]")
     c = _Call([input, tstw, ctrl_pts, weights, coefs, tonemap])
+    if c.host and len(shp) == 4 and batch > 1:
+        x = hostmem.pinned_view(c.host_array(input, np.uint8, "input"))
+        out = hostmem.pinned_empty(shp, _torch().uint8)
+        cava_pipelined(x, tstw, ctrl_pts, weights, coefs, tonemap, out=out, device=c.device)
+        return out.numpy()
     din = c.dev(input, np.uint8, "input")
     dt, dc, dw, dco, dtm = (c.dev(x, np.float32, nm) for x, nm in
                             ((tstw, "TsTw"), (ctrl_pts, "ctrl_pts"), (weights, "weights"),
                              (coefs, "coefs"), (tonemap, "tonemap")))
     out = c.empty(shp, np.uint8)
-    _check(_lib.load().jb_cava_u8(batch, r, cc, P, _ptr(din), _ptr(dt), _ptr(dc), _ptr(dw), _ptr(dco),
-                                  _ptr(dtm), _ptr(out), c.s), "cava")
+    with c.on_device():
+        _check(_lib.load().jb_cava_u8(batch, r, cc, P, _ptr(din), _ptr(dt), _ptr(dc), _ptr(dw), _ptr(dco),
+                                      _ptr(dtm), _ptr(out), c.s), "cava")
     return c.out(out)
 
 
@@ -342,15 +414,16 @@ def srad(niter, lam, image, return_q0sqr: bool = False):
     """srad<rows,cols>(niter, lambda, image f32[rows,cols]) -> f32[rows,cols]."""
     niter = _scalar(niter, int)
     if niter < 0:
-        raise DynConstError(f"srad: niter must be >= 0 (got {niter})")
+        raise _err(DynConstError, f"srad: niter must be >= 0 (got {niter})")
     _need(len(_shape(image)) == 2, "srad: image must be f32[rows,cols]")
     rows, cols = _shape(image)
     c = _Call([image])
     dimg = c.dev(image, np.float32, "image")
     out = c.empty((rows, cols), np.float32)
     q0 = c.empty((max(niter, 1),), np.float32)
-    _check(_lib.load().jb_srad_f32(rows, cols, niter, _scalar(lam), _ptr(dimg), _ptr(out), _ptr(q0), c.s),
-           "srad")
+    with c.on_device():
+        _check(_lib.load().jb_srad_f32(rows, cols, niter, _scalar(lam), _ptr(dimg), _ptr(out), _ptr(q0), c.s),
+               "srad")
     if return_q0sqr:
         return c.out(out), c.out(q0[:niter])
     return c.out(out)
@@ -362,7 +435,7 @@ def euler(iterations, areas, neighbors, normals, ff_variable, variables):
     normals f32[4,3,nelr], ff_variable f32[5], variables f32[5,nelr]) -> f32[5,nelr]."""
     iterations = _scalar(iterations, int)
     if iterations < 0:
-        raise DynConstError("euler: iterations must be >= 0")
+        raise _err(DynConstError, "euler: iterations must be >= 0")
     nelr = _shape(areas)[0]
     _need(_shape(neighbors) == (4, nelr), "euler: neighbors must be i32[4,nelr]")
     _need(_shape(normals) == (4, 3, nelr), "euler: normals must be f32[4,3,nelr]")
@@ -374,8 +447,9 @@ def euler(iterations, areas, neighbors, normals, ff_variable, variables):
     dno = c.dev(normals, np.float32, "normals")
     dff = c.dev(ff_variable, np.float32, "ff_variable")
     dv = c.dev(variables, np.float32, "variables", copy=True)  # value semantics
-    _check(_lib.load().jb_euler_f32(nelr, iterations, _ptr(da), _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), c.s),
-           "euler")
+    with c.on_device():
+        _check(_lib.load().jb_euler_f32(nelr, iterations, _ptr(da), _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), c.s),
+               "euler")
     return c.out(dv)
 
 
@@ -384,7 +458,8 @@ def euler_step_factor(variables, areas):
     c = _Call([variables, areas])
     dv, da = c.dev(variables, np.float32, "variables"), c.dev(areas, np.float32, "areas")
     out = c.empty((nelr,), np.float32)
-    _check(_lib.load().jb_euler_step_factor_f32(nelr, _ptr(dv), _ptr(da), _ptr(out), c.s), "euler_step_factor")
+    with c.on_device():
+        _check(_lib.load().jb_euler_step_factor_f32(nelr, _ptr(dv), _ptr(da), _ptr(out), c.s), "euler_step_factor")
     return c.out(out)
 
 
@@ -394,8 +469,9 @@ def euler_flux(neighbors, normals, ff_variable, variables):
     dn = c.dev(neighbors, np.int32, "neighbors")
     dno, dff, dv = (c.dev(x, np.float32, "f") for x in (normals, ff_variable, variables))
     out = c.empty((5, nelr), np.float32)
-    _check(_lib.load().jb_euler_flux_f32(nelr, _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), _ptr(out), c.s),
-           "euler_flux")
+    with c.on_device():
+        _check(_lib.load().jb_euler_flux_f32(nelr, _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), _ptr(out), c.s),
+               "euler_flux")
     return c.out(out)
 
 
@@ -412,7 +488,8 @@ def bfs(starting, no_of_edges, edges, source):
     dne = c.dev(no_of_edges, np.uint32, "no_of_edges")
     de = c.dev(edges, np.uint32, "edges") if m else c.empty((1,), np.int32)
     cost = c.empty((n,), np.int32)
-    _check(_lib.load().jb_bfs(n, m, _ptr(ds), _ptr(dne), _ptr(de), source, _ptr(cost), c.s), "bfs")
+    with c.on_device():
+        _check(_lib.load().jb_bfs(n, m, _ptr(ds), _ptr(dne), _ptr(de), source, _ptr(cost), c.s), "bfs")
     return c.out(cost)
 
 
@@ -439,9 +516,10 @@ def backprop(input_vals, input_weights, hidden_weights, target, input_prev_weigh
     hidden = c.empty((n_hid1,), np.float32)
     output = c.empty((n_out1,), np.float32)
     errs = c.empty((2,), np.float32)
-    _check(_lib.load().jb_bp_train_f32(n_in1 - 1, n_hid1 - 1, n_out1 - 1, _ptr(dx), _ptr(diw), _ptr(dhw),
-                                       _ptr(dt), _ptr(dipw), _ptr(dhpw), _ptr(hidden), _ptr(output),
-                                       _ptr(errs), c.s), "backprop")
+    with c.on_device():
+        _check(_lib.load().jb_bp_train_f32(n_in1 - 1, n_hid1 - 1, n_out1 - 1, _ptr(dx), _ptr(diw), _ptr(dhw),
+                                           _ptr(dt), _ptr(dipw), _ptr(dhpw), _ptr(hidden), _ptr(output),
+                                           _ptr(errs), c.s), "backprop")
     e = c.out(errs)
     return (e[0], e[1], c.out(diw), c.out(dhw), c.out(dipw), c.out(dhpw))
 
@@ -487,52 +565,73 @@ ENTRIES: dict[str, Entry] = {
 
 
 def execute(entry: str, dyn_consts, args):
-    """Run Juno ``entry`` on the B200: ``oracle_execute`` without the module."""
+    """Run Juno ``entry`` on the B200: ``oracle_execute`` without the module
+    (the entry names the benchmark program of SURVEY.md §8 (a.2))."""
     dcs, args = validate(entry, dyn_consts, args)
     return ENTRIES[entry].run(dcs, args)
+
+
+# argument index that may carry a leading batch dimension (independent frames)
+BATCHED_ARG = {"edge_detection": 0, "cava": 0}
 
 
 def validate(entry: str, dyn_consts, args):
     """The invocation checks of ``execute``: entry known, dynamic constants
     counted and non-negative (dynconst.py:179-204), argument extents equal to
-    the ones the dynamic constants give.  Returns (dcs, args)."""
+    the ones the dynamic constants give (edge/cava input may add a leading
+    batch dimension).  Returns (dcs, args)."""
     if entry not in ENTRIES:
-        raise RuntimeError_(f"no B200 kernel for entry {entry!r}; known: {sorted(ENTRIES)}")
+        raise _err(RuntimeError_, f"no B200 kernel for entry {entry!r}; known: {sorted(ENTRIES)}")
     spec = ENTRIES[entry]
     dcs = [int(x) for x in dyn_consts]
     if len(dcs) != len(spec.dyn_consts):
-        raise DynConstError(f"{entry}: expected {len(spec.dyn_consts)} dynamic constants "
-                            f"{spec.dyn_consts}, got {len(dcs)}")
+        raise _err(DynConstError, f"{entry}: expected {len(spec.dyn_consts)} dynamic constants "
+                                  f"{spec.dyn_consts}, got {len(dcs)}")
     for nm, v in zip(spec.dyn_consts, dcs):
         if v < 0:
-            raise DynConstError(f"{entry}: dynamic constant {nm} = {v} is negative")
+            raise _err(DynConstError, f"{entry}: dynamic constant {nm} = {v} is negative")
     args = list(args)
     for idx, want in spec.shapes(dcs, args):
         if idx >= len(args):
-            raise RuntimeError_(f"{entry}: missing argument {idx}")
-        got = _shape(args[idx])
-        # edge/cava also accept a leading batch dimension
-        if got != tuple(want) and got[1:] != tuple(want):
-            raise RuntimeError_(f"{entry}: argument {idx} has shape {got}, expected {tuple(want)} "
-                                f"under dyn-consts {dict(zip(spec.dyn_consts, dcs))}")
+            raise _err(RuntimeError_, f"{entry}: missing argument {idx}")
+        got, want = _shape(args[idx]), tuple(want)
+        batched = BATCHED_ARG.get(entry) == idx and len(got) == len(want) + 1 and got[1:] == want
+        if got != want and not batched:
+            raise _err(RuntimeError_, f"{entry}: argument {idx} has shape {got}, expected {want} "
+                                      f"under dyn-consts {dict(zip(spec.dyn_consts, dcs))}")
     return dcs, args
+
+
+def _raise_dc(msg, cause):
+    raise _err(DynConstError, msg) from cause
 
 
 def oracle_execute(module, entry: str, dyn_consts, args, max_steps: int = 50_000_000):
     """Drop-in for skiff.runtime.oracle.oracle_execute (oracle.py:28-32).
 
-    ``module`` may be a skiff ``Module`` (its function table must contain
-    ``entry``; an entry under another name is matched to a B200 kernel by
-    its signature, see planner.py) or None.  ``max_steps`` is accepted for signature parity; the
-    device path has no interpreter budget."""
+    ``module`` is a skiff ``Module``.  Its function ``entry`` (KeyError when
+    absent, as oracle.py:30) is first held to its invocation contract --
+    divisibility constraints and exact dynamic-constant evaluation, raising
+    ``DynConstError`` as the reference does (recognize.check_invocation) --
+    then recognised structurally (recognize.recognize: the body, not the name
+    or signature).  A function no kernel computes raises
+    ``UnsupportedError``.  ``module=None`` runs the benchmark program named
+    by ``entry`` directly (``execute``).  ``max_steps`` is accepted for
+    signature parity; the device path has no interpreter budget."""
     del max_steps
+    if module is None:
+        return execute(entry, dyn_consts, args)
     fns = getattr(module, "functions", None)
-    if fns is not None:
-        if entry not in fns:
-            raise KeyError(entry)
-        if entry not in ENTRIES:
-            # a renamed / scheduled entry: pick the kernel by signature and
-            # extents (planner.select_kernel, SURVEY §8(f)1)
-            from .planner import select_kernel
-            entry = select_kernel(module, entry, [int(x) for x in dyn_consts]).entry
-    return execute(entry, dyn_consts, args)
+    if fns is None:
+        raise _err(RuntimeError_, f"oracle_execute: {type(module).__name__} is not a Module")
+    fn = fns[entry]
+    from .recognize import check_invocation, recognize
+    dcs = check_invocation(fn, dyn_consts, _raise_dc)
+    args = list(args)
+    if len(args) != len(fn.param_types):
+        raise _err(RuntimeError_, f"{entry}: expected {len(fn.param_types)} arguments, got {len(args)}")
+    rec, why = recognize(fn, dcs)
+    if rec is None:
+        raise _err(UnsupportedError, f"no B200 kernel computes function {entry!r}: " +
+                   "; ".join(f"not {k} ({v})" for k, v in why.items()))
+    return execute(rec.entry, rec.dyn_consts, args)

@@ -49,6 +49,9 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "tcgen05.cuh"
 
@@ -82,6 +85,13 @@ constexpr int IR = 70;                 // input region (tile + 5 halo)
 constexpr int IP = 72;                 // input row pitch (floats)
 constexpr int LR = 62;                 // laplacian region (tile + 1 halo)
 constexpr int THREADS = 256;
+
+struct ConstBank {
+  cudaEvent_t ev = nullptr;   // recorded after the last kernel reading the bank
+  cudaStream_t stream = nullptr;
+};
+static std::map<std::pair<int, int>, ConstBank> g_bank;
+static std::mutex g_bank_mu;
 
 __constant__ float c_gauss[49];
 __constant__ float c_struct[9];
@@ -1162,6 +1172,15 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   fa.sched = (unsigned *)(ctl + 6 * pf);
   int *flags = (int *)(ctl + 6 * pf + 128);
 
+  // The filters live in this device's __constant__ bank, which every stream
+  // shares: a call on another stream than the previous one first waits for
+  // the previous call's kernels (recorded below), so it cannot overwrite
+  // filters a running kernel still reads.
+  std::unique_lock<std::mutex> bank_lock(g_bank_mu);
+  int bdev = 0;
+  cudaGetDevice(&bdev);
+  ConstBank &bank = g_bank[{bdev, 0}];
+  if (bank.ev && bank.stream != s) JB_CHECK_CUDA(cudaStreamWaitEvent(s, bank.ev, 0));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_gauss, gf, 49 * 4, 0, cudaMemcpyDeviceToDevice, s));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_struct, st, 9 * 4, 0, cudaMemcpyDeviceToDevice, s));
   JB_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_sx, sx, 9 * 4, 0, cudaMemcpyDeviceToDevice, s));
@@ -1213,6 +1232,9 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   edge_fused_kernel<<<grid, THREADS, smem, s>>>(fa);
   prof_end(tok, s);
   JB_LAUNCHED("edge_fused");
+  if (!bank.ev) JB_CHECK_CUDA(cudaEventCreateWithFlags(&bank.ev, cudaEventDisableTiming));
+  JB_CHECK_CUDA(cudaEventRecord(bank.ev, s));
+  bank.stream = s;
   return JB_OK;
 }
 

@@ -25,6 +25,8 @@
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer.
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
+#include <mutex>
+
 #include "common.cuh"
 #include "tcgen05.cuh"
 
@@ -351,8 +353,9 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     return JB_OK;
   }
   JB_REQUIRE(a && b, "matmul: null pointer");
+  // the epilogue stores res with 16-byte vector stores / reductions
   const bool tma_ok = (m % 4 == 0) && (l % 4 == 0) && ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
-                      tmap_encode_fn() != nullptr;
+                      ((uintptr_t)res % 16 == 0) && tmap_encode_fn() != nullptr;
   if (!tma_ok) return jb_matmul_exact_f32(n, m, l, a, b, res, stream);
 
   // tensor maps are encoded on the host (~microseconds each): keep the last
@@ -364,6 +367,9 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     bool valid;
   };
   static MapCache cache[64] = {};
+  // the caches below are per device and shared by host threads: one lock
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
   int cdev = 0;
   cudaGetDevice(&cdev);
   JB_REQUIRE(cdev >= 0 && cdev < 64, "matmul: device index out of range");
@@ -408,6 +414,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     const void *a, *b, *c;
     uint64_t n, m, l;
     cudaGraphExec_t exec;
+    bool failed;  // capture/instantiate failed for this key: plain launches
   };
   static GraphCache gcache[64] = {};
   static cudaStream_t cap_stream[64] = {};
@@ -415,7 +422,10 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   const bool repeat = gc.a == a && gc.b == b && gc.c == res && gc.n == n && gc.m == m && gc.l == l;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   JB_CHECK_CUDA(cudaStreamIsCapturing(s, &cap));
-  if (repeat && !gc.exec && cap == cudaStreamCaptureStatusNone) {
+  // never consume an error the caller has not seen yet: only capture with a
+  // clean error state, and clear only what the capture itself raised
+  if (repeat && !gc.exec && !gc.failed && cap == cudaStreamCaptureStatusNone &&
+      cudaPeekAtLastError() == cudaSuccess) {
     if (!cap_stream[cdev]) JB_CHECK_CUDA(cudaStreamCreateWithFlags(&cap_stream[cdev], cudaStreamNonBlocking));
     cudaStream_t cs = cap_stream[cdev];
     cudaGraph_t graph = nullptr;
@@ -427,7 +437,10 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
       if (cudaGraphInstantiate(&gc.exec, graph, 0) != cudaSuccess) gc.exec = nullptr;
       cudaGraphDestroy(graph);
     }
-    cudaGetLastError();  // a failed capture falls back to plain launches
+    if (!gc.exec) {
+      gc.failed = true;    // a failed capture falls back to plain launches, once
+      cudaGetLastError();
+    }
   }
   if (repeat && gc.exec && cap == cudaStreamCaptureStatusNone) {  // (a caller's capture records plain launches)
     void *tok = prof_begin("matmul_tcgen05", s);
@@ -438,7 +451,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   if (!repeat) {
     if (gc.exec) cudaGraphExecDestroy(gc.exec);
-    gc = GraphCache{a, b, res, n, m, l, nullptr};
+    gc = GraphCache{a, b, res, n, m, l, nullptr, false};
   }
   if (splitk > 1) JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
   void *tok = prof_begin("matmul_tcgen05", s);

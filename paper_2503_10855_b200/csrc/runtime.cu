@@ -67,23 +67,33 @@ void set_error(const char *fmt, ...) {
   va_end(ap);
 }
 
+// One scratch arena per (device, stream): two streams of one device never
+// share scratch, so concurrent calls on different streams cannot corrupt
+// each other.  Growing waits for the stream's own earlier users only; it is
+// refused while the stream is being captured into a graph (free/alloc are
+// not capturable): run the call once outside the capture to size it.
 struct Arena {
   void *ptr = nullptr;
   size_t cap = 0;
 };
-static Arena g_arena[64];
+static std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
 static std::mutex g_arena_mu;
 
 void *workspace(size_t bytes, cudaStream_t s) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return nullptr;
   std::lock_guard<std::mutex> lk(g_arena_mu);
-  Arena &a = g_arena[dev];
+  Arena &a = g_arenas[{dev, s}];
   if (bytes <= a.cap) return a.ptr;
-  // growing: wait for in-flight users of the old block before freeing it
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    set_error("scratch arena must grow to %zu bytes while the stream is capturing; "
+              "run the call once outside the capture first", bytes);
+    return nullptr;
+  }
   if (a.ptr) {
-    cudaStreamSynchronize(s);
-    cudaDeviceSynchronize();
+    cudaStreamSynchronize(s);  // the old block's users are on this stream
     cudaFree(a.ptr);
     a.ptr = nullptr;
     a.cap = 0;
@@ -213,18 +223,47 @@ jb_status jb_prof_read(const char *name, double *ms, uint64_t *count) {
 
 jb_status jb_release_workspace(void) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
     jb::set_error("jb_release_workspace: no current device");
     return JB_ECUDA;
   }
   std::lock_guard<std::mutex> lk(jb::g_arena_mu);
-  jb::Arena &a = jb::g_arena[dev];
-  if (a.ptr) {
-    cudaDeviceSynchronize();
-    cudaFree(a.ptr);
+  cudaDeviceSynchronize();
+  for (auto it = jb::g_arenas.begin(); it != jb::g_arenas.end();) {
+    if (it->first.first == dev) {
+      if (it->second.ptr) cudaFree(it->second.ptr);
+      it = jb::g_arenas.erase(it);
+    } else {
+      ++it;
+    }
   }
-  a.ptr = nullptr;
-  a.cap = 0;
+  return JB_OK;
+}
+
+// Page-lock caller-owned host memory in place (the numpy path of the
+// Python mirror uses it so host<->device copies are DMA at full PCIe rate
+// without a staging copy).  Registration errors are reported, not sticky.
+jb_status jb_host_register(void *ptr, uint64_t bytes) {
+  if (!ptr || !bytes) {
+    jb::set_error("jb_host_register: null range");
+    return JB_EINVAL;
+  }
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    jb::set_error("cudaHostRegister(%zu bytes): %s", (size_t)bytes, cudaGetErrorString(e));
+    return e == cudaErrorHostMemoryAlreadyRegistered ? JB_EINVAL : JB_ECUDA;
+  }
+  return JB_OK;
+}
+
+jb_status jb_host_unregister(void *ptr) {
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    jb::set_error("cudaHostUnregister: %s", cudaGetErrorString(e));
+    return JB_ECUDA;
+  }
   return JB_OK;
 }
 

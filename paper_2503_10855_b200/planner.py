@@ -7,23 +7,21 @@ LaunchPlan`` but does not implement it.
 This module implements that contract over the reference's own IR objects and
 connects the result to the hand-written B200 kernels:
 
-  * :func:`fork_nest` matches every fork with its join and builds the
-    containment tree, with a synthetic factor-1 root when there are several
-    top-level forks (the tree of PAPER.md:376; matching rule as in
-    skiff/analysis.py:192-237 fork_joins / :262-291 fork_join_nest);
+  * :func:`fork_nest` takes the fork-join nest from the reference's own
+    analysis (skiff/analysis.py:199-312 fork_joins / fork_join_nest /
+    reduces_of_join; synthetic factor-1 root for several top-level forks,
+    the tree of PAPER.md:376) and classifies each fork's reductions;
   * :func:`launch_plan` sizes the tree bottom-up with the paper's three rules
     and splits the root size into blocks and threads (PAPER.md:378-383);
-  * :func:`select_kernel` picks the B200 entry for a (scheduled) function by
-    name or, failing that, by signature + extents, and reports the B200
-    launch geometry next to the schedule's plan;
+  * :func:`select_kernel` checks the function's invocation contract and
+    recognises its body structurally (recognize.py) -- never by name or
+    signature -- and reports the B200 launch geometry next to the plan;
   * :func:`execute_module` is ``oracle_execute`` for a scheduled module: it
     plans, selects and runs (api.execute), and returns the plan it used.
 
-The IR is consumed duck-typed (``module.functions[name]`` with ``nodes``,
-``live_nodes()``, ``param_types``, ``num_dyn_consts``, ``device``; nodes with
-``kind``, ``control``, ``preds``, ``inputs``, ``factors``, ``attributes``;
-DynConst trees DcParam/DcLiteral/DcAdd/DcSub/DcMul/DcDiv), so this package
-never imports the reference.
+The IR is the reference's; the reference helpers used (analysis,
+dynconst) are imported from the package that built the function, so this
+package never imports the reference on its own.
 
 Reduction classes (reduce-node attributes, skiff/ir.py:26-28, inferred by
 skiff/passes/attrs.py:174-194 or applied by a schedule):
@@ -33,12 +31,12 @@ skiff/passes/attrs.py:174-194 or applied by a schedule):
 """
 from __future__ import annotations
 
+import importlib
 from dataclasses import dataclass, field
 from typing import Any, Optional, Sequence
 
 PARALLEL_REDUCE = "parallel_reduce"  # skiff/ir.py:26
 MONOID_REDUCE = "monoid_reduce"      # skiff/ir.py:27
-CONTROL_KINDS = frozenset({"start", "region", "if", "proj", "return", "fork", "join"})  # ir.py:31
 
 BLOCK, THREAD, SEQUENTIAL = "BlockLevel", "ThreadLevel", "Sequential"
 PARALLEL, COOPERATIVE, SEQ_REDUCE = "Parallel", "CooperativeTile", "Sequential"
@@ -155,54 +153,6 @@ class Nest:
             yield from c.walk()
 
 
-def _control_successors(fn) -> dict:
-    succ: dict[int, list[int]] = {}
-    for i, n in fn.live_nodes():
-        if n.kind in CONTROL_KINDS:
-            succ.setdefault(i, [])
-    for i, n in fn.live_nodes():
-        if n.kind not in CONTROL_KINDS:
-            continue
-        for p in ([n.control] if n.control is not None else []) + list(n.preds):
-            if p in succ:
-                succ[p].append(i)
-    return succ
-
-
-def _match_joins(fn, succ) -> dict[int, tuple[int, set]]:
-    """fork -> (join, body controls).  A token leaving the fork is followed
-    with a nesting counter (+1 through a fork, -1 through a join); the join
-    reached at counter 0 closes the fork."""
-    out = {}
-    for f, n in fn.live_nodes():
-        if n.kind != "fork":
-            continue
-        joins, body, seen = set(), set(), set()
-        todo = [(f, 0)]
-        while todo:
-            c, depth = todo.pop()
-            for s in succ.get(c, ()):
-                k = fn.nodes[s].kind
-                d = depth
-                if k == "join":
-                    if d == 0:
-                        joins.add(s)
-                        continue
-                    d -= 1
-                elif k == "fork":
-                    d += 1
-                if (s, d) not in seen:
-                    seen.add((s, d))
-                    body.add(s)
-                    todo.append((s, d))
-        if len(joins) != 1:
-            raise PlanError(f"{fn.name}: fork %{f} reaches joins {sorted(joins)}; fork-joins must nest")
-        j = joins.pop()
-        body.discard(j)
-        out[f] = (j, body)
-    return out
-
-
 def _classify(fn, reduces) -> str:
     kind = "parallel"
     for r in reduces:
@@ -216,33 +166,38 @@ def _classify(fn, reduces) -> str:
     return kind
 
 
+def _analysis(fn):
+    """The reference's own analysis module (the package that built ``fn``)."""
+    root = type(fn).__module__.split(".")[0]
+    return importlib.import_module(f"{root}.analysis")
+
+
 def fork_nest(fn) -> Optional[Nest]:
-    """Containment tree of ``fn``'s fork-joins, or None without forks."""
-    matched = _match_joins(fn, _control_successors(fn))
-    if not matched:
+    """Containment tree of ``fn``'s fork-joins, or None without forks.
+
+    Fork/join matching and nesting are the reference's own
+    (``analysis.fork_joins`` / ``fork_join_nest`` / ``reduces_of_join``,
+    skiff/analysis.py:199-312), so the planner cannot drift from them; this
+    adds only each fork's reduction class."""
+    an = _analysis(fn)
+    try:
+        infos = an.fork_joins(fn)
+        tree = an.fork_join_nest(fn)
+    except Exception as e:  # analysis.AnalysisError: forks that do not nest
+        raise PlanError(str(e)) from e
+    if tree is None:
         return None
-    reduces: dict[int, list[int]] = {}
-    for i, n in fn.live_nodes():
-        if n.kind == "reduce":
-            reduces.setdefault(n.control, []).append(i)
-    nodes = {}
-    for f, (j, body) in matched.items():
-        rs = sorted(reduces.get(j, []))
-        nodes[f] = Nest(f, j, list(fn.nodes[f].factors), body, reduces=rs, kind=_classify(fn, rs))
-    roots = []
-    for f in sorted(matched):
-        # parent: the enclosing fork with the smallest body
-        enc = [g for g in matched if g != f and f in matched[g][1]]
-        if enc:
-            p = min(enc, key=lambda g: (len(matched[g][1]), g))
-            nodes[p].children.append(nodes[f])
-        else:
-            roots.append(nodes[f])
-    for nd in nodes.values():
-        nd.children.sort(key=lambda c: c.fork)
-    if len(roots) == 1:
-        return roots[0]
-    return Nest(None, None, [], set(), children=roots)
+
+    def conv(t) -> Nest:
+        kids = [conv(c) for c in t.children]
+        if t.fork is None:
+            return Nest(None, None, [], set(), children=kids)
+        info = infos[t.fork]
+        rs = an.reduces_of_join(fn, info.join)
+        return Nest(t.fork, info.join, list(fn.nodes[t.fork].factors), set(info.body_controls), kids,
+                    reduces=rs, kind=_classify(fn, rs))
+
+    return conv(tree)
 
 
 # -------------------------------------------------------------- launch plan
@@ -349,32 +304,6 @@ def launch_plan(fn) -> LaunchPlan:
 
 
 # ---------------------------------------------------------- kernel selection
-def _type_sig(ty) -> tuple:
-    """('f32', rank) for arrays, ('f32', 0) for scalars."""
-    kind = type(ty).__name__
-    if kind == "ArrayType":
-        return (_type_sig(ty.element)[0], len(ty.extents))
-    if kind == "FloatType":
-        return (f"f{ty.width}", 0)
-    if kind == "IntType":
-        return (f"{'i' if ty.signed else 'u'}{ty.width}", 0)
-    if kind == "BoolType":
-        return ("bool", 0)
-    return (kind, 0)
-
-
-# B200 entries by structural signature (dyn-const count, parameter
-# (element, rank) list, return (element, rank)): the Juno signatures of
-# SURVEY.md §8 (a.2) b1-b7.
-SIGNATURES = {
-    "matmul": (3, [("f32", 2), ("f32", 2)], ("f32", 2)),
-    "edge_detection": (5, [("f32", 2)] * 5 + [("f32", 0)], ("f32", 2)),
-    "cava": (3, [("u8", 3), ("f32", 2), ("f32", 2), ("f32", 2), ("f32", 2), ("f32", 2)], ("u8", 3)),
-    "srad": (2, [("u64", 0), ("f32", 0), ("f32", 2)], ("f32", 2)),
-    "euler": (1, [("u64", 0), ("f32", 1), ("i32", 2), ("f32", 3), ("f32", 1), ("f32", 2)], ("f32", 2)),
-    "bfs": (2, [("u32", 1), ("u32", 1), ("u32", 1), ("u32", 0)], ("i32", 1)),
-}
-
 # the kernel each entry runs on the B200 (DESIGN.md §Kernels) and its fixed
 # launch geometry: the hand-written kernels size themselves to the machine
 # (persistent, SM-count multiples), not to the schedule's fork factors
@@ -394,52 +323,34 @@ class KernelChoice:
     entry: str           # B200 entry (api.ENTRIES key)
     c_symbol: str        # libjunob200.so function
     geometry: str        # the B200 kernel's own launch geometry
-    matched_by: str      # "name" | "signature"
+    matched_by: str      # "structure": the function body was recognised (recognize.py)
     plan: LaunchPlan     # the schedule's §4.4 plan of the function
+    dyn_consts: list = field(default_factory=list)   # the entry's dyn-consts
+    detail: str = ""
 
 
-def _signature(fn) -> tuple:
-    return (fn.num_dyn_consts, [_type_sig(t) for t in fn.param_types], _type_sig(fn.return_type))
+def select_kernel(module, entry: str, dyn_consts: Sequence[int]) -> KernelChoice:
+    """Pick the B200 kernel for ``module.functions[entry]`` under
+    ``dyn_consts``.
 
-
-def _extents_ok(fn, entry: str, dyn_consts: Sequence[int]) -> bool:
-    """The function's parameter extents, evaluated, match the shapes the B200
-    entry expects under the same dynamic constants."""
-    from .api import ENTRIES
-    want = dict(ENTRIES[entry].shapes(list(dyn_consts), []))
-    for i, ty in enumerate(fn.param_types):
-        if type(ty).__name__ != "ArrayType" or i not in want:
-            continue
-        try:
-            got = tuple(_dc_eval(e, dyn_consts) for e in ty.extents)
-        except PlanError:
-            return False
-        if got != tuple(want[i]):
-            return False
-    return True
-
-
-def select_kernel(module, entry: str, dyn_consts: Optional[Sequence[int]] = None) -> KernelChoice:
-    """Pick the B200 kernel for ``module.functions[entry]``.
-
-    By name when the entry is one of the benchmark entries, otherwise by
-    structural signature (and, given dyn_consts, evaluated extents).  Raises
-    api.UnsupportedError when nothing matches."""
-    from .api import ENTRIES, UnsupportedError
+    The function is held to its invocation contract (constraints, exact
+    dynamic-constant evaluation: ``DynConstError``) and then recognised from
+    its data graph (recognize.py) -- never by name or type signature.  Raises
+    api.UnsupportedError when no kernel computes it."""
+    from .api import UnsupportedError, _err, _raise_dc
+    from .recognize import check_invocation, recognize
     fns = getattr(module, "functions", None)
     if fns is None or entry not in fns:
         raise KeyError(entry)
     fn = fns[entry]
     plan = launch_plan(fn)
-    if entry in ENTRIES:
-        sym, geo = B200_KERNELS[entry]
-        return KernelChoice(entry, sym, geo, "name", plan)
-    sig = _signature(fn)
-    for name, want in SIGNATURES.items():
-        if sig == (want[0], list(want[1]), want[2]) and (dyn_consts is None or _extents_ok(fn, name, dyn_consts)):
-            sym, geo = B200_KERNELS[name]
-            return KernelChoice(name, sym, geo, "signature", plan)
-    raise UnsupportedError(f"no B200 kernel for function {entry!r} with signature {sig}")
+    dcs = check_invocation(fn, dyn_consts, _raise_dc)
+    rec, why = recognize(fn, dcs)
+    if rec is None:
+        raise _err(UnsupportedError, f"no B200 kernel computes function {entry!r}: " +
+                   "; ".join(f"not {k} ({v})" for k, v in why.items()))
+    sym, geo = B200_KERNELS[rec.entry]
+    return KernelChoice(rec.entry, sym, geo, "structure", plan, rec.dyn_consts, rec.detail)
 
 
 def execute_module(module, entry: str, dyn_consts, args, max_steps: int = 50_000_000):
@@ -448,4 +359,4 @@ def execute_module(module, entry: str, dyn_consts, args, max_steps: int = 50_000
     from .api import execute
     del max_steps
     choice = select_kernel(module, entry, [int(x) for x in dyn_consts])
-    return execute(choice.entry, dyn_consts, args), choice
+    return execute(choice.entry, choice.dyn_consts, args), choice

@@ -1,0 +1,246 @@
+"""The drop-in honours the module it is handed.
+
+``oracle_execute(module, entry, dyn_consts, args)`` must behave like the
+reference's (/root/reference/pkg/src/skiff/runtime/oracle.py:28-32) on the
+module's own terms:
+
+* a schedule's divisibility constraints and exact dyn-const divisions are
+  enforced at invocation: ``fork-chunk![4]`` on Fig. 1 matmul called at
+  n = 6 raises ``DynConstError`` on both sides (dynconst.py:179-204,
+  241-253; SPEC.md:542-545 names the constraint ``4 | n``);
+* the kernel is chosen from the function's body, not its name or type
+  signature: a same-signature function that computes something else raises
+  ``UnsupportedError`` instead of returning a matrix product;
+* errors are the reference's own classes when skiff is loaded
+  (``except skiff.dynconst.DynConstError`` catches the drop-in's).
+
+All checks before the kernel launch run on CPU; the last tests run the
+recognised, scheduled modules on the GPU against the reference interpreter.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in ("/root/reference/pkg/src", os.path.join(ROOT, "baseline", "_ref")):
+    if os.path.isdir(os.path.join(p, "skiff")) and p not in sys.path:
+        sys.path.append(p)
+skiff = pytest.importorskip("skiff")
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+
+import skiff.dynconst  # noqa: E402
+import skiff.runtime.values  # noqa: E402
+from skiff.frontend import parse  # noqa: E402
+from skiff.lower import lower  # noqa: E402
+from skiff.runtime.oracle import oracle_execute as ref_execute  # noqa: E402
+from skiff.schedule import parse_schedule, run_schedule  # noqa: E402
+
+from paper_2503_10855_b200 import api  # noqa: E402
+from paper_2503_10855_b200 import planner as P  # noqa: E402
+from paper_2503_10855_b200.recognize import check_invocation, recognize  # noqa: E402
+
+MATMUL = """
+#[entry]
+fn matmul<n, m, l: usize>(a: f32[n, m], b: f32[m, l]) -> f32[n, l] {
+  let res : f32[n, l];
+  @outer for i in 0..n {
+    @middle for j in 0..l {
+      @inner for k in 0..m {
+        res[i, j] += a[i, k] * b[k, j];
+      }
+    }
+  }
+  return res;
+}
+"""
+FORKS = "forkify(*); forkify(*); forkify(*);"
+# Fig. 4's first step: chunk the two outer loops by 4
+CHUNK4 = FORKS + r" let par = matmul@outer \ matmul@inner; fork-chunk![4](par);"
+SCHEDULES = {
+    "sequential": "",
+    "forkify-inner": "forkify(*); infer-attributes(*);",
+    "forkify-all": FORKS,
+    "chunk4-outer": CHUNK4,
+    "tile16-inner": FORKS + " fork-tile![16](matmul@inner);",
+    "tile4-all": FORKS + " fork-tile![4](matmul);",
+    "chunk2-tile2": FORKS + " fork-chunk![2](matmul); fork-tile![2](matmul);",
+}
+
+
+def module(src=MATMUL, schedule=""):
+    mod = lower(parse(src))[0]
+    if schedule:
+        run_schedule(mod, parse_schedule(schedule))
+    return mod
+
+
+def _ones(n, m):
+    return np.ones((n, m), np.float32)
+
+
+# ----------------------------------------------------------- invocation
+def test_chunk4_at_n6_raises_dynconst_error_on_both_sides():
+    mod = module(schedule=CHUNK4)
+    a = _ones(6, 6)
+    with pytest.raises(skiff.dynconst.DynConstError) as ref_err:
+        ref_execute(mod, "matmul", [6, 6, 6], [a, a])
+    assert "inexact dynamic-constant division 6/4" in str(ref_err.value)
+    with pytest.raises(skiff.dynconst.DynConstError) as ours:
+        api.oracle_execute(mod, "matmul", [6, 6, 6], [a, a])
+    # also the package's own class, and the message names the constraint
+    assert isinstance(ours.value, api.DynConstError)
+    assert "4 | " in str(ours.value) and "fork-chunk" in str(ours.value)
+
+
+def test_constraint_message_names_the_dyn_const():
+    mod = module(schedule=CHUNK4)
+    with pytest.raises(api.DynConstError, match=r"4 \| (n|l)"):
+        P.select_kernel(mod, "matmul", [6, 8, 8])
+    with pytest.raises(api.DynConstError, match=r"4 \| l"):
+        P.select_kernel(mod, "matmul", [8, 8, 6])
+    # satisfied constraints pass
+    assert P.select_kernel(mod, "matmul", [8, 6, 8]).entry == "matmul"
+
+
+def test_negative_and_miscounted_dyn_consts():
+    mod = module(schedule=FORKS)
+    with pytest.raises(skiff.dynconst.DynConstError):
+        api.oracle_execute(mod, "matmul", [4, -1, 4], [_ones(4, 1), _ones(1, 4)])
+    with pytest.raises(skiff.dynconst.DynConstError):
+        api.oracle_execute(mod, "matmul", [4, 4], [_ones(4, 4), _ones(4, 4)])
+
+
+def test_inexact_fork_factor_without_recorded_constraint():
+    """A fork factor n/3 written by hand (no DivisibilityConstraint recorded)
+    still fails exactly like the reference's evaluate at invocation."""
+    mod = module(schedule=FORKS)
+    fn = mod.functions["matmul"]
+    fk = next(n for _, n in fn.live_nodes() if n.kind == "fork")
+    fk.factors = [skiff.dynconst.dc_div(fk.factors[0], skiff.dynconst.DcLiteral(3))] + list(fk.factors[1:])
+    with pytest.raises(skiff.dynconst.DynConstError, match="inexact"):
+        check_invocation(fn, [4, 4, 4], api._raise_dc)
+
+
+def test_unknown_entry_is_a_key_error():
+    with pytest.raises(KeyError):
+        api.oracle_execute(module(), "nope", [1, 1, 1], [_ones(1, 1), _ones(1, 1)])
+
+
+# ---------------------------------------------------------- recognition
+@pytest.mark.parametrize("name", sorted(SCHEDULES))
+def test_every_matmul_schedule_is_recognised(name):
+    mod = module(schedule=SCHEDULES[name])
+    fn = mod.functions["matmul"]
+    for dcs in ([16, 32, 16], [32, 16, 64]):
+        rec, why = recognize(fn, check_invocation(fn, dcs, api._raise_dc))
+        assert rec is not None, why
+        assert rec.entry == "matmul" and rec.dyn_consts == dcs
+
+
+SAME_SIGNATURE = {
+    "transpose-b": ("res[i, j] += a[i, k] * b[k, j];", "res[i, j] += a[i, k] * b[j, k];",
+                    ("b: f32[m, l]", "b: f32[l, m]")),
+    "sum-not-product": ("res[i, j] += a[i, k] * b[k, j];", "res[i, j] += a[i, k] + b[k, j];", None),
+    "overwrite": ("res[i, j] += a[i, k] * b[k, j];", "res[i, j] = a[i, k] * b[k, j];", None),
+    "cubic": ("res[i, j] += a[i, k] * b[k, j];", "res[i, j] += a[i, k] * b[k, j] * a[i, k];", None),
+    "transposed-result": ("res[i, j] += a[i, k] * b[k, j];", "res[j, i] += a[i, k] * b[k, j];", None),
+    "subtract": ("res[i, j] += a[i, k] * b[k, j];", "res[i, j] = res[i, j] - a[i, k] * b[k, j];", None),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SAME_SIGNATURE))
+def test_same_signature_other_body_is_refused(name):
+    old, new, sig = SAME_SIGNATURE[name]
+    src = MATMUL.replace(old, new)
+    if sig:
+        src = src.replace(*sig)
+    n = 8
+    mod = module(src, FORKS)
+    a = np.arange(n * n, dtype=np.float32).reshape(n, n)
+    with pytest.raises(api.UnsupportedError) as e:
+        api.oracle_execute(mod, "matmul", [n, n, n], [a, a])
+    # UnsupportedError is the reference's RuntimeError_ class too
+    assert isinstance(e.value, skiff.runtime.values.RuntimeError_)
+    with pytest.raises(api.UnsupportedError):
+        P.select_kernel(mod, "matmul", [n, n, n])
+
+
+def test_offset_index_and_partial_range_are_refused():
+    # a[i, k] with k running over m-1 values: an iteration space that does not
+    # cover the extent (reads a shifted window)
+    src = MATMUL.replace("for k in 0..m", "for k in 1..m")
+    mod = module(src)
+    with pytest.raises(api.UnsupportedError):
+        P.select_kernel(mod, "matmul", [4, 4, 4])
+
+
+def test_renamed_benchmark_names_do_not_select_kernels():
+    """A function called edge_detection that is not edge detection (the
+    reference cannot express its sqrt) is refused."""
+    src = """
+#[entry]
+fn edge_detection<n: usize>(x: f32[n]) -> f32[n] {
+  let y : f32[n];
+  for i in 0..n { y[i] = x[i] + x[i]; }
+  return y;
+}
+"""
+    mod = module(src, "forkify(*);")
+    with pytest.raises(api.UnsupportedError):
+        api.oracle_execute(mod, "edge_detection", [16], [np.zeros(16, np.float32)])
+
+
+def test_errors_are_reference_classes_for_entry_level_calls():
+    with pytest.raises(skiff.dynconst.DynConstError):
+        api.execute("matmul", [4, 4], [_ones(4, 4), _ones(4, 4)])
+    with pytest.raises(skiff.runtime.values.RuntimeError_):
+        api.validate("matmul", [4, 4, 4], [_ones(4, 5), _ones(4, 4)])
+
+
+def test_batch_dimension_only_on_frame_inputs():
+    with pytest.raises(api.RuntimeError_):
+        api.validate("bfs", [4, 4], [np.zeros((4, 4), np.uint32), np.zeros(4, np.uint32),
+                                     np.zeros(4, np.uint32), 0])
+    f = np.zeros((3, 3), np.float32)
+    api.validate("edge_detection", [8, 8, 3, 3, 3], [np.zeros((2, 8, 8), np.float32), f, f, f, f, 0.1])
+    with pytest.raises(api.RuntimeError_):
+        api.validate("edge_detection", [8, 8, 3, 3, 3], [np.zeros((8, 8), np.float32),
+                                                         np.zeros((2, 3, 3), np.float32), f, f, f, 0.1])
+
+
+# ----------------------------------------------------------------- GPU
+def _bound(a, b):
+    u = 2.0 ** -24
+    m = a.shape[1]
+    gamma = m * u / (1 - m * u)
+    return (2 * gamma + 8 * u) * (np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SCHEDULES))
+def test_scheduled_modules_match_the_reference_interpreter(jb, name):
+    """Each recognised schedule runs the tcgen05 kernel; the result agrees
+    with skiff's own oracle_execute on the same module within the fp32
+    matmul bound (the reference folds k sequentially)."""
+    mod = module(schedule=SCHEDULES[name])
+    rng = np.random.default_rng(3)
+    n, m, l = 16, 32, 16
+    a = rng.uniform(-1, 1, (n, m)).astype(np.float32)
+    b = rng.uniform(-1, 1, (m, l)).astype(np.float32)
+    got = api.oracle_execute(mod, "matmul", [n, m, l], [a, b])
+    ref = ref_execute(mod, "matmul", [n, m, l], [a, b], max_steps=50_000_000)
+    assert got.dtype == np.float32 and got.shape == (n, l)
+    assert np.all(np.abs(got.astype(np.float64) - ref.astype(np.float64)) <= _bound(a, b))
+
+
+@pytest.mark.gpu
+def test_scheduled_module_full_size(jb, oracle):
+    """The Fig. 4 chunked schedule at the 1024^3 config, against the oracle."""
+    from paper_2503_10855_b200 import workloads as W
+    mod = module(schedule=CHUNK4)
+    a, b = W.matmul_inputs(1024, 1024, 1024, seed=0)
+    got = api.oracle_execute(mod, "matmul", [1024, 1024, 1024], [a, b])
+    ref = oracle.matmul(a, b)
+    assert np.all(np.abs(got.astype(np.float64) - ref.astype(np.float64)) <= _bound(a, b))

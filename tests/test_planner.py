@@ -158,7 +158,8 @@ def test_matmul_module_plan_and_selection():
     mod = _module(MATMUL, "forkify(*); infer-attributes(*); gpu(matmul);")
     assert mod.functions["matmul"].device == "gpu_sim"
     choice = P.select_kernel(mod, "matmul", [64, 32, 16])
-    assert choice.entry == "matmul" and choice.c_symbol == "jb_matmul_f32" and choice.matched_by == "name"
+    assert choice.entry == "matmul" and choice.c_symbol == "jb_matmul_f32" and choice.matched_by == "structure"
+    assert choice.dyn_consts == [64, 32, 16]
     forks = choice.plan.forks()
     assert forks, choice.plan.describe()
     # the forkified k loop carries res[i,j] += ...: an associative leaf
@@ -168,10 +169,11 @@ def test_matmul_module_plan_and_selection():
     assert leaf
 
 
-def test_selection_by_signature_checks_extents():
+def test_selection_is_structural_not_by_name():
     mod = _module(MATMUL.replace("matmul", "mm"), "forkify(*); infer-attributes(*);")
     choice = P.select_kernel(mod, "mm", [8, 4, 2])
-    assert choice.entry == "matmul" and choice.matched_by == "signature"
+    assert choice.entry == "matmul" and choice.matched_by == "structure"
+    assert choice.dyn_consts == [8, 4, 2]
 
 
 def test_unsupported_function_raises():
@@ -189,7 +191,7 @@ fn twice<n: usize>(x: f32[n]) -> f32[n] {
     with pytest.raises(UnsupportedError):
         P.select_kernel(mod, "twice", [100])
     with pytest.raises(KeyError):
-        P.select_kernel(mod, "nope")
+        P.select_kernel(mod, "nope", [1])
 
 
 def test_plans_of_every_golden_fixture_program():
@@ -223,7 +225,7 @@ def test_execute_module_runs_the_selected_kernel(jb, oracle):
     mod = _module(MATMUL.replace("matmul", "mm"), "forkify(*); infer-attributes(*); gpu(mm);")
     a, b = W.matmul_inputs(96, 64, 80, seed=5)
     c, choice = P.execute_module(mod, "mm", [96, 64, 80], [a, b])
-    assert choice.entry == "matmul" and choice.matched_by == "signature"
+    assert choice.entry == "matmul" and choice.matched_by == "structure"
     ref = oracle.matmul(a, b)
     u = 2.0 ** -24
     gamma = 64 * u / (1 - 64 * u)
