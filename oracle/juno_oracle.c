@@ -433,9 +433,34 @@ EXPORT float jo_srad_q0sqr(int64_t N, const float *J) {
   return (float)(var / (mean * mean));
 }
 
+/* q0^2 with Rodinia srad_v1's own arithmetic: sequential f32 sums in row-
+ * major order, f32 mean/variance (the reference fold order, oracle.py:
+ * 288-304).  Kept to measure the f64 contract against. */
+EXPORT float jo_srad_q0sqr_f32(int64_t N, const float *J) {
+  float sum = 0.0f, sum2 = 0.0f;
+  for (int64_t k = 0; k < N; k++) {
+    const float t = J[k];
+    sum = sum + t;
+    sum2 = sum2 + t * t;
+  }
+  const float mean = sum / (float)N;
+  const float var = (sum2 / (float)N) - mean * mean;
+  return var / (mean * mean);
+}
+
+EXPORT void jo_srad_f32_acc(int64_t rows, int64_t cols, int64_t niter,
+                            float lambda, const float *image, float *out,
+                            float *q0sqr_o, int acc64);
+
 EXPORT void jo_srad_f32(int64_t rows, int64_t cols, int64_t niter,
                         float lambda, const float *image, float *out,
                         float *q0sqr_o) {
+  jo_srad_f32_acc(rows, cols, niter, lambda, image, out, q0sqr_o, 1);
+}
+
+EXPORT void jo_srad_f32_acc(int64_t rows, int64_t cols, int64_t niter,
+                            float lambda, const float *image, float *out,
+                            float *q0sqr_o, int acc64) {
   const int64_t N = rows * cols;
   float *J = (float *)malloc(N * sizeof(float));
   float *c = (float *)malloc(N * sizeof(float));
@@ -446,7 +471,7 @@ EXPORT void jo_srad_f32(int64_t rows, int64_t cols, int64_t niter,
 #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < N; k++) J[k] = exp_ref(image[k] / 255.0f);
   for (int64_t it = 0; it < niter; it++) {
-    const float q0sqr = jo_srad_q0sqr(N, J);
+    const float q0sqr = acc64 ? jo_srad_q0sqr(N, J) : jo_srad_q0sqr_f32(N, J);
     if (q0sqr_o) q0sqr_o[it] = q0sqr;
     jo_srad_iter(rows, cols, q0sqr, lambda, J, c, dN, dS, dW, dE);
   }

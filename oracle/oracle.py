@@ -148,13 +148,15 @@ def cava(raw_batch, tstw, ctrl, wts, coefs, tmap) -> np.ndarray:
 
 
 # -- SRAD -----------------------------------------------------------------------
-def srad(image, niter: int, lam: float, return_q0: bool = False):
+def srad(image, niter: int, lam: float, return_q0: bool = False, acc64: bool = True):
+    """acc64: q0^2 from f64 sums rounded once (the GPU contract); False:
+    Rodinia's sequential f32 sums."""
     img = _f32(image)
     rows, cols = img.shape
     out = np.empty_like(img)
     q0 = np.zeros(max(int(niter), 1), np.float32)
-    lib().jo_srad_f32(_i64(rows), _i64(cols), _i64(niter), ctypes.c_float(lam),
-                      _p(img, _f32p), _p(out, _f32p), _p(q0, _f32p))
+    lib().jo_srad_f32_acc(_i64(rows), _i64(cols), _i64(niter), ctypes.c_float(lam),
+                          _p(img, _f32p), _p(out, _f32p), _p(q0, _f32p), ctypes.c_int(1 if acc64 else 0))
     return (out, q0[:niter]) if return_q0 else out
 
 

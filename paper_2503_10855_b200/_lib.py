@@ -37,10 +37,12 @@ SIGNATURES = {
                            _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_cava_u8": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_srad_f32": [_u64, _u64, _u64, _f32, _vp, _vp, _vp, _vp],
+    "jb_srad_exact_f32": [_u64, _u64, _u64, _f32, _vp, _vp, _vp, _vp],
     "jb_srad_extract_f32": [_u64, _vp, _vp, _vp, ctypes.c_int, _vp],
-    "jb_srad_slab_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, _vp, ctypes.c_int, _vp],
+    "jb_srad_slab_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, _vp, ctypes.c_int, ctypes.c_int, _vp],
     "jb_srad_q0_f32": [_vp, _u64, _vp, _vp],
-    "jb_srad_slab_p2p_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, ctypes.c_int, _vp, _vp],
+    "jb_srad_slab_p2p_step_f32": [_u64, _u64, _u64, _u64, _vp, _vp, _vp, _f32, ctypes.c_int, ctypes.c_int, _vp,
+                                  _vp],
     "jb_p2p_alloc": [_u64, ctypes.POINTER(_vp)],
     "jb_p2p_free": [_vp],
     "jb_ipc_handle": [_vp, _vp],

@@ -410,8 +410,11 @@ def cava(input, tstw, ctrl_pts, weights, coefs, tonemap):
 
 
 # ------------------------------------------------------------------------ srad
-def srad(niter, lam, image, return_q0sqr: bool = False):
-    """srad<rows,cols>(niter, lambda, image f32[rows,cols]) -> f32[rows,cols]."""
+def srad(niter, lam, image, return_q0sqr: bool = False, exact: bool = False):
+    """srad<rows,cols>(niter, lambda, image f32[rows,cols]) -> f32[rows,cols].
+
+    Default: tolerance mode (rel 1e-4 of the oracle after niter, DESIGN.md
+    §srad).  ``exact=True``: the oracle's arithmetic op for op."""
     niter = _scalar(niter, int)
     if niter < 0:
         raise _err(DynConstError, f"srad: niter must be >= 0 (got {niter})")
@@ -422,8 +425,8 @@ def srad(niter, lam, image, return_q0sqr: bool = False):
     out = c.empty((rows, cols), np.float32)
     q0 = c.empty((max(niter, 1),), np.float32)
     with c.on_device():
-        _check(_lib.load().jb_srad_f32(rows, cols, niter, _scalar(lam), _ptr(dimg), _ptr(out), _ptr(q0), c.s),
-               "srad")
+        fn = _lib.load().jb_srad_exact_f32 if exact else _lib.load().jb_srad_f32
+        _check(fn(rows, cols, niter, _scalar(lam), _ptr(dimg), _ptr(out), _ptr(q0), c.s), "srad")
     if return_q0sqr:
         return c.out(out), c.out(q0[:niter])
     return c.out(out)
@@ -494,11 +497,13 @@ def bfs(starting, no_of_edges, edges, source):
 
 
 # -------------------------------------------------------------------- backprop
-def backprop(input_vals, input_weights, hidden_weights, target, input_prev_weights, hidden_prev_weights):
+def backprop(input_vals, input_weights, hidden_weights, target, input_prev_weights, hidden_prev_weights,
+             return_layers: bool = False):
     """One Rodinia bpnn_train step (layerforward x2, output/hidden error,
     adjust_weights x2).  Returns (out_err, hid_err, input_weights,
     hidden_weights, input_prev_weights, hidden_prev_weights) -- fresh arrays
-    (value semantics; the inputs are not mutated)."""
+    (value semantics; the inputs are not mutated) -- plus (hidden, output)
+    unit values when ``return_layers``."""
     n_in1, n_hid1 = _shape(input_weights)
     n_hid1b, n_out1 = _shape(hidden_weights)
     _need(n_hid1 == n_hid1b, "backprop: weight shapes disagree on the hidden layer")
@@ -521,7 +526,8 @@ def backprop(input_vals, input_weights, hidden_weights, target, input_prev_weigh
                                            _ptr(dt), _ptr(dipw), _ptr(dhpw), _ptr(hidden), _ptr(output),
                                            _ptr(errs), c.s), "backprop")
     e = c.out(errs)
-    return (e[0], e[1], c.out(diw), c.out(dhw), c.out(dipw), c.out(dhpw))
+    res = (e[0], e[1], c.out(diw), c.out(dhw), c.out(dipw), c.out(dhpw))
+    return res + (c.out(hidden), c.out(output)) if return_layers else res
 
 
 # --------------------------------------------------------- oracle_execute mirror

@@ -319,6 +319,9 @@ constexpr int SW = 124, SH = 32, SWARPS = 8;
 #ifndef SRAD_MINB
 #define SRAD_MINB 2
 #endif
+#ifndef SRAD_TOL_MINB
+#define SRAD_TOL_MINB 3
+#endif
 
 struct StripCtx {
   const float *src;
@@ -690,6 +693,166 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, const PeerRows pr, 
   return __all_sync(FULL, mn >= 0.00390625f && mx <= 256.0f && mnc >= 8.6736174e-19f);  // c >= 2^-60
 }
 
+// ---- tolerance mode (the default entry): the oracle's
+// coefficient rewritten with the 1/Jc factors cancelled,
+//   qsqr = num/den^2 = N/D^2,  N = G2num/2 - Ls^2/16,  D = Jc + Ls/4
+//   (G2num = dN^2+dS^2+dW^2+dE^2, Ls = dN+dS+dW+dE),
+//   c = 1/(1 + (qsqr - q0)/q0den) = D^2 / (D^2 + (N - q0 D^2)/q0den),
+// so a pixel costs ONE approximate reciprocal (MUFU.RCP) instead of four
+// IEEE divisions, and every multiply-add is one FFMA2 for a pixel pair.
+// Where the final denominator cancels (Y < D^2/64, the only place the
+// rewrite can lose more than a few ulps) or the result is not finite, the
+// pair is recomputed with the exact coefficient.  Result: c within ~1e-6
+// relative of the oracle's, J' within ql*|D| of that; the test contract is
+// rel 1e-4 after the full iteration count.
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 rcp2_approx(f2 b) { return pk2(rcp_approx(lo2(b)), rcp_approx(hi2(b))); }
+
+struct TolK {
+  f2 n2q0;   // -2 q0
+  f2 hiq;    // 0.5 / q0den
+  f2 ql;
+};
+
+// c for a pixel pair (unclamped); sets bad when the pair needs the exact redo
+__device__ __forceinline__ f2 coef2_tol(f2 Jc, const PxPair &d, const TolK &t, bool &bad) {
+  const f2 G2num = fma2(d.e, d.e, fma2(d.w, d.w, fma2(d.s, d.s, mul2(d.n, d.n))));
+  const f2 Ls = add2(add2(add2(d.n, d.s), d.w), d.e);
+  const f2 D = fma2(Ls, bc2(0.25f), Jc);
+  const f2 D2 = mul2(D, D);
+  const f2 N2 = fma2(mul2(Ls, Ls), bc2(-0.125f), G2num);   // 2N
+  const f2 X = fma2(D2, t.n2q0, N2);                        // 2N - 2 q0 D^2
+  const f2 Y = fma2(X, t.hiq, D2);                          // D^2 + (N - q0 D^2)/q0den
+  const f2 c = mul2(D2, rcp2_approx(Y));
+  const f2 g = fma2(D2, bc2(-0.015625f), Y);                // Y - D^2/64
+  const float c0 = lo2(c), c1 = hi2(c);
+  bad = bad | (lo2(g) < 0.0f) | (hi2(g) < 0.0f) | !(fabsf(c0) <= 3.0e38f) | !(fabsf(c1) <= 3.0e38f);
+  return c;
+}
+
+template <bool COMPRESS>
+__device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, RowRing &R, int x0, int y0, int y1,
+                                          double &s, double &s2) {
+  const int lane = threadIdx.x & 31;
+  const int cols = k.cols;
+  const int xl = x0 + 4 * lane;
+  const int xb = xl < cols ? xl : cols - 4;
+  const bool out_lane = lane < 31 && xl < cols;
+  const bool east_edge = xl + 4 >= cols;
+  const int xw = x0 > 0 ? x0 - 1 : 0;
+  const unsigned FULL = 0xffffffffu;
+  TolK t;
+  t.n2q0 = bc2(-2.0f * k.q0);
+  t.hiq = bc2(0.5f / k.q0den);
+  t.ql = bc2(k.ql);
+  const size_t cs = (size_t)cols;
+  const int nrow = y1 - y0 + 3;                                     // rows y0-1 .. y1+1
+  const float *gj = k.src + (size_t)(y0 - 1) * cs + xb;
+  const float *gw = k.src + (size_t)(y0 - 1) * cs + xw;
+  float *po = k.dst + (size_t)(y0 - k.row_lo) * cs + xl;
+  int issued = 0;
+  auto request = [&]() {
+    if (issued < nrow) {
+      const int sl = issued % RING;
+      cp_async16(&R.v[sl][lane], gj);
+      if (lane == 0) cp_async4(&R.w[sl][0], gw);
+      gj += cs;
+      gw += cs;
+    }
+    issued++;
+    cp_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < PD; i++) request();
+  PxPair DA[2], DB[2];
+  f2 CA[2], CB[2];
+  f2 as = 0ull, as2 = 0ull;  // f32 pair partials of sum(J'), sum(J'^2), flushed to f64 every 2 rows
+
+  auto step = [&](int i, bool upd, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
+                  f2 (&ccur)[2]) {
+    request();
+    cp_wait<PD - 2>();
+    const float4 Jm = R.v[(i - 1) % RING][lane], J0 = R.v[i % RING][lane], Jp = R.v[(i + 1) % RING][lane];
+    const float w0 = lane == 0 ? R.w[i % RING][0] : J0.x;
+    float W = __shfl_up_sync(FULL, J0.w, 1);
+    float E = __shfl_down_sync(FULL, J0.x, 1);
+    if (lane == 0) W = w0;
+    if (east_edge) E = J0.w;
+    const f2 c01 = pk2(J0.x, J0.y), c23 = pk2(J0.z, J0.w);
+    dcur[0].n = sub2z(pk2(Jm.x, Jm.y), c01);
+    dcur[1].n = sub2z(pk2(Jm.z, Jm.w), c23);
+    dcur[0].s = sub2z(pk2(Jp.x, Jp.y), c01);
+    dcur[1].s = sub2z(pk2(Jp.z, Jp.w), c23);
+    dcur[0].w = sub2z(pk2(W, J0.x), c01);
+    dcur[1].w = sub2z(pk2(J0.y, J0.z), c23);
+    dcur[0].e = sub2z(pk2(J0.y, J0.z), c01);
+    dcur[1].e = sub2z(pk2(J0.w, E), c23);
+    bool bad = false;
+    const f2 k01 = coef2_tol(c01, dcur[0], t, bad);
+    const f2 k23 = coef2_tol(c23, dcur[1], t, bad);
+    float c[4] = {fminf(fmaxf(lo2(k01), 0.0f), 1.0f), fminf(fmaxf(hi2(k01), 0.0f), 1.0f),
+                  fminf(fmaxf(lo2(k23), 0.0f), 1.0f), fminf(fmaxf(hi2(k23), 0.0f), 1.0f)};
+    if (__any_sync(FULL, bad)) {  // cancellation in the rewritten denominator, or non-finite data
+      const float jc[4] = {J0.x, J0.y, J0.z, J0.w};
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const PxPair &d = dcur[q >> 1];
+        const float dn = (q & 1) ? hi2(d.n) : lo2(d.n), ds = (q & 1) ? hi2(d.s) : lo2(d.s);
+        const float dw = (q & 1) ? hi2(d.w) : lo2(d.w), de = (q & 1) ? hi2(d.e) : lo2(d.e);
+        c[q] = coef_exact(jc[q], dn, ds, dw, de, k.q0, k.q0den);
+      }
+    }
+    ccur[0] = pk2(c[0], c[1]);
+    ccur[1] = pk2(c[2], c[3]);
+    if (upd) {
+      float cE3 = __shfl_down_sync(FULL, lo2(cprev[0]), 1);
+      if (east_edge) cE3 = hi2(cprev[1]);
+      const f2 cE01 = pk2(hi2(cprev[0]), lo2(cprev[1])), cE23 = pk2(hi2(cprev[1]), cE3);
+      // D = cN dN + cS dS + cN dW + cE dE of row r-1; J' = J + ql D
+      const f2 D01 = fma2(cE01, dprev[0].e, fma2(cprev[0], dprev[0].w,
+                                                 fma2(ccur[0], dprev[0].s, mul2(cprev[0], dprev[0].n))));
+      const f2 D23 = fma2(cE23, dprev[1].e, fma2(cprev[1], dprev[1].w,
+                                                 fma2(ccur[1], dprev[1].s, mul2(cprev[1], dprev[1].n))));
+      const f2 o01 = fma2(t.ql, D01, pk2(Jm.x, Jm.y));
+      const f2 o23 = fma2(t.ql, D23, pk2(Jm.z, Jm.w));
+      if (out_lane) {
+        if (COMPRESS) {
+          *reinterpret_cast<float4 *>(po) =
+              make_float4(mul_rn(log_ref(lo2(o01)), 255.0f), mul_rn(log_ref(hi2(o01)), 255.0f),
+                          mul_rn(log_ref(lo2(o23)), 255.0f), mul_rn(log_ref(hi2(o23)), 255.0f));
+        } else {
+          const float4 ov = make_float4(lo2(o01), hi2(o01), lo2(o23), hi2(o23));
+          if (pr.pn || pr.ps) put_row(k, pr, (int)((po - k.dst) / cs), xl, ov);
+          else *reinterpret_cast<float4 *>(po) = ov;
+          as = add2(as, add2(o01, o23));
+          as2 = fma2(o23, o23, fma2(o01, o01, as2));
+        }
+      }
+      po += cs;
+    }
+  };
+  auto flush = [&]() {
+    s += (double)lo2(as) + (double)hi2(as);
+    s2 += (double)lo2(as2) + (double)hi2(as2);
+    as = 0ull;
+    as2 = 0ull;
+  };
+
+  step(1, false, DB, DA, CB, CA);
+  for (int i = 2; i < nrow - 1; i += 2) {
+    step(i, true, DA, DB, CA, CB);
+    if (i + 1 >= nrow - 1) break;
+    step(i + 1, true, DB, DA, CB, CA);
+    if (!COMPRESS) flush();
+  }
+  if (!COMPRESS) flush();
+  cp_wait<0>();
+}
+
 struct StripRes {
   double s, s2;
   bool ok;
@@ -708,8 +871,8 @@ __device__ __noinline__ StripRes strip_exact(const StripCtx k, const PeerRows pr
 
 // P2P: the fused multi-GPU step (peer halo stores, mailbox q0); the
 // single-GPU instantiation compiles that code out (register pressure)
-template <bool P2P>
-__global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args a) {
+template <bool P2P, bool TOL>
+__global__ void __launch_bounds__(SWARPS * 32, TOL ? SRAD_TOL_MINB : SRAD_MINB) srad_strip_kernel(Args a) {
   const int warp = threadIdx.x >> 5;
   StripCtx k;
   k.src = a.src; k.dst = a.dst; k.rows = a.rows; k.cols = a.cols;
@@ -734,8 +897,14 @@ __global__ void __launch_bounds__(SWARPS * 32, SRAD_MINB) srad_strip_kernel(Args
     StripRes res{0.0, 0.0, false};
     if (q0ok) {
       if (y0 >= 1 && y1 + 1 <= a.rows - 1 && y1 - y0 == SH) {  // interior strip
-        res.ok = a.compress ? strip_fast<true>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2)
-                            : strip_fast<false>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2);
+        if (TOL) {
+          if (a.compress) strip_tol<true>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2);
+          else strip_tol<false>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2);
+          res.ok = true;
+        } else {
+          res.ok = a.compress ? strip_fast<true>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2)
+                              : strip_fast<false>(k, pr, rings[warp], x0, y0, y1, res.s, res.s2);
+        }
       } else {
         res = strip_edge(k, pr, x0, y0, y1);
       }
@@ -763,18 +932,33 @@ using namespace jb::srad;
 static bool strip_ok(uint64_t cols, const void *p0, const void *p1) {
   return cols % 4 == 0 && cols >= 4 && ((uintptr_t)p0 % 16) == 0 && ((uintptr_t)p1 % 16) == 0;
 }
+template <bool P2P, bool TOL>
 static int strip_grid() {
   static int per_sm = 0;
   if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_strip_kernel<false>, SWARPS * 32, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srad_strip_kernel<P2P, TOL>, SWARPS * 32, 0) !=
+            cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
   }
   return sm_count() * per_sm;
 }
+static int strip_grid_for(bool p2p, bool tol) {
+  return p2p ? (tol ? strip_grid<true, true>() : strip_grid<true, false>())
+             : (tol ? strip_grid<false, true>() : strip_grid<false, false>());
+}
+static void launch_strips(bool p2p, bool tol, int grid, cudaStream_t s, const Args &a) {
+  if (p2p) {
+    if (tol) srad_strip_kernel<true, true><<<grid, SWARPS * 32, 0, s>>>(a);
+    else srad_strip_kernel<true, false><<<grid, SWARPS * 32, 0, s>>>(a);
+  } else {
+    if (tol) srad_strip_kernel<false, true><<<grid, SWARPS * 32, 0, s>>>(a);
+    else srad_strip_kernel<false, false><<<grid, SWARPS * 32, 0, s>>>(a);
+  }
+}
 
-extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, float lambda, const float *image,
-                                 float *out, float *q0sqr, void *stream) {
+static jb_status srad_run(uint64_t rows, uint64_t cols, uint64_t niter, float lambda, const float *image,
+                          float *out, float *q0sqr, void *stream, bool tol) {
   JB_REQUIRE(rows >= 1 && cols >= 1, "srad: rows and cols must be >= 1");
   JB_REQUIRE(rows * cols < (1ull << 40) && rows < (1u << 30) && cols < (1u << 30), "srad: image too large");
   JB_REQUIRE(niter < (1u << 30), "srad: niter too large");
@@ -789,7 +973,7 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
   const int grid = tiles < sm_count() * per_sm ? tiles : sm_count() * per_sm;
   const int grid_x = sm_count() * 8;
   const bool strips = strip_ok(cols, image, out);
-  const int sgrid = strips ? strip_grid() : 0;
+  const int sgrid = strips ? strip_grid_for(false, tol) : 0;
   int gmax = grid > grid_x ? grid : grid_x;
   if (sgrid > gmax) gmax = sgrid;
   // scratch: J ping-pong (2 images), q0 per iteration, partials, ticket
@@ -825,7 +1009,7 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
     a.q0_next = q0 + it + 1;
     a.compress = last;
     void *tok = prof_begin("srad_iter", s);
-    if (strips) srad_strip_kernel<false><<<sgrid, SWARPS * 32, 0, s>>>(a);
+    if (strips) launch_strips(false, tol, sgrid, s, a);
     else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
     prof_end(tok, s);
     JB_LAUNCHED("srad_iter");
@@ -835,6 +1019,19 @@ extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, f
     JB_LAUNCHED("srad_q0_copy");
   }
   return JB_OK;
+}
+
+// default entry: tolerance mode (one approximate reciprocal per pixel,
+// contracted FMAs; DESIGN.md §srad states the contract)
+extern "C" jb_status jb_srad_f32(uint64_t rows, uint64_t cols, uint64_t niter, float lambda, const float *image,
+                                 float *out, float *q0sqr, void *stream) {
+  return srad_run(rows, cols, niter, lambda, image, out, q0sqr, stream, true);
+}
+
+// bit-exact entry: the oracle's arithmetic op for op
+extern "C" jb_status jb_srad_exact_f32(uint64_t rows, uint64_t cols, uint64_t niter, float lambda,
+                                       const float *image, float *out, float *q0sqr, void *stream) {
+  return srad_run(rows, cols, niter, lambda, image, out, q0sqr, stream, false);
 }
 
 // ------------------------------------------------------------ slab entries
@@ -874,7 +1071,7 @@ extern "C" jb_status jb_srad_extract_f32(uint64_t n, const float *image, float *
 
 extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uint64_t own_lo, uint64_t own_hi,
                                            const float *J_ext, float *out_own, const float *q0, float lambda,
-                                           double *sums, int compress, void *stream) {
+                                           double *sums, int compress, int exact, void *stream) {
   JB_REQUIRE(rows_ext >= 1 && cols >= 1 && own_lo < own_hi && own_hi <= rows_ext, "srad_slab: bad slab");
   JB_REQUIRE(J_ext && out_own && q0, "srad_slab: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -885,7 +1082,7 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
   if (per_sm < 1) per_sm = 1;
   const int grid = tiles < sm_count() * per_sm ? tiles : sm_count() * per_sm;
   const bool strips = strip_ok(cols, J_ext, out_own);
-  const int sgrid = strips ? strip_grid() : 0;
+  const int sgrid = strips ? strip_grid_for(false, !exact) : 0;
   const size_t pb = (((grid > sgrid ? grid : sgrid) * sizeof(Stats) + 255) / 256) * 256;
   char *ws = (char *)workspace(pb + 256, s);
   if (!ws) return JB_ECUDA;
@@ -899,7 +1096,7 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
   a.sums_out = sums;
   JB_CHECK_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned), s));
   void *tok = prof_begin("srad_iter", s);
-  if (strips) srad_strip_kernel<false><<<sgrid, SWARPS * 32, 0, s>>>(a);
+  if (strips) launch_strips(false, !exact, sgrid, s, a);
   else srad_iter_kernel<<<grid, THREADS, 0, s>>>(a);
   prof_end(tok, s);
   JB_LAUNCHED("srad_slab_step");
@@ -913,7 +1110,7 @@ extern "C" jb_status jb_srad_slab_step_f32(uint64_t rows_ext, uint64_t cols, uin
 // host round trip per iteration.
 extern "C" jb_status jb_srad_slab_p2p_step_f32(uint64_t rows_ext, uint64_t cols, uint64_t own_lo, uint64_t own_hi,
                                                const float *J_ext, float *out_own, const float *q0, float lambda,
-                                               int compress, const jb_srad_p2p *p2p, void *stream) {
+                                               int compress, int exact, const jb_srad_p2p *p2p, void *stream) {
   JB_REQUIRE(rows_ext >= 1 && cols >= 1 && own_lo < own_hi && own_hi <= rows_ext, "srad_p2p: bad slab");
   JB_REQUIRE(p2p && J_ext && out_own && p2p->mbox && p2p->flag, "srad_p2p: null pointer");
   JB_REQUIRE(p2p->world >= 1 && p2p->world <= kMaxRanks && p2p->rank >= 0 && p2p->rank < p2p->world,
@@ -922,7 +1119,7 @@ extern "C" jb_status jb_srad_slab_p2p_step_f32(uint64_t rows_ext, uint64_t cols,
   JB_REQUIRE(strip_ok(cols, J_ext, out_own), "srad_p2p: rows must be float4-aligned (cols %% 4 == 0)");
   for (int r = 0; r < p2p->world; r++) JB_REQUIRE(p2p->peer_mbox[r] && p2p->peer_flag[r], "srad_p2p: null peer");
   cudaStream_t s = (cudaStream_t)stream;
-  const int sgrid = p2p->grid > 0 ? p2p->grid : strip_grid();
+  const int sgrid = p2p->grid > 0 ? p2p->grid : strip_grid_for(true, !exact);
   const size_t pb = ((sgrid * sizeof(Stats) + 255) / 256) * 256;
   char *ws = (char *)workspace(pb + 256, s);
   if (!ws) return JB_ECUDA;
@@ -944,7 +1141,7 @@ extern "C" jb_status jb_srad_slab_p2p_step_f32(uint64_t rows_ext, uint64_t cols,
   a.world = p2p->world; a.rank = p2p->rank; a.iter = p2p->iter; a.flag_base = p2p->flag_base;
   a.npx_global = (long long)p2p->npx_global;
   void *tok = prof_begin("srad_iter", s);
-  srad_strip_kernel<true><<<sgrid, SWARPS * 32, 0, s>>>(a);
+  launch_strips(true, !exact, sgrid, s, a);
   prof_end(tok, s);
   JB_LAUNCHED("srad_p2p_step");
   return JB_OK;

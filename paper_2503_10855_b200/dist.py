@@ -256,7 +256,8 @@ class SradP2PSlabs:
             self.base = None
 
 
-def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs, backend=None):
+def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs, backend=None,
+                         exact: bool = False):
     """Row-slab SRAD where each iteration is ONE kernel per rank: it stores
     the slab's boundary rows into the neighbours' next slabs and its sums into
     every rank's mailbox over peer memory, and the next iteration's kernel
@@ -301,7 +302,7 @@ def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs,
         a.peer_south = slabs.ext(nxt, rank + 1) if rank < w - 1 else None
         rc = lib.jb_srad_slab_p2p_step_f32(n_ext, cols, lo, hi, slabs.ext(cur), slabs.ext(nxt) + lo * cols * 4,
                                             q0.data_ptr() if it == 0 else None, float(lam), int(last),
-                                            ctypes.byref(a), stream)
+                                            int(exact), ctypes.byref(a), stream)
         if rc:
             raise RuntimeError(f"srad_p2p_step: {_lib.last_error()}")
     slabs.epoch += w * niter
@@ -309,12 +310,15 @@ def srad_distributed_p2p(image_own, niter: int, lam: float, slabs: SradP2PSlabs,
 
 
 class CudaSradBackend:
-    """libjunob200 slab kernels on device tensors (NCCL collectives)."""
+    """libjunob200 slab kernels on device tensors (NCCL collectives).
+    exact=True: the bit-exact slab step (else the tolerance mode of
+    jb_srad_f32)."""
 
-    def __init__(self):
+    def __init__(self, exact: bool = False):
         import torch
         self.torch = torch
         self.lib = _lib.load()
+        self.exact = exact
 
     def _s(self):
         return self.torch.cuda.current_stream().cuda_stream
@@ -342,7 +346,8 @@ class CudaSradBackend:
         sums = t.zeros(2, dtype=t.float64, device=J_ext.device)
         self._chk(self.lib.jb_srad_slab_step_f32(J_ext.shape[0], J_ext.shape[1], own_lo, own_hi,
                                                  J_ext.data_ptr(), out.data_ptr(), q0.data_ptr(), float(lam),
-                                                 sums.data_ptr(), int(compress), self._s()), "srad_slab_step")
+                                                 sums.data_ptr(), int(compress), int(self.exact), self._s()),
+                  "srad_slab_step")
         return out, sums
 
     def q0(self, sums, npx):

@@ -156,3 +156,20 @@ def bp_inputs(n_in=1 << 24, n_hid=16, n_out=1, seed=7):
     ipw = np.zeros_like(iw)
     hpw = np.zeros_like(hw)
     return x, iw, hw, t, ipw, hpw
+
+
+def bp_inputs_unsaturated(n_in=1 << 24, n_hid=16, n_out=1, seed=11):
+    """A parity configuration where every stage is live: input weights
+    U(-1,1)*4/sqrt(n_in) keep the hidden sums O(1) (Rodinia's U[0,1)
+    weights drive them to ~4e6, where squash is exactly 1 and every delta
+    and weight update is 0), and non-zero previous weights exercise the
+    momentum term.  Inputs and target as Rodinia."""
+    rng = np.random.default_rng(seed)
+    x = rng.random(n_in + 1, dtype=np.float32)
+    scale = np.float32(4.0 / np.sqrt(n_in))
+    iw = ((rng.random((n_in + 1, n_hid + 1), dtype=np.float32) * np.float32(2) - np.float32(1)) * scale)
+    hw = rng.random((n_hid + 1, n_out + 1), dtype=np.float32) * np.float32(2) - np.float32(1)
+    t = np.full(n_out + 1, 0.1, np.float32)
+    ipw = (rng.random(iw.shape, dtype=np.float32) - np.float32(0.5)) * np.float32(1e-3)
+    hpw = (rng.random(hw.shape, dtype=np.float32) - np.float32(0.5)) * np.float32(1e-3)
+    return x, iw.astype(np.float32), hw.astype(np.float32), t, ipw.astype(np.float32), hpw.astype(np.float32)

@@ -13,7 +13,8 @@ def test_srad_distributed_world1_matches_oracle(jb, oracle):
     import torch
     from paper_2503_10855_b200 import dist as D
     img = W.srad_image(96, 130, seed=2)
-    out = D.srad_distributed(torch.from_numpy(img).cuda(), 5, 0.5, 96, 130, D.CudaSradBackend()).cpu().numpy()
+    out = D.srad_distributed(torch.from_numpy(img).cuda(), 5, 0.5, 96, 130,
+                             D.CudaSradBackend(exact=True)).cpu().numpy()
     ref = oracle.srad(img, 5, 0.5)
     assert np.count_nonzero(out.view(np.uint32) != ref.view(np.uint32)) <= out.size // 10000
     np.testing.assert_allclose(out, ref, rtol=1e-5)
@@ -25,7 +26,7 @@ def test_srad_emulated_slabs_match_oracle(jb, oracle, nslab):
     from paper_2503_10855_b200 import dist as D
     rows, cols, niter = 70, 150, 4
     img = W.srad_image(rows, cols, seed=4)
-    be = D.CudaSradBackend()
+    be = D.CudaSradBackend(exact=True)
     plans = [D.srad_slab(rows, nslab, r) for r in range(nslab)]
     Js, sums = [], []
     for p in plans:
@@ -105,8 +106,8 @@ def _p2p_rank(rank, world, port, rows, cols, niter, q):
         # a small grid per rank: the two ranks' persistent kernels must be
         # co-resident on the shared GPU (on separate GPUs any grid works)
         slabs = D.SradP2PSlabs(rows, cols, grid=8)
-        out = D.srad_distributed_p2p(own, niter, 0.5, slabs)
-        out2 = D.srad_distributed_p2p(own, niter, 0.5, slabs)  # buffers reused by a second call
+        out = D.srad_distributed_p2p(own, niter, 0.5, slabs, exact=True)
+        out2 = D.srad_distributed_p2p(own, niter, 0.5, slabs, exact=True)  # buffers reused by a second call
         torch.cuda.synchronize()
         dist.barrier()
         slabs.close()

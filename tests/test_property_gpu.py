@@ -87,7 +87,9 @@ def test_matmul_random_shapes_within_bound(jb, oracle, n, m, l, seed):
 @given(rows=st.integers(2, 140), cols=st.integers(2, 260), niter=st.integers(0, 4), seed=st.integers(0, 10**6))
 def test_srad_random_shapes(jb, oracle, rows, cols, niter, seed):
     img = W.srad_image(rows, cols, seed=seed)
-    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True)
+    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True, exact=True)
     ref, rq0 = oracle.srad(img, niter, 0.5, return_q0=True)
     assert np.array_equal(_bits(np.asarray(q0)), _bits(np.asarray(rq0)))
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5)
+    fast = jb.srad(niter, 0.5, img)   # tolerance mode (the default)
+    np.testing.assert_allclose(fast, ref, rtol=1e-4, atol=1e-4)

@@ -29,9 +29,9 @@ def _exact(got, ref):
 # ------------------------------------------------------------------ SRAD
 @pytest.mark.parametrize("shape,niter", [((64, 64), 3), ((100, 130), 5), ((257, 129), 4), ((1, 1), 2),
                                          ((33, 260), 1), ((48, 48), 0), ((512, 512), 10), ((700, 1000), 3)])
-def test_srad_matches_oracle(jb, oracle, shape, niter):
+def test_srad_exact_matches_oracle(jb, oracle, shape, niter):
     img = W.srad_image(*shape, seed=shape[0])
-    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True)
+    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True, exact=True)
     ref, rq0 = oracle.srad(img, niter, 0.5, return_q0=True)
     if shape == (1, 1):  # zero variance: q0 = 0/0 on both sides
         assert np.isnan(q0).all() == np.isnan(rq0).all()
@@ -41,6 +41,34 @@ def test_srad_matches_oracle(jb, oracle, shape, niter):
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5, equal_nan=True)
     # observed: bit-identical
     assert np.count_nonzero(_bits(out) != _bits(ref)) <= out.size // 10000
+
+
+SRAD_TOL = 1e-4   # the tolerance-mode contract: rel, after niter
+
+
+@pytest.mark.parametrize("shape,niter", [((64, 64), 3), ((100, 130), 5), ((257, 129), 4), ((1, 1), 2),
+                                         ((33, 260), 1), ((48, 48), 0), ((512, 512), 10), ((700, 1000), 3),
+                                         ((1024, 2048), 30)])
+def test_srad_tolerance_mode_matches_oracle(jb, oracle, shape, niter):
+    img = W.srad_image(*shape, seed=shape[0])
+    out, q0 = jb.srad(niter, 0.5, img, return_q0sqr=True)
+    ref, rq0 = oracle.srad(img, niter, 0.5, return_q0=True)
+    np.testing.assert_allclose(out, ref, rtol=SRAD_TOL, atol=SRAD_TOL, equal_nan=True)
+    np.testing.assert_allclose(q0, rq0, rtol=SRAD_TOL, equal_nan=True)
+
+
+def test_srad_tolerance_mode_near_singular_coefficients(jb, oracle):
+    """Images whose diffusion coefficients sit on the clamp's singularity
+    (1 + (qsqr - q0)/q0den -> 0) and flat regions (zero differences): the
+    tolerance kernel must hand those pixels to the exact coefficient."""
+    rng = np.random.default_rng(5)
+    img = np.full((256, 512), 100.0, np.float32)
+    img[::7, ::5] = 255.0
+    img[3::11, 2::3] = 1.0
+    img += (rng.random(img.shape) < 0.01).astype(np.float32) * 50.0
+    out = jb.srad(6, 0.5, img)
+    ref = oracle.srad(img, 6, 0.5)
+    np.testing.assert_allclose(out, ref, rtol=SRAD_TOL, atol=SRAD_TOL)
 
 
 def test_srad_iteration_pinned_to_reference_interpreter(jb, oracle):
