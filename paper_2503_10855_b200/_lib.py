@@ -49,9 +49,10 @@ SIGNATURES = {
     "jb_ipc_open": [_vp, ctypes.POINTER(_vp)],
     "jb_ipc_close": [_vp],
     "jb_euler_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
-    "jb_euler_stage_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "jb_euler_exact_f32": [_u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "jb_euler_stage_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp],
     "jb_euler_stage_p2p_f32": [_u64, _u64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32,
-                               ctypes.c_uint32, _vp],
+                               ctypes.c_uint32, ctypes.c_int, _vp],
     "jb_euler_push_f32": [_vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp],
     "jb_euler_step_factor_f32": [_u64, _vp, _vp, _vp, _vp],
     "jb_euler_flux_f32": [_u64, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -433,9 +433,12 @@ def srad(niter, lam, image, return_q0sqr: bool = False, exact: bool = False):
 
 
 # ----------------------------------------------------------------------- euler
-def euler(iterations, areas, neighbors, normals, ff_variable, variables):
+def euler(iterations, areas, neighbors, normals, ff_variable, variables, exact: bool = False):
     """euler<nelr>(iterations, areas f32[nelr], neighbors i32[4,nelr],
-    normals f32[4,3,nelr], ff_variable f32[5], variables f32[5,nelr]) -> f32[5,nelr]."""
+    normals f32[4,3,nelr], ff_variable f32[5], variables f32[5,nelr]) -> f32[5,nelr].
+
+    Default: tolerance mode (rel 1e-5 per RK stage).
+    ``exact=True``: bit-identical to the oracle."""
     iterations = _scalar(iterations, int)
     if iterations < 0:
         raise _err(DynConstError, "euler: iterations must be >= 0")
@@ -451,8 +454,8 @@ def euler(iterations, areas, neighbors, normals, ff_variable, variables):
     dff = c.dev(ff_variable, np.float32, "ff_variable")
     dv = c.dev(variables, np.float32, "variables", copy=True)  # value semantics
     with c.on_device():
-        _check(_lib.load().jb_euler_f32(nelr, iterations, _ptr(da), _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), c.s),
-               "euler")
+        fn = _lib.load().jb_euler_exact_f32 if exact else _lib.load().jb_euler_f32
+        _check(fn(nelr, iterations, _ptr(da), _ptr(dn), _ptr(dno), _ptr(dff), _ptr(dv), c.s), "euler")
     return c.out(dv)
 
 

@@ -52,6 +52,7 @@ struct Args {
   int row_lo, row_hi; // output rows [row_lo, row_hi) of src (slab mode: the rest is halo)
   float ql;           // 0.25f * lambda
   int compress;       // write log(J')*255 instead of J'
+  int tol;            // tolerance mode (f32 exp/log in extract; the strip kernel is templated)
   double *sums_out;   // slab mode: the last CTA writes (sum, sum2) here instead of q0
   // ---- fused multi-GPU slab step (peer memory over NVLink; dist.py
   // srad_distributed_p2p).  Null mbox: the NCCL-driven slab mode above.
@@ -161,9 +162,11 @@ __global__ void __launch_bounds__(THREADS) srad_extract_kernel(Args a) {
   double s = 0.0, s2 = 0.0;
   const long long n = (long long)a.rows * a.cols;
   for (long long i = blockIdx.x * (long long)THREADS + threadIdx.x; i < n; i += (long long)gridDim.x * THREADS) {
-    const float j = exp_ref(div_rn(__ldg(a.src + i), 255.0f));
+    // tolerance mode: f32 expf/logf (<= 2 ulp); exact mode: double, rounded once
+    const float x = div_rn(__ldg(a.src + i), 255.0f);
+    const float j = a.tol ? expf(x) : exp_ref(x);
     if (a.compress) {
-      a.dst[i] = mul_rn(log_ref(j), 255.0f);  // niter == 0
+      a.dst[i] = mul_rn(a.tol ? logf(j) : log_ref(j), 255.0f);  // niter == 0
     } else {
       a.dst[i] = j;
       s += (double)j;
@@ -719,6 +722,8 @@ struct TolK {
 };
 
 // c for a pixel pair (unclamped); sets bad when the pair needs the exact redo
+// (Y < D^2/64: the rewritten denominator cancels; NaN data propagates the
+// same way on both paths)
 __device__ __forceinline__ f2 coef2_tol(f2 Jc, const PxPair &d, const TolK &t, bool &bad) {
   const f2 G2num = fma2(d.e, d.e, fma2(d.w, d.w, fma2(d.s, d.s, mul2(d.n, d.n))));
   const f2 Ls = add2(add2(add2(d.n, d.s), d.w), d.e);
@@ -729,14 +734,35 @@ __device__ __forceinline__ f2 coef2_tol(f2 Jc, const PxPair &d, const TolK &t, b
   const f2 Y = fma2(X, t.hiq, D2);                          // D^2 + (N - q0 D^2)/q0den
   const f2 c = mul2(D2, rcp2_approx(Y));
   const f2 g = fma2(D2, bc2(-0.015625f), Y);                // Y - D^2/64
-  const float c0 = lo2(c), c1 = hi2(c);
-  bad = bad | (lo2(g) < 0.0f) | (hi2(g) < 0.0f) | !(fabsf(c0) <= 3.0e38f) | !(fabsf(c1) <= 3.0e38f);
+  bad = bad | (fminf(lo2(g), hi2(g)) < 0.0f);
   return c;
 }
 
+__device__ __forceinline__ float logc(float x) { return mul_rn(logf(x), 255.0f); }  // tolerance compress
+
+// scalar coefficient (tolerance mode), see coef2_tol
+__device__ __forceinline__ float coef_tol(float Jc, float dn, float ds, float dw, float de, float n2q0, float hiq,
+                                          bool &bad) {
+  const float G2num = __fmaf_rn(de, de, __fmaf_rn(dw, dw, __fmaf_rn(ds, ds, dn * dn)));
+  const float Ls = ((dn + ds) + dw) + de;
+  const float D = __fmaf_rn(Ls, 0.25f, Jc);
+  const float D2 = D * D;
+  const float N2 = __fmaf_rn(Ls * Ls, -0.125f, G2num);
+  const float X = __fmaf_rn(D2, n2q0, N2);
+  const float Y = __fmaf_rn(X, hiq, D2);
+  bad = bad | (__fmaf_rn(D2, -0.015625f, Y) < 0.0f);
+  return __saturatef(D2 * rcp_approx(Y));
+}
+
+// One interior strip in tolerance mode (scalar FFMA code: every value lives
+// in whatever register suits it, no pair packing).  The row loop is unrolled
+// over the ring period (RING = 8 steps), so every ring slot is a
+// compile-time constant; the 3-row window rotates by register renaming.
+// SH = 32 rows = 4 ring periods.
 template <bool COMPRESS>
 __device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, RowRing &R, int x0, int y0, int y1,
                                           double &s, double &s2) {
+  static_assert(SH % RING == 0 && RING == 8, "the tolerance strip unrolls whole ring periods");
   const int lane = threadIdx.x & 31;
   const int cols = k.cols;
   const int xl = x0 + 4 * lane;
@@ -745,21 +771,17 @@ __device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, R
   const bool east_edge = xl + 4 >= cols;
   const int xw = x0 > 0 ? x0 - 1 : 0;
   const unsigned FULL = 0xffffffffu;
-  TolK t;
-  t.n2q0 = bc2(-2.0f * k.q0);
-  t.hiq = bc2(0.5f / k.q0den);
-  t.ql = bc2(k.ql);
+  const float n2q0 = -2.0f * k.q0, hiq = 0.5f / k.q0den, ql = k.ql;
   const size_t cs = (size_t)cols;
-  const int nrow = y1 - y0 + 3;                                     // rows y0-1 .. y1+1
+  const int nrow = y1 - y0 + 3;                                     // rows y0-1 .. y1+1 (= SH + 2)
   const float *gj = k.src + (size_t)(y0 - 1) * cs + xb;
   const float *gw = k.src + (size_t)(y0 - 1) * cs + xw;
   float *po = k.dst + (size_t)(y0 - k.row_lo) * cs + xl;
   int issued = 0;
-  auto request = [&]() {
+  auto request = [&](int slot) {  // slot == issued % RING, known at compile time at every call site
     if (issued < nrow) {
-      const int sl = issued % RING;
-      cp_async16(&R.v[sl][lane], gj);
-      if (lane == 0) cp_async4(&R.w[sl][0], gw);
+      cp_async16(&R.v[slot][lane], gj);
+      if (lane == 0) cp_async4(&R.w[slot][0], gw);
       gj += cs;
       gw += cs;
     }
@@ -767,89 +789,95 @@ __device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, R
     cp_commit();
   };
 #pragma unroll
-  for (int i = 0; i < PD; i++) request();
-  PxPair DA[2], DB[2];
-  f2 CA[2], CB[2];
-  f2 as = 0ull, as2 = 0ull;  // f32 pair partials of sum(J'), sum(J'^2), flushed to f64 every 2 rows
+  for (int i = 0; i < PD; i++) request(i);
+  cp_wait<PD - 2>();  // rows 0, 1
+  float jm[4], j0[4];
+  {
+    const float4 a = R.v[0][lane], b = R.v[1][lane];
+    jm[0] = a.x; jm[1] = a.y; jm[2] = a.z; jm[3] = a.w;
+    j0[0] = b.x; j0[1] = b.y; j0[2] = b.z; j0[3] = b.w;
+  }
+  float w0 = lane == 0 ? R.w[1][0] : 0.0f;
+  float pn[4], ps[4], pw[4], pe[4], pc[4];  // the previous row's differences and coefficients
+  float as = 0.0f, as2 = 0.0f;              // f32 partials of sum(J'), sum(J'^2), flushed every 2 rows
 
-  auto step = [&](int i, bool upd, const PxPair (&dprev)[2], PxPair (&dcur)[2], const f2 (&cprev)[2],
-                  f2 (&ccur)[2]) {
-    request();
-    cp_wait<PD - 2>();
-    const float4 Jm = R.v[(i - 1) % RING][lane], J0 = R.v[i % RING][lane], Jp = R.v[(i + 1) % RING][lane];
-    const float w0 = lane == 0 ? R.w[i % RING][0] : J0.x;
-    float W = __shfl_up_sync(FULL, J0.w, 1);
-    float E = __shfl_down_sync(FULL, J0.x, 1);
+  auto step = [&](const int slot_i, bool upd) {
+    request((slot_i + PD - 1) % RING);  // row i+PD-1
+    cp_wait<PD - 2>();                  // row i+1 has landed
+    const int sp = (slot_i + 1) % RING;
+    const float4 Jp4 = R.v[sp][lane];
+    const float jp[4] = {Jp4.x, Jp4.y, Jp4.z, Jp4.w};
+    const float wp = lane == 0 ? R.w[sp][0] : 0.0f;
+    float W = __shfl_up_sync(FULL, j0[3], 1);
+    float E = __shfl_down_sync(FULL, j0[0], 1);
     if (lane == 0) W = w0;
-    if (east_edge) E = J0.w;
-    const f2 c01 = pk2(J0.x, J0.y), c23 = pk2(J0.z, J0.w);
-    dcur[0].n = sub2z(pk2(Jm.x, Jm.y), c01);
-    dcur[1].n = sub2z(pk2(Jm.z, Jm.w), c23);
-    dcur[0].s = sub2z(pk2(Jp.x, Jp.y), c01);
-    dcur[1].s = sub2z(pk2(Jp.z, Jp.w), c23);
-    dcur[0].w = sub2z(pk2(W, J0.x), c01);
-    dcur[1].w = sub2z(pk2(J0.y, J0.z), c23);
-    dcur[0].e = sub2z(pk2(J0.y, J0.z), c01);
-    dcur[1].e = sub2z(pk2(J0.w, E), c23);
+    if (east_edge) E = j0[3];
+    const float jw[4] = {W, j0[0], j0[1], j0[2]};
+    const float je[4] = {j0[1], j0[2], j0[3], E};
+    float dn[4], ds[4], dw[4], de[4], c[4];
     bool bad = false;
-    const f2 k01 = coef2_tol(c01, dcur[0], t, bad);
-    const f2 k23 = coef2_tol(c23, dcur[1], t, bad);
-    float c[4] = {fminf(fmaxf(lo2(k01), 0.0f), 1.0f), fminf(fmaxf(hi2(k01), 0.0f), 1.0f),
-                  fminf(fmaxf(lo2(k23), 0.0f), 1.0f), fminf(fmaxf(hi2(k23), 0.0f), 1.0f)};
-    if (__any_sync(FULL, bad)) {  // cancellation in the rewritten denominator, or non-finite data
-      const float jc[4] = {J0.x, J0.y, J0.z, J0.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      dn[q] = jm[q] - j0[q];
+      ds[q] = jp[q] - j0[q];
+      dw[q] = jw[q] - j0[q];
+      de[q] = je[q] - j0[q];
+      c[q] = coef_tol(j0[q], dn[q], ds[q], dw[q], de[q], n2q0, hiq, bad);
+    }
+    if (__any_sync(FULL, bad)) {  // cancellation in the rewritten denominator
+#pragma unroll
+      for (int q = 0; q < 4; q++) c[q] = coef_exact(j0[q], dn[q], ds[q], dw[q], de[q], k.q0, k.q0den);
+    }
+    if (upd) {
+      float cE3 = __shfl_down_sync(FULL, pc[0], 1);
+      if (east_edge) cE3 = pc[3];
+      const float cE[4] = {pc[1], pc[2], pc[3], cE3};
+      float o[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const PxPair &d = dcur[q >> 1];
-        const float dn = (q & 1) ? hi2(d.n) : lo2(d.n), ds = (q & 1) ? hi2(d.s) : lo2(d.s);
-        const float dw = (q & 1) ? hi2(d.w) : lo2(d.w), de = (q & 1) ? hi2(d.e) : lo2(d.e);
-        c[q] = coef_exact(jc[q], dn, ds, dw, de, k.q0, k.q0den);
+        // D = cN dN + cS dS + cN dW + cE dE of row i-1; J' = J + ql D
+        const float D = __fmaf_rn(cE[q], pe[q], __fmaf_rn(pc[q], pw[q], __fmaf_rn(c[q], ps[q], pc[q] * pn[q])));
+        o[q] = __fmaf_rn(ql, D, jm[q]);
       }
-    }
-    ccur[0] = pk2(c[0], c[1]);
-    ccur[1] = pk2(c[2], c[3]);
-    if (upd) {
-      float cE3 = __shfl_down_sync(FULL, lo2(cprev[0]), 1);
-      if (east_edge) cE3 = hi2(cprev[1]);
-      const f2 cE01 = pk2(hi2(cprev[0]), lo2(cprev[1])), cE23 = pk2(hi2(cprev[1]), cE3);
-      // D = cN dN + cS dS + cN dW + cE dE of row r-1; J' = J + ql D
-      const f2 D01 = fma2(cE01, dprev[0].e, fma2(cprev[0], dprev[0].w,
-                                                 fma2(ccur[0], dprev[0].s, mul2(cprev[0], dprev[0].n))));
-      const f2 D23 = fma2(cE23, dprev[1].e, fma2(cprev[1], dprev[1].w,
-                                                 fma2(ccur[1], dprev[1].s, mul2(cprev[1], dprev[1].n))));
-      const f2 o01 = fma2(t.ql, D01, pk2(Jm.x, Jm.y));
-      const f2 o23 = fma2(t.ql, D23, pk2(Jm.z, Jm.w));
       if (out_lane) {
         if (COMPRESS) {
-          *reinterpret_cast<float4 *>(po) =
-              make_float4(mul_rn(log_ref(lo2(o01)), 255.0f), mul_rn(log_ref(hi2(o01)), 255.0f),
-                          mul_rn(log_ref(lo2(o23)), 255.0f), mul_rn(log_ref(hi2(o23)), 255.0f));
+          *reinterpret_cast<float4 *>(po) = make_float4(logc(o[0]), logc(o[1]), logc(o[2]), logc(o[3]));
         } else {
-          const float4 ov = make_float4(lo2(o01), hi2(o01), lo2(o23), hi2(o23));
+          const float4 ov = make_float4(o[0], o[1], o[2], o[3]);
           if (pr.pn || pr.ps) put_row(k, pr, (int)((po - k.dst) / cs), xl, ov);
           else *reinterpret_cast<float4 *>(po) = ov;
-          as = add2(as, add2(o01, o23));
-          as2 = fma2(o23, o23, fma2(o01, o01, as2));
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            as += o[q];
+            as2 = __fmaf_rn(o[q], o[q], as2);
+          }
         }
       }
       po += cs;
     }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      pn[q] = dn[q]; ps[q] = ds[q]; pw[q] = dw[q]; pe[q] = de[q]; pc[q] = c[q];
+      jm[q] = j0[q]; j0[q] = jp[q];
+    }
+    w0 = wp;
   };
   auto flush = [&]() {
-    s += (double)lo2(as) + (double)hi2(as);
-    s2 += (double)lo2(as2) + (double)hi2(as2);
-    as = 0ull;
-    as2 = 0ull;
+    s += (double)as;
+    s2 += (double)as2;
+    as = 0.0f;
+    as2 = 0.0f;
   };
 
-  step(1, false, DB, DA, CB, CA);
-  for (int i = 2; i < nrow - 1; i += 2) {
-    step(i, true, DA, DB, CA, CB);
-    if (i + 1 >= nrow - 1) break;
-    step(i + 1, true, DB, DA, CB, CA);
-    if (!COMPRESS) flush();
+  step(1, false);  // c(y0)
+#pragma unroll 1
+  for (int base = 2; base < nrow; base += RING) {  // rows i = base .. base+7 (slots 2..7,0,1)
+#pragma unroll
+    for (int u = 0; u < RING; u++) {
+      step((2 + u) % RING, true);
+      if (!COMPRESS && (u & 1)) flush();
+    }
   }
-  if (!COMPRESS) flush();
   cp_wait<0>();
 }
 
@@ -992,6 +1020,7 @@ static jb_status srad_run(uint64_t rows, uint64_t cols, uint64_t niter, float la
   a.rows = (int)rows; a.cols = (int)cols; a.tiles_x = tiles_x; a.tiles = tiles;
   a.row_lo = 0; a.row_hi = (int)rows; a.sums_out = nullptr;
   a.ql = 0.25f * lambda;  // one IEEE multiply, as in the oracle
+  a.tol = tol;
   a.partials = parts; a.ticket = ticket;
   // extract (+ stats of J0), or extract+compress when niter == 0
   a.src = image;

@@ -546,7 +546,8 @@ class EulerP2PSlabs:
             self.base = None
 
 
-def euler_distributed_p2p(slabs: EulerP2PSlabs, areas_own, normals_own, ff, vars_own, iterations: int):
+def euler_distributed_p2p(slabs: EulerP2PSlabs, areas_own, normals_own, ff, vars_own, iterations: int,
+                          exact: bool = False):
     """Rodinia euler on this rank's element slab with the fused peer-memory
     exchange: per RK stage one stage kernel (waits on the arrival counter)
     and one push kernel (stores the halo values into the peers' arrays, counts
@@ -569,7 +570,8 @@ def euler_distributed_p2p(slabs: EulerP2PSlabs, areas_own, normals_own, ff, vars
             target = slabs.epoch + pushes  # every source has pushed `pushes` times this call
             rc = lib.jb_euler_stage_p2p_f32(n_own, n_loc, j, areas_own.data_ptr(), nbrs.data_ptr(),
                                             normals_own.data_ptr(), ff.data_ptr(), slabs.buf(cb), slabs.buf(0),
-                                            slabs.buf(db), slabs.flags(), slabs.srcmask, target, stream)
+                                            slabs.buf(db), slabs.flags(), slabs.srcmask, target, int(exact),
+                                            stream)
             if rc:
                 raise RuntimeError(f"euler_stage_p2p: {_lib.last_error()}")
             slabs.push(db, stream)
@@ -579,12 +581,16 @@ def euler_distributed_p2p(slabs: EulerP2PSlabs, areas_own, normals_own, ff, vars
 
 
 class CudaEulerBackend:
-    """libjunob200's slab stage kernel on device tensors (NCCL exchanges)."""
+    """libjunob200's slab stage kernel on device tensors (NCCL exchanges).
+    exact=True: the bit-exact stage (else the tolerance mode of jb_euler_f32;
+    either way a sharded run is bit-identical to the single-device run of the
+    same mode, since CFD has no reductions)."""
 
-    def __init__(self):
+    def __init__(self, exact: bool = False):
         import torch
         self.torch = torch
         self.lib = _lib.load()
+        self.exact = exact
 
     def to_device(self, a, like):
         return self.torch.as_tensor(a).to(like.device)
@@ -592,6 +598,6 @@ class CudaEulerBackend:
     def stage(self, n_own, n_loc, j, areas, nbrs, normals, ff, cur, old, dst):
         rc = self.lib.jb_euler_stage_f32(int(n_own), int(n_loc), int(j), areas.data_ptr(), nbrs.data_ptr(),
                                          normals.data_ptr(), ff.data_ptr(), cur.data_ptr(), old.data_ptr(),
-                                         dst.data_ptr(), self.torch.cuda.current_stream().cuda_stream)
+                                         dst.data_ptr(), int(self.exact), self.torch.cuda.current_stream().cuda_stream)
         if rc:
             raise RuntimeError(f"euler_stage: {_lib.last_error()}")

@@ -62,9 +62,19 @@ def test_fullsize_srad_16384_100_iterations_tolerance(jb, oracle):
 
 def test_fullsize_euler_2048_mesh_10_iterations_bit_exact(jb, oracle):
     areas, nb, normals, ff, v = W.euler_mesh(2048, 2048)
-    got = jb.euler(10, areas, nb, normals, ff, v)
+    got = jb.euler(10, areas, nb, normals, ff, v, exact=True)
     ref = oracle.euler(areas, nb, normals, ff, v, 10)
     assert np.array_equal(_bits(got), _bits(ref))
+
+
+def test_fullsize_euler_2048_mesh_tolerance(jb, oracle):
+    """The default tolerance mode at the benchmark mesh: 1e-5 per RK stage of
+    each variable's scale, after 10 iterations (30 stages)."""
+    areas, nb, normals, ff, v = W.euler_mesh(2048, 2048)
+    got = np.asarray(jb.euler(10, areas, nb, normals, ff, v), np.float64)
+    ref = oracle.euler(areas, nb, normals, ff, v, 10).astype(np.float64)
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    assert np.all(np.abs(got - ref) <= 1e-5 * 30 * scale)
 
 
 def test_fullsize_bfs_16m_bit_exact(jb, oracle):

@@ -52,8 +52,12 @@ def test_cava_random_shapes_bit_exact(jb, oracle, b, r, c, P, seed):
 @given(w=st.integers(1, 70), h=st.integers(1, 40), iters=st.integers(1, 3), seed=st.integers(0, 10**6))
 def test_euler_random_meshes_bit_exact(jb, oracle, w, h, iters, seed):
     areas, nb, normals, ff, v = W.euler_mesh(w, h, seed=seed)
-    got = jb.euler(iters, areas, nb, normals, ff, v)
-    assert np.array_equal(_bits(got), _bits(oracle.euler(areas, nb, normals, ff, v, iters)))
+    got = jb.euler(iters, areas, nb, normals, ff, v, exact=True)
+    ref = oracle.euler(areas, nb, normals, ff, v, iters)
+    assert np.array_equal(_bits(got), _bits(ref))
+    fast = np.asarray(jb.euler(iters, areas, nb, normals, ff, v), np.float64)   # tolerance mode
+    scale = np.nanmax(np.abs(ref), axis=1, keepdims=True)
+    assert np.all(np.abs(fast - ref) <= 1e-5 * 3 * iters * scale)
 
 
 @SETTINGS
