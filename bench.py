@@ -95,6 +95,8 @@ class Dist:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             dist.init_process_group(backend=backend)
             self.pg = dist
+            # every rank of the launch is in the group the collectives use
+            assert dist.get_world_size() == self.world, (dist.get_world_size(), self.world)
 
     def barrier(self):
         if self.pg:
@@ -278,14 +280,21 @@ class MatmulWorkload:
     flush_l2 = True
 
     def __init__(self, args, rank, world):
+        from paper_2503_10855_b200 import dist as D
         from paper_2503_10855_b200 import workloads as W
         self.n = self.m = self.l = 1024
         self.a, self.b = W.matmul_inputs(self.n, self.m, self.l)
         self.local = 1
+        # N > 1: row blocks of A and C (dist.MatmulRowBlocks), B broadcast once
+        self.world = world
+        self.r0, self.rows = D.row_block(self.n, world, rank)
+        if world > 1:
+            self.scaling = "strong"
 
     def config(self, world):
         return {"workload": "matmul<1024,1024,1024> f32 (Fig. 1 entry), 3xTF32 tcgen05",
-                "parallelism": "replica" if world == 1 else f"replicas/{world}",
+                "parallelism": "single GPU" if world == 1 else
+                f"row blocks/{world}: A and C rows split, B broadcast once at setup (dist.MatmulRowBlocks)",
                 "l2": "flushed (256 MiB write) before every timed call"}
 
     def units_per_step(self):
@@ -296,16 +305,20 @@ class MatmulWorkload:
 
     def setup_device(self, torch):
         from paper_2503_10855_b200 import _lib
+        from paper_2503_10855_b200 import dist as D
         self.lib = _lib.load()
-        self.da, self.db = torch.from_numpy(self.a).cuda(), torch.from_numpy(self.b).cuda()
-        self.dc = torch.empty((self.n, self.l), dtype=torch.float32, device="cuda")
+        self.da = torch.from_numpy(np.ascontiguousarray(self.a[self.r0:self.r0 + self.rows])).cuda()
+        self.db = torch.from_numpy(self.b).cuda()
+        if self.world > 1:
+            self.blocks = D.MatmulRowBlocks(self.db, self.n)   # the one broadcast of B
+        self.dc = torch.empty((self.rows, self.l), dtype=torch.float32, device="cuda")
         self.stream = torch.cuda.current_stream()
         self.pa = torch.from_numpy(self.a).pin_memory()
         self.pb = torch.from_numpy(self.b).pin_memory()
         self.pc = torch.empty((self.n, self.l), dtype=torch.float32).pin_memory()
 
     def step_device(self):
-        rc = self.lib.jb_matmul_f32(self.n, self.m, self.l, self.da.data_ptr(), self.db.data_ptr(),
+        rc = self.lib.jb_matmul_f32(self.rows, self.m, self.l, self.da.data_ptr(), self.db.data_ptr(),
                                     self.dc.data_ptr(), self.stream.cuda_stream)
         if rc:
             from paper_2503_10855_b200 import _lib
@@ -313,12 +326,13 @@ class MatmulWorkload:
 
     def step_e2e(self):
         from paper_2503_10855_b200 import api
-        self.e2e_out = api.execute("matmul", [self.n, self.m, self.l], [self.a, self.b])
+        a = self.a if self.world == 1 else self.a[self.r0:self.r0 + self.rows]
+        self.e2e_out = api.execute("matmul", [a.shape[0], self.m, self.l], [a, self.b])
 
     e2e_api = "paper_2503_10855_b200.api.execute('matmul', ...) on numpy in/out"
 
     def e2e_bytes(self):
-        return 8 * self.n * self.m, 4 * self.n * self.l
+        return 4 * (self.rows * self.m + self.m * self.l), 4 * self.rows * self.l
 
     def ref_step(self, oracle, sample=False):
         oracle.matmul(self.a, self.b)

@@ -773,7 +773,7 @@ __device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, R
   const unsigned FULL = 0xffffffffu;
   const float n2q0 = -2.0f * k.q0, hiq = 0.5f / k.q0den, ql = k.ql;
   const size_t cs = (size_t)cols;
-  const int nrow = y1 - y0 + 3;                                     // rows y0-1 .. y1+1 (= SH + 2)
+  const int nrow = y1 - y0 + 3;                                     // ring rows y0-1 .. y1+1 (= SH + 3)
   const float *gj = k.src + (size_t)(y0 - 1) * cs + xb;
   const float *gw = k.src + (size_t)(y0 - 1) * cs + xw;
   float *po = k.dst + (size_t)(y0 - k.row_lo) * cs + xl;
@@ -871,7 +871,7 @@ __device__ __forceinline__ void strip_tol(const StripCtx k, const PeerRows pr, R
 
   step(1, false);  // c(y0)
 #pragma unroll 1
-  for (int base = 2; base < nrow; base += RING) {  // rows i = base .. base+7 (slots 2..7,0,1)
+  for (int base = 2; base < nrow - 1; base += RING) {  // centre rows i = base .. base+7 (slots 2..7,0,1)
 #pragma unroll
     for (int u = 0; u < RING; u++) {
       step((2 + u) % RING, true);

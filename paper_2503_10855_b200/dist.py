@@ -45,14 +45,72 @@ def row_block(n: int, world: int, rank: int) -> tuple[int, int]:
     return partition(n, world, rank)
 
 
-def matmul_row_blocks(a_rows, b, group=None, src: int = 0):
-    """C[rows] = A[rows] @ B on this rank; B is broadcast from `src` once."""
-    import torch.distributed as dist
+class MatmulRowBlocks:
+    """Row-block matmul<n,m,l> across the ranks of `group`.
 
-    from .api import matmul
-    if dist.is_initialized():
-        dist.broadcast(b, src=src, group=group)
-    return matmul(a_rows, b)
+    A and C are split by rows (row_block); B is replicated: it is broadcast
+    from `src` ONCE, when the object is built, and cached on every rank, so a
+    call is collective-free -- each rank runs the tcgen05 kernel on its own
+    rows (`mm`, default api.matmul; the CPU tests pass the oracle).
+    ``gather(c_rows)`` all-gathers the full C when one rank needs it."""
+
+    def __init__(self, b, n: int, group=None, src: int = 0, mm=None):
+        import torch.distributed as dist
+        self.group, self.n = group, int(n)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.r0, self.rows = row_block(self.n, self.world, self.rank)
+        if self.world > 1:
+            b = b.contiguous()
+            if b.is_cuda and _gloo(group):   # shared-GPU test mode: stage through the host
+                x = b.cpu()
+                dist.broadcast(x, src=src, group=group)
+                b.copy_(x)
+            else:
+                dist.broadcast(b, src=src, group=group)
+        self.b = b
+        if mm is None:
+            from .api import matmul as mm
+        self.mm = mm
+        self.broadcasts = 1 if self.world > 1 else 0
+
+    def own_rows(self, a_full):
+        """This rank's rows of a full A."""
+        return a_full[self.r0:self.r0 + self.rows]
+
+    def __call__(self, a_rows):
+        assert a_rows.shape[0] == self.rows, f"rank {self.rank} owns {self.rows} rows, got {a_rows.shape[0]}"
+        return self.mm(a_rows, self.b)
+
+    def gather(self, c_rows):
+        """The full C on every rank (all-gather of the row blocks)."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return c_rows
+        t = c_rows if isinstance(c_rows, torch.Tensor) else torch.from_numpy(c_rows)
+        cap = -(-self.n // self.world)
+        pad = torch.zeros((cap, t.shape[1]), dtype=t.dtype, device=t.device)
+        pad[:self.rows] = t
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        if pad.is_cuda and _gloo(self.group):
+            cpu = [p.cpu() for p in parts]
+            dist.all_gather(cpu, pad.cpu(), group=self.group)
+            parts = [c.to(pad.device) for c in cpu]
+        else:
+            dist.all_gather(parts, pad, group=self.group)
+        full = torch.cat([p[:row_block(self.n, self.world, r)[1]] for r, p in enumerate(parts)])
+        return full if isinstance(c_rows, torch.Tensor) else full.numpy()
+
+
+def matmul_row_blocks(a_rows, b, n: int = None, group=None, src: int = 0):
+    """One-shot row-block matmul: C[rows] = A[rows] @ B with B broadcast from
+    `src` (for repeated calls build a MatmulRowBlocks: it broadcasts once)."""
+    n = a_rows.shape[0] if n is None else n
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    mb = MatmulRowBlocks(b, n if world > 1 else a_rows.shape[0], group, src)
+    return mb(a_rows)
 
 
 # ------------------------------------------------------------------- SRAD

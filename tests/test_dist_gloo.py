@@ -209,3 +209,62 @@ def test_euler_element_slabs_match_single_device(world):
     ref = oracle.euler(areas, nb, normals, ff, v, CFD_ITERS)
     got = np.concatenate(_run(world, _euler_rank), axis=1)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+# --------------------------------------------------------- matmul / CAVA
+MM_N, MM_M, MM_L = 37, 16, 24
+
+
+def _matmul_rank(rank, world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    a, b = W.matmul_inputs(MM_N, MM_M, MM_L, seed=4)
+    # only the source rank starts with B: the others receive it once
+    bt = torch.from_numpy(b) if rank == 0 else torch.zeros((MM_M, MM_L), dtype=torch.float32)
+    mb = D.MatmulRowBlocks(bt, MM_N, mm=lambda x, y: torch.from_numpy(oracle.matmul(x.numpy(), y.numpy())))
+    a_own = torch.from_numpy(np.ascontiguousarray(mb.own_rows(a)))
+    c1 = mb(a_own)
+    c2 = mb(a_own)           # a second call: no further broadcast
+    assert torch.equal(c1, c2) and mb.broadcasts == 1
+    return c1.numpy(), mb.gather(c1).numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_matmul_row_blocks_match_single_device(world):
+    """Row blocks of A and C with B broadcast once: the concatenated blocks
+    (and the all-gathered C on every rank) are bit-identical to the
+    single-device oracle (rows of the sequential-k product do not interact)."""
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    a, b = W.matmul_inputs(MM_N, MM_M, MM_L, seed=4)
+    ref = oracle.matmul(a, b)
+    outs = _run(world, _matmul_rank)
+    got = np.concatenate([o[0] for o in outs])
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    for _, full in outs:
+        assert np.array_equal(full.view(np.uint32), ref.view(np.uint32))
+
+
+def _cava_rank(rank, world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    raw = W.cava_raw(5, 20, 34, seed=2)
+    params = W.cava_params(16)
+    f0, cnt = D.shard_frames(5, world, rank)
+    out = torch.from_numpy(oracle.cava(raw[f0:f0 + cnt], *params))
+    sizes = [D.shard_frames(5, world, r)[1] for r in range(world)]
+    pad = torch.zeros((max(sizes), 3, 20, 34), dtype=torch.uint8)
+    pad[:cnt] = out
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    return torch.cat([b[:s] for b, s in zip(bufs, sizes)]).numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cava_frame_sharding_gathers_the_batch(world):
+    from oracle import oracle
+    from paper_2503_10855_b200 import workloads as W
+    raw = W.cava_raw(5, 20, 34, seed=2)
+    ref = oracle.cava(raw, *W.cava_params(16))
+    for o in _run(world, _cava_rank):
+        assert np.array_equal(o, ref)

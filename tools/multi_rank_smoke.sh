@@ -15,4 +15,8 @@ for w in ${WORKLOADS:-edge cava matmul srad euler bfs backprop}; do
     echo "rc=$?" >> gpurun_out/multi_rank.log
   done
 done
-grep -E "^==|^rc=|\"metric\"|unavailable|Error" gpurun_out/multi_rank.log | cut -c1-220
+echo "== matmul row blocks vs N=1" >> gpurun_out/multi_rank.log
+JB_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29518 tools/matmul_rowblock_check.py >> gpurun_out/multi_rank.log 2>&1
+echo "rc=$?" >> gpurun_out/multi_rank.log
+grep -E "^==|^rc=|\"metric\"|unavailable|Error|bit-identical|DIFFERENT" gpurun_out/multi_rank.log | cut -c1-220
