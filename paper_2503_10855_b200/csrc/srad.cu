@@ -323,7 +323,7 @@ constexpr int SW = 124, SH = 32, SWARPS = 8;
 #define SRAD_MINB 2
 #endif
 #ifndef SRAD_TOL_MINB
-#define SRAD_TOL_MINB 3
+#define SRAD_TOL_MINB 2  // 128 registers, no spills: 0.518 against 0.587 ms/iteration at 3 (85 regs, spills)
 #endif
 
 struct StripCtx {
@@ -702,12 +702,16 @@ __device__ __forceinline__ bool strip_fast(const StripCtx k, const PeerRows pr, 
 //   (G2num = dN^2+dS^2+dW^2+dE^2, Ls = dN+dS+dW+dE),
 //   c = 1/(1 + (qsqr - q0)/q0den) = D^2 / (D^2 + (N - q0 D^2)/q0den),
 // so a pixel costs ONE approximate reciprocal (MUFU.RCP) instead of four
-// IEEE divisions, and every multiply-add is one FFMA2 for a pixel pair.
-// Where the final denominator cancels (Y < D^2/64, the only place the
+// IEEE divisions, and the rest is contracted FFMAs.
+// Where the final denominator cancels (Y < D^2/2^16, the only place the
 // rewrite can lose more than a few ulps) or the result is not finite, the
-// pair is recomputed with the exact coefficient.  Result: c within ~1e-6
-// relative of the oracle's, J' within ql*|D| of that; the test contract is
-// rel 1e-4 after the full iteration count.
+// pair is recomputed with the exact coefficient.  (Mathematically
+// N >= G2num/4 >= 0 by Cauchy-Schwarz, so Y >= D^2 q0/(1+q0) > 0 and c is at
+// most (1+q0)/q0: a small Y means c >> 1, which the clamp maps to 1 however
+// it is rounded.  Only Y within rounding noise of 0 -- q0 below ~2^-16 --
+// could flip its sign, so pixels with Y < D^2/2^16 take the exact path.)
+// Result: c within ~1e-6 relative of the oracle's, J' within ql*|D| of that;
+// the test contract is rel 1e-4 after the full iteration count.
 __device__ __forceinline__ f2 add2(f2 a, f2 b) {
   f2 d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -722,8 +726,7 @@ struct TolK {
 };
 
 // c for a pixel pair (unclamped); sets bad when the pair needs the exact redo
-// (Y < D^2/64: the rewritten denominator cancels; NaN data propagates the
-// same way on both paths)
+// (Y < D^2/2^16, see above; NaN data propagates the same way on both paths)
 __device__ __forceinline__ f2 coef2_tol(f2 Jc, const PxPair &d, const TolK &t, bool &bad) {
   const f2 G2num = fma2(d.e, d.e, fma2(d.w, d.w, fma2(d.s, d.s, mul2(d.n, d.n))));
   const f2 Ls = add2(add2(add2(d.n, d.s), d.w), d.e);
@@ -733,7 +736,7 @@ __device__ __forceinline__ f2 coef2_tol(f2 Jc, const PxPair &d, const TolK &t, b
   const f2 X = fma2(D2, t.n2q0, N2);                        // 2N - 2 q0 D^2
   const f2 Y = fma2(X, t.hiq, D2);                          // D^2 + (N - q0 D^2)/q0den
   const f2 c = mul2(D2, rcp2_approx(Y));
-  const f2 g = fma2(D2, bc2(-0.015625f), Y);                // Y - D^2/64
+  const f2 g = fma2(D2, bc2(-1.52587890625e-05f), Y);       // Y - D^2/2^16
   bad = bad | (fminf(lo2(g), hi2(g)) < 0.0f);
   return c;
 }
@@ -750,7 +753,7 @@ __device__ __forceinline__ float coef_tol(float Jc, float dn, float ds, float dw
   const float N2 = __fmaf_rn(Ls * Ls, -0.125f, G2num);
   const float X = __fmaf_rn(D2, n2q0, N2);
   const float Y = __fmaf_rn(X, hiq, D2);
-  bad = bad | (__fmaf_rn(D2, -0.015625f, Y) < 0.0f);
+  bad = bad | (__fmaf_rn(D2, -1.52587890625e-05f, Y) < 0.0f);  // Y < D^2 / 2^16
   return __saturatef(D2 * rcp_approx(Y));
 }
 
