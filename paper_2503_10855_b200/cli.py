@@ -8,7 +8,7 @@ and scheduling stay with the reference:
   python -m paper_2503_10855_b200 entries
   python -m paper_2503_10855_b200 run ENTRY --dc n=4 --dc m=4 --dc l=4 \\
         --input a.json --input b.json [-o out.json | --out-dir DIR]
-        [--source prog.jn --schedule prog.sch]
+        [--source prog.jn --schedule prog.sch [--oracle]]
   python -m paper_2503_10855_b200 plan --source prog.jn [--schedule s.sch]
         [--function NAME] [--dc k=v ...]
 
@@ -17,7 +17,11 @@ the entry through api.execute (or, with --source, plans and selects the
 kernel for the scheduled function: planner.execute_module), writes the
 result in the same format (a tuple result: one file per element,
 ``out_<i>.json``) and prints one machine-readable metrics line (SPEC.md:584
-"metrics on a machine-readable trailer line").  ``plan`` prints the §4.4
+"metrics on a machine-readable trailer line").  ``run --oracle`` is the
+SPEC's A/B switch ("runs the value-semantics interpreter
+instead"): the same --source/--schedule module, inputs and output files, but
+executed by the reference's own interpreter (skiff.runtime.oracle
+.oracle_execute), so ``cmp`` on the two output files is the A/B check.  ``plan`` prints the §4.4
 launch plan of each function.  --source/--schedule/plan need the reference's
 skiff package importable (they parse Juno with it).
 
@@ -102,6 +106,9 @@ def cmd_run(args) -> int:
     except (OSError, tensor_io.TensorFormatError, KeyError, ValueError) as e:
         print(f"error: {e}", file=sys.stderr)
         return 2
+    if args.oracle and not args.source:
+        print("error: --oracle runs the reference interpreter on a module: it needs --source", file=sys.stderr)
+        return 2
     module = _skiff_module(args.source, args.schedule) if args.source else None
     if module is None and args.entry not in api.ENTRIES:
         print(f"error: unknown entry {args.entry!r}; known: {sorted(api.ENTRIES)}", file=sys.stderr)
@@ -116,14 +123,16 @@ def cmd_run(args) -> int:
     launches0 = _lib.launch_count()
     t0 = time.perf_counter()
     try:
-        if module is not None:
+        if args.oracle:
+            result, kernel = _reference_oracle(module, args.entry, dcs, inputs), "skiff.oracle_execute"
+        elif module is not None:
             from .planner import execute_module
             result, choice = execute_module(module, args.entry, dcs, inputs)
             kernel = choice.entry
         else:
             result = api.execute(args.entry, dcs, inputs)
             kernel = args.entry
-    except (api.RuntimeError_, api.DynConstError, KeyError) as e:
+    except (api.RuntimeError_, api.DynConstError, api.OracleLimitError, KeyError) as e:
         print(f"error: {type(e).__name__}: {e}", file=sys.stderr)
         return 1
     wall = (time.perf_counter() - t0) * 1e3
@@ -135,6 +144,26 @@ def cmd_run(args) -> int:
                       "gpu_launches": _lib.launch_count() - launches0, "h2d_bytes": h2d, "d2h_bytes": d2h,
                       "outputs": paths}))
     return 0
+
+
+def _reference_oracle(module, entry, dcs, inputs):
+    """``run --oracle``: the reference's value-semantics interpreter
+    (skiff/runtime/oracle.py:28-32) on the same module and inputs.  Its
+    exceptions are the reference classes; they are re-raised as the
+    drop-in's (which also derive from the reference's, api._err) so both
+    arms of the A/B report errors the same way."""
+    from skiff.dynconst import DynConstError
+    from skiff.runtime.oracle import OracleLimitError, oracle_execute
+    from skiff.runtime.values import RuntimeError_
+    from . import api
+    try:
+        return oracle_execute(module, entry, list(dcs), list(inputs))
+    except OracleLimitError as e:
+        raise api._err(api.OracleLimitError, str(e)) from e
+    except DynConstError as e:
+        raise api._err(api.DynConstError, str(e)) from e
+    except RuntimeError_ as e:
+        raise api._err(api.RuntimeError_, str(e)) from e
 
 
 def cmd_plan(args) -> int:
@@ -162,6 +191,8 @@ def main(argv=None) -> int:
     r.add_argument("--out-dir", help="output directory (out.json / out_<i>.json)")
     r.add_argument("--source", help="Juno source: plan + select the kernel for ENTRY (needs skiff)")
     r.add_argument("--schedule", help="schedule applied to --source")
+    r.add_argument("--oracle", action="store_true",
+                   help="A/B: run --source with the reference's value-semantics interpreter instead (SPEC.md:600)")
     p = sub.add_parser("plan", help="print the paper-§4.4 launch plan of each function (needs skiff)")
     p.add_argument("--source", required=True)
     p.add_argument("--schedule")

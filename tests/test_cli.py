@@ -129,3 +129,83 @@ def test_cli_runs_a_tuple_entry(tmp_path):
                        text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert len(json.loads(r.stdout.strip().splitlines()[-1])["outputs"]) == 6
+
+
+_MATMUL_JN = """
+#[entry]
+fn matmul<n, m, l: usize>(a: f32[n, m], b: f32[m, l]) -> f32[n, l] {
+  let res : f32[n, l];
+  @outer for i in 0..n {
+    @middle for j in 0..l {
+      @inner for k in 0..m {
+        res[i, j] += a[i, k] * b[k, j];
+      }
+    }
+  }
+  return res;
+}
+"""
+
+
+def _ab_files(tmp_path, n, m, l, schedule):
+    rng = np.random.default_rng(11)
+    src, sch = tmp_path / "matmul.jn", tmp_path / "matmul.sch"
+    src.write_text(_MATMUL_JN)
+    sch.write_text(schedule)
+    args = []
+    for name, shape in (("a", (n, m)), ("b", (m, l))):
+        p = tmp_path / f"{name}.json"
+        tensor_io.dump_tensor(rng.uniform(-1, 1, shape).astype(np.float32), str(p))
+        args += ["--input", str(p)]
+    return ["run", "matmul", "--dc", f"n={n}", "--dc", f"m={m}", "--dc", f"l={l}", "--source", str(src),
+            "--schedule", str(sch), *args]
+
+
+def test_oracle_ab_runs_the_reference_interpreter(tmp_path, capsys):
+    """SPEC.md:600 ``run --oracle``: the same module and inputs through the
+    reference's value-semantics interpreter; the file equals what skiff's
+    own oracle_execute + dump_tensor give."""
+    values = _ref_values()
+    from skiff.runtime.oracle import oracle_execute
+    argv = _ab_files(tmp_path, 4, 6, 5, "forkify(*); forkify(*); forkify(*);")
+    out = tmp_path / "o.json"
+    assert cli.main(argv + ["--oracle", "-o", str(out)]) == 0
+    metrics = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert metrics["kernel"] == "skiff.oracle_execute" and metrics["gpu_launches"] == 0
+    mod = cli._skiff_module(str(tmp_path / "matmul.jn"), str(tmp_path / "matmul.sch"))
+    a, b = tensor_io.load_tensor(str(tmp_path / "a.json")), tensor_io.load_tensor(str(tmp_path / "b.json"))
+    ref = tmp_path / "ref.json"
+    values.dump_tensor(oracle_execute(mod, "matmul", [4, 6, 5], [a, b]), str(ref))
+    assert out.read_bytes() == ref.read_bytes()
+
+
+def test_oracle_ab_constraint_error_exit_1(tmp_path, capsys):
+    # SPEC.md:585 "n=6 chunk-4 -> constraint error", through the reference arm
+    _ref_values()
+    sch = r"forkify(*); forkify(*); forkify(*); let par = matmul@outer \ matmul@inner; fork-chunk![4](par);"
+    argv = _ab_files(tmp_path, 6, 6, 6, sch)
+    assert cli.main(argv + ["--oracle", "-o", str(tmp_path / "o.json")]) == 1
+    assert "DynConstError" in capsys.readouterr().err
+
+
+def test_oracle_needs_source(tmp_path):
+    a = tmp_path / "a.json"
+    tensor_io.dump_tensor(np.eye(2, dtype=np.float32), str(a))
+    assert cli.main(["run", "matmul", "--dc", "2", "--dc", "2", "--dc", "2", "--input", str(a), "--input", str(a),
+                     "--oracle"]) == 2
+
+
+@pytest.mark.gpu
+def test_oracle_ab_matches_gpu_arm(tmp_path, capsys):
+    """The two arms of the A/B on a scheduled Fig. 1 matmul: the GPU kernel
+    (3xTF32, re-associated k) within the fp32 bound of the interpreter."""
+    _ref_values()
+    argv = _ab_files(tmp_path, 64, 48, 40, r"forkify(*); forkify(*); forkify(*); fork-tile![4](matmul);")
+    assert cli.main(argv + ["--oracle", "-o", str(tmp_path / "ref.json")]) == 0
+    assert cli.main(argv + ["-o", str(tmp_path / "gpu.json")]) == 0
+    ref = tensor_io.load_tensor(str(tmp_path / "ref.json")).astype(np.float64)
+    gpu = tensor_io.load_tensor(str(tmp_path / "gpu.json")).astype(np.float64)
+    a, b = (tensor_io.load_tensor(str(tmp_path / f"{x}.json")).astype(np.float64) for x in "ab")
+    u, m = 2.0 ** -24, 48
+    gam = m * u / (1 - m * u)
+    assert np.all(np.abs(gpu - ref) <= (2 * gam + 8 * u) * (np.abs(a) @ np.abs(b)))
