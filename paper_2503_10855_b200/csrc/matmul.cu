@@ -10,19 +10,31 @@
 //   x_hi = trunc_tf32(x) (what kind::tf32 reads from an f32 container),
 //   x_lo = x - x_hi (exact in f32),
 //   D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi   (f32 accumulators in TMEM).
-// One kernel, one 128x128 output tile per CTA (split-K 2 when the tile
-// count is below one wave: the two partials meet in C through f32 vector
-// reductions, order independent), 320 threads:
+// One kernel, one 128x128 output tile per CTA, 320 threads:
 //   warp 0     TMA producer: raw fp32 A tile (K-major, 128B swizzle) and raw
 //              B tile (MN-major, 128B swizzle with 32-byte atoms = UMMA
 //              layout SWIZZLE_128B_BASE32B) per 32-wide k-block into a
 //              4-stage mbarrier ring.  Only raw operands cross L2 -> SMEM;
 //              the raw tiles ARE the hi operands (the tensor core truncates
 //              the 13 low bits, verified by tools/mma_probe.cu).
-//   warps 2-9  converters: lo = x - trunc(x) into a 2-slot ring, elementwise in the same
-//              swizzled layouts (no transpose), then the epilogue
-//              (tcgen05.ld -> global, f32x4 reductions under split-K).
+//   warps 2-9  converters: lo = x - trunc(x).  B_lo goes to a 2-slot smem
+//              ring in B's swizzled layout; A_lo goes to TMEM (tcgen05.st,
+//              thread = row of its lane quarter) and the lo*hi MMA reads A
+//              from there (kind::tf32 with A in TMEM).  Shared memory, not
+//              the tensor core, bounds this loop (per k-block 32 KiB TMA in,
+//              converter reads and B_lo writes, three MMA operand reads at
+//              ~128 B/clk): keeping A_lo out of it saves 32 KiB per k-block,
+//              0.0293 -> 0.0276 ms per 1024^3 call.  Warps 2-5 then run the
+//              epilogue (tcgen05.ld -> global).
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer.
+// Split-K 2 when the tile count is below one wave: the two partials meet in
+// C through f32 vector reductions onto zero (0 + p0 + p1 rounds the same in
+// either order: deterministic).  Two designs that drop the memset were
+// measured and lost: a CTA-pair kernel (cta_group::2,
+// 256x256 pair tiles, split-K 4 through an L2 scratch; its main loop ran at
+// the measured tensor peak but the 12 MB partial exchange cost more,
+// 0.0303 ms per call) and store-then-add split-K ordered by a per-tile flag
+// (the second split waits: 0.0309 ms).
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
 #include <mutex>
@@ -326,413 +338,6 @@ done:
   }
 }
 
-// ------------------------------------------------ CTA-pair kernel (default)
-// The single-CTA kernel above is bound by shared-memory bandwidth, not by the
-// tensor core: per 32-wide k-block a 128x128 tile moves 32 KiB in by TMA,
-// 64 KiB through the converters and 96 KiB into the three MMAs -- 192 KiB
-// against 768 tensor-core clocks at ~128 B/clk (ncu: tensor pipe 46%).  A
-// CTA pair (cta_group::2, M = 256) with a 256-wide pair tile halves B per SM
-// and doubles the MMA work per byte: per SM and k-block 32 KiB TMA + 64 KiB
-// conversion + 96 KiB MMA reads against 1536 tensor clocks.
-//
-// 1024^3 maps to 16 pair tiles x split-K 4 = 64 pairs (128 CTAs, clusters of
-// 2: the pair).  The split-K partials meet in an L2-resident scratch, not in
-// C: split s owns columns [64s, 64s+64) of the pair tile; every CTA writes
-// the other splits' columns of its TMEM partial to the scratch, counts
-// itself in on a per-tile counter and, once all splits are in, sums its own
-// columns over the splits in split order (deterministic, no memset of C, no
-// atomics on C).  The splits of a tile wait for each other, so the grid must
-// be co-resident: the host only takes this path when it fits one wave.
-// (Distributed shared memory was tried first: 17-21 B/clk per SM and
-// clusters of 8 that did not all fit at once made it 2.5x slower.)
-namespace mm2 {
-
-constexpr int BM = 128;           // rows per CTA (256 per pair)
-constexpr int BK = 32;
-constexpr int B_ATOM = BK * 32 * 4;
-constexpr int STAGES = 4, LO_STAGES = 2;
-constexpr int A_TILE = BM * BK * 4;   // 16 KiB
-constexpr int THREADS = 320, CONVERTERS = 256;
-#ifndef MM_A_SMEM
-// A's tf32 residual goes to TMEM (tcgen05.st) and the lo*hi MMA reads it
-// from there: 32 KiB less shared-memory traffic per k-block (the A_lo store
-// and its MMA read).  -DMM_A_SMEM keeps it in shared memory (A/B builds).
-#define MM_A_TMEM 1
-#else
-#define MM_A_TMEM 0
-#endif
-
-// BNP: pair tile width (256 or 128); each CTA stages BNP/2 columns of B
-template <int BNP>
-struct PairCfg {
-  static constexpr int BNH = BNP / 2;
-  static constexpr int B_TILE = BK * BNH * 4;
-  static constexpr int CHUNKS = BNP / 16;       // 16-column TMEM chunks of a partial
-  static constexpr int PART_FLOATS = BM * BNP;  // one CTA's partial in the scratch
-  static constexpr uint32_t ALO_COL = BNP;      // A_lo stages at BNP + 32*stage
-  static constexpr uint32_t TMEM_COLS = MM_A_TMEM ? (BNP + BK * LO_STAGES <= 256 ? 256u : 512u) : (uint32_t)BNP;
-  struct Smem {
-    uint8_t a_raw[STAGES][A_TILE];  // [128 m][32 k] K-major, 128B swizzle (also the tf32 hi operand)
-    uint8_t b_raw[STAGES][B_TILE];  // BNH/32 MN atoms x [32 k][32 n], 128B swizzle / 32B atoms
-    uint8_t a_lo[LO_STAGES][A_TILE];
-    uint8_t b_lo[LO_STAGES][B_TILE];
-    uint64_t full[STAGES];       // TMA -> local converters
-    uint64_t empty[STAGES];      // pair MMAs -> local TMA (multicast commit)
-    uint64_t conv[LO_STAGES];    // converters of BOTH CTAs -> the MMA issuer (even CTA)
-    uint64_t lo_empty[LO_STAGES];
-    uint64_t tmem_full;
-    uint64_t red_full;           // the other splits' partials of the owned columns landed
-    uint32_t tmem_base;
-  };
-  static constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
-  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-};
-
-__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void epi_bar() {  // the 8 converter/epilogue warps
-  asm volatile("bar.sync 1, %0;" ::"n"(CONVERTERS) : "memory");
-}
-
-// grid = pair tiles x SPLITK pairs (clusters of 2, split fastest); CTA p of
-// the pair takes rows [128p, 128p+128) of the pair tile
-template <int BNP, int SPLITK>
-__global__ void __launch_bounds__(THREADS, 1)
-gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                        float *__restrict__ c, int M, int N, int K, int tiles_n, float *__restrict__ part,
-                        unsigned *__restrict__ cnt) {
-  using Cfg = PairCfg<BNP>;
-  using Smem = typename Cfg::Smem;
-  constexpr int BNH = Cfg::BNH, B_TILE = Cfg::B_TILE, CHUNKS = Cfg::CHUNKS, PART_FLOATS = Cfg::PART_FLOATS;
-  constexpr uint32_t ALO_COL = Cfg::ALO_COL, TMEM_COLS = Cfg::TMEM_COLS;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
-  Smem &S = *reinterpret_cast<Smem *>(smem_raw + pad);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = (int)(tc::cluster_ctarank() & 1u);
-  const int pair = blockIdx.x >> 1;
-  const int tile = pair / SPLITK, sk = pair % SPLITK;
-  const int m0 = (tile / tiles_n) * (2 * BM) + p * BM;  // this CTA's rows of A and C
-  const int n0 = (tile % tiles_n) * BNP;                // the pair tile's columns
-  const int kblocks = (K + BK - 1) / BK;
-  const int kb0 = (int)((long long)kblocks * sk / SPLITK);
-  const int nkb = (int)((long long)kblocks * (sk + 1) / SPLITK) - kb0;  // >= 1 (host)
-  if (threadIdx.x == 0) MM_T(0);
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      tc::mbar_init(&S.full[s], 1);
-      tc::mbar_init(&S.empty[s], 1);
-    }
-    for (int s = 0; s < LO_STAGES; s++) {
-      tc::mbar_init(&S.conv[s], 2 * (CONVERTERS / 32));
-      tc::mbar_init(&S.lo_empty[s], 1);
-    }
-    tc::mbar_init(&S.tmem_full, 1);
-    tc::mbar_init(&S.red_full, 1);
-    tc::fence_mbar_init();
-    tc::tma_prefetch(&tm_a);
-    tc::tma_prefetch(&tm_b);
-    // the first stages need nothing from the peer: load them before the
-    // cluster handshake (their completion is local)
-    const int nb = n0 + p * BNH;
-    for (int j = 0; j < min(nkb, STAGES); j++) {
-      tc::mbar_arrive_expect_tx(&S.full[j], A_TILE + B_TILE);
-      const int k0 = (kb0 + j) * BK;
-      tc::tma_load_2d(S.a_raw[j], &tm_a, &S.full[j], k0, m0);
-#pragma unroll
-      for (int at = 0; at < BNH / 32; at++)
-        tc::tma_load_2d(S.b_raw[j] + at * B_ATOM, &tm_b, &S.full[j], nb + 32 * at, k0);
-    }
-  }
-  if (warp == 1) tc::tmem_alloc_pair<TMEM_COLS>(&S.tmem_base);
-  tc::tc_fence_before();
-  tc::cluster_sync();  // barriers and TMEM of both CTAs are set up
-  tc::tc_fence_after();
-  const uint32_t tmem_d = S.tmem_base;
-  if (threadIdx.x == 0) MM_T(1);
-
-  if (warp == 0) {
-    // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const int nb = n0 + p * BNH;
-      for (int j = STAGES; j < nkb; j++) {
-        const int s = j % STAGES;
-        tc::mbar_wait(&S.empty[s], ((j / STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&S.full[s], A_TILE + B_TILE);
-        const int k0 = (kb0 + j) * BK;
-        tc::tma_load_2d(S.a_raw[s], &tm_a, &S.full[s], k0, m0);
-#pragma unroll
-        for (int at = 0; at < BNH / 32; at++)
-          tc::tma_load_2d(S.b_raw[s] + at * B_ATOM, &tm_b, &S.full[s], nb + 32 * at, k0);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------------------------------ MMA issuer (even CTA)
-    if (p == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(2 * BM, BNP, /*a MN-major*/ 0, /*b MN-major*/ 1);
-      for (int j = 0; j < nkb; j++) {
-        const int s = j % STAGES, ls = j % LO_STAGES;
-        {
-          MM_ACC_BEGIN;
-          tc::mbar_wait_cluster(&S.conv[ls], (j / LO_STAGES) & 1);
-          if (lane == 0 && j > 0) MM_ACC(10);
-        }
-        tc::tc_fence_after();
-        if (lane == 0) {
-          if (j == 0) MM_T(3);
-          const uint32_t ahi = tc::smem_u32(S.a_raw[s]), alo = tc::smem_u32(S.a_lo[ls]);
-          const uint32_t bhi = tc::smem_u32(S.b_raw[s]), blo = tc::smem_u32(S.b_lo[ls]);
-#pragma unroll
-          for (int k = 0; k < BK / 8; k++) {
-            const uint64_t da_hi = tc::smem_desc_sw128(ahi + k * 32, 16, 1024);
-            const uint64_t da_lo = tc::smem_desc_sw128(alo + k * 32, 16, 1024);
-            const uint64_t db_hi = mm::desc_b_mn(bhi + k * 1024);
-            const uint64_t db_lo = mm::desc_b_mn(blo + k * 1024);
-            tc::mma_tf32_pair(tmem_d, da_hi, db_hi, idesc, (j | k) != 0);
-            tc::mma_tf32_pair(tmem_d, da_hi, db_lo, idesc, 1);
-#if MM_A_TMEM
-            (void)da_lo;
-            tc::mma_tf32_pair_ts(tmem_d, tmem_d + ALO_COL + ls * BK + k * 8, db_hi, idesc, 1);
-#else
-            tc::mma_tf32_pair(tmem_d, da_lo, db_hi, idesc, 1);
-#endif
-          }
-          tc::mma_commit_pair(&S.empty[s], 3);
-          tc::mma_commit_pair(&S.lo_empty[ls], 3);
-          if (j == nkb - 1) {
-            tc::mma_commit_pair(&S.tmem_full, 3);
-            MM_T(4);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ------------------------------------------------------ converters
-    const int ct = threadIdx.x - 64;
-    const uint32_t conv_remote0 = tc::mapa(tc::smem_u32(&S.conv[0]), 0);
-    for (int j = 0; j < nkb; j++) {
-      const int s = j % STAGES, ls = j % LO_STAGES;
-      tc::mbar_wait(&S.full[s], (j / STAGES) & 1);
-      if (j == 0 && ct == 0) MM_T(2);
-      {
-        MM_ACC_BEGIN;
-        if (j >= LO_STAGES) tc::mbar_wait(&S.lo_empty[ls], ((j / LO_STAGES) - 1) & 1);
-        if (ct == 0) MM_ACC(11);
-      }
-      const float4 *ar = reinterpret_cast<const float4 *>(S.a_raw[s]);
-      const float4 *br = reinterpret_cast<const float4 *>(S.b_raw[s]);
-      float4 *al = reinterpret_cast<float4 *>(S.a_lo[ls]);
-      float4 *bl = reinterpret_cast<float4 *>(S.b_lo[ls]);
-      float4 vb[B_TILE / 16 / CONVERTERS];
-#if MM_A_TMEM
-      // A: thread = row 32q + lane of its TMEM lane quarter, k chunks 4h..4h+3
-      // of the 128B-swizzled K-major row (16B chunk c sits at c ^ (row & 7))
-      float4 va[4];
-      {
-        const int rq = warp & 3, hh = (warp - 2) >> 2, r = rq * 32 + lane;
-        const uint8_t *rowp = S.a_raw[s] + r * 128;
-#pragma unroll
-        for (int i = 0; i < 4; i++) va[i] = *reinterpret_cast<const float4 *>(rowp + (((4 * hh + i) ^ (r & 7)) << 4));
-      }
-#else
-      float4 va[A_TILE / 16 / CONVERTERS];
-#pragma unroll
-      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++) va[i] = ar[ct + i * CONVERTERS];
-#endif
-#pragma unroll
-      for (int i = 0; i < B_TILE / 16 / CONVERTERS; i++) vb[i] = br[ct + i * CONVERTERS];
-#if MM_A_TMEM
-      {
-        uint32_t lo[16];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          lo[4 * i] = __float_as_uint(mm::tf32_residual(va[i].x));
-          lo[4 * i + 1] = __float_as_uint(mm::tf32_residual(va[i].y));
-          lo[4 * i + 2] = __float_as_uint(mm::tf32_residual(va[i].z));
-          lo[4 * i + 3] = __float_as_uint(mm::tf32_residual(va[i].w));
-        }
-        const int rq = warp & 3, hh = (warp - 2) >> 2;
-        tc::tmem_st_32x32b_x16(tmem_d + ((uint32_t)(rq * 32) << 16) + ALO_COL + ls * BK + 16 * hh, lo);
-        (void)al;
-      }
-#else
-#pragma unroll
-      for (int i = 0; i < A_TILE / 16 / CONVERTERS; i++)
-        al[ct + i * CONVERTERS] = make_float4(mm::tf32_residual(va[i].x), mm::tf32_residual(va[i].y),
-                                              mm::tf32_residual(va[i].z), mm::tf32_residual(va[i].w));
-#endif
-#pragma unroll
-      for (int i = 0; i < B_TILE / 16 / CONVERTERS; i++)
-        bl[ct + i * CONVERTERS] = make_float4(mm::tf32_residual(vb[i].x), mm::tf32_residual(vb[i].y),
-                                              mm::tf32_residual(vb[i].z), mm::tf32_residual(vb[i].w));
-      tc::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
-#if MM_A_TMEM
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-#endif
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(conv_remote0 + ls * 8);
-    }
-
-    // ---------------------------------------------------- epilogue
-    // warps 2..9: TMEM lane quarter q = warp & 3, column half h (two warps
-    // per quarter); thread = row (32q + lane), 16 columns per chunk
-    tc::mbar_wait(&S.tmem_full, 0);
-    tc::tc_fence_after();
-    if (ct == 0) MM_T(5);
-    const int q = warp & 3, h = (warp - 2) >> 2;
-    constexpr int OWN = CHUNKS / SPLITK;  // 16-column chunks each split finishes
-    constexpr int GRP = OWN * 512;        // floats of one (quarter, owner) block: OWN chunks x 32 rows x 16
-    // scratch layout [tile][split][p][q][chunk][v][lane] float4s: the OWN
-    // chunks of one quarter that one owner needs are one contiguous block,
-    // moved by one bulk copy each way (TMA engine, not per-thread stores)
-    float *mine = part + (size_t)((tile * SPLITK + sk) * 2 + p) * PART_FLOATS;
-    unsigned *arrive = cnt + (tile * 2 + p) * 2, *depart = arrive + 1;
-    float *smf = reinterpret_cast<float *>(S.a_raw[0]);  // operand smem, idle now
-    if (SPLITK > 1) {
-      // phase A: warp (q, h) stages the owner groups g in its column half
-      // that this split does not own and bulk-stores each one
-      constexpr int GPW = SPLITK / 2;  // owner groups per column half
-      float *stage_w = smf + (size_t)(warp - 2) * GPW * GRP;
-#pragma unroll 1
-      for (int gi = 0; gi < GPW; gi++) {
-        const int g = h * GPW + gi;
-        if (g == sk) continue;
-        float4 *st4 = reinterpret_cast<float4 *>(stage_w + gi * GRP);
-#pragma unroll
-        for (int c2 = 0; c2 < OWN; c2 += 2) {
-          uint32_t r[2][16];
-          tc::tmem_ld_32x32b_x16(tmem_d + ((uint32_t)(q * 32) << 16) + (g * OWN + c2) * 16, r[0]);
-          tc::tmem_ld_32x32b_x16(tmem_d + ((uint32_t)(q * 32) << 16) + (g * OWN + c2 + 1) * 16, r[1]);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int u = 0; u < 2; u++)
-#pragma unroll
-            for (int v = 0; v < 4; v++)
-              st4[((c2 + u) * 4 + v) * 32 + lane] =
-                  make_float4(__uint_as_float(r[u][4 * v]), __uint_as_float(r[u][4 * v + 1]),
-                              __uint_as_float(r[u][4 * v + 2]), __uint_as_float(r[u][4 * v + 3]));
-        }
-        tc::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tc::bulk_store(mine + (size_t)(q * CHUNKS + g * OWN) * 512, st4, GRP * 4);
-          tc::bulk_commit();
-        }
-      }
-      if (lane == 0) {
-        tc::bulk_wait<0>();  // this warp's partials are in global memory
-        tc::fence_proxy_async_global();
-      }
-      epi_bar();
-      if (ct == 0) {
-        MM_T(6);
-        __threadfence();
-        red_release_add(arrive, 1u);
-        while (ld_acquire(arrive) < (unsigned)SPLITK) __nanosleep(32);
-        __threadfence();
-        MM_T(7);
-        // phase B input: the other splits' blocks of the owned group, every quarter
-        tc::fence_proxy_async_global();
-        tc::mbar_arrive_expect_tx(&S.red_full, (SPLITK - 1) * 4 * GRP * 4);
-        for (int t = 0, o = 0; t < SPLITK; t++) {
-          if (t == sk) continue;
-          const float *src = part + (size_t)((tile * SPLITK + t) * 2 + p) * PART_FLOATS;
-          for (int qq = 0; qq < 4; qq++)
-            tc::bulk_load(smf + (size_t)(o * 4 + qq) * GRP, src + (size_t)(qq * CHUNKS + sk * OWN) * 512, GRP * 4,
-                          &S.red_full);
-          o++;
-        }
-      }
-      tc::mbar_wait(&S.red_full, 0);
-    }
-    // own columns: sum the SPLITK partials in split order into a staging
-    // tile, then coalesced row stores to C
-    constexpr int SPITCH = OWN * 16 + 4;  // 16-byte stores of 32 rows hit 8 bank groups
-    float *stg = smf + (SPLITK - 1) * 4 * GRP;
-    const int row = q * 32 + lane;
-    static_assert(OWN % 2 == 0, "two warps per TMEM lane quarter split the owned chunks");
-#pragma unroll
-    for (int i = 0; i < OWN / 2; i++) {
-      const int cl = h + 2 * i, cb = sk * OWN + cl;
-      uint32_t r[16];
-      tc::tmem_ld_32x32b_x16(tmem_d + ((uint32_t)(q * 32) << 16) + cb * 16, r);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int v = 0; v < 4; v++) {
-        const float4 own = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                       __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-        float4 acc = own;
-        bool first = true;
-#pragma unroll
-        for (int t = 0; t < SPLITK; t++) {
-          float4 x = own;
-          if (t != sk) {
-            const int o = t < sk ? t : t - 1;
-            x = reinterpret_cast<const float4 *>(smf + (size_t)(o * 4 + q) * GRP)[(cl * 4 + v) * 32 + lane];
-          }
-          if (first) {
-            acc = x;
-            first = false;
-          } else {
-            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-          }
-        }
-        *reinterpret_cast<float4 *>(stg + row * SPITCH + cl * 16 + 4 * v) = acc;
-      }
-    }
-    epi_bar();
-    {
-      constexpr int C4 = OWN * 4;  // float4s per staged row
-      const bool vec = (N & 3) == 0;
-      const int gc0 = n0 + sk * OWN * 16;
-#pragma unroll 4
-      for (int idx = ct; idx < BM * C4; idx += CONVERTERS) {
-        const int r = idx / C4, c4 = (idx % C4) * 4;
-        const int grow = m0 + r, gcol = gc0 + c4;
-        if (grow >= M) continue;
-        const float4 v = *reinterpret_cast<const float4 *>(stg + r * SPITCH + c4);
-        float *dst = c + (size_t)grow * N + gcol;
-        if (vec && gcol + 4 <= N) {
-          *reinterpret_cast<float4 *>(dst) = v;
-        } else {
-          const float e[4] = {v.x, v.y, v.z, v.w};
-          for (int k = 0; k < 4; k++)
-            if (gcol + k < N) dst[k] = e[k];
-        }
-      }
-    }
-    if (SPLITK > 1) {
-      epi_bar();  // every thread of this CTA has read the scratch
-      if (ct == 0) {
-        // the last split out returns the tile's counters to zero for the
-        // next call (stream order separates calls)
-        if (atomicAdd(depart, 1u) == (unsigned)SPLITK - 1) {
-          *reinterpret_cast<volatile unsigned *>(arrive) = 0u;
-          *reinterpret_cast<volatile unsigned *>(depart) = 0u;
-        }
-      }
-    }
-    if (ct == 0) MM_T(8);
-  }
-  tc::tc_fence_before();
-  tc::cluster_sync();  // both CTAs are done with TMEM
-  if (warp == 1) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc_pair<TMEM_COLS>(tmem_d);
-  }
-}
-
-}  // namespace mm2
 
 // exact SIMT path: the oracle's sequential k order with single roundings
 __global__ void matmul_exact_kernel(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ c,
@@ -839,102 +444,6 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     mc.valid = true;
   }
   const CUtensorMap &m_a = mc.ma, &m_b = mc.mb;
-  {
-    // CTA-pair kernel: split K over the cluster so the pair tiles fill the
-    // SMs (each split keeps >= 2 k-blocks); JB_MM_PAIR=0 selects the
-    // single-CTA kernel below (A/B experiments)
-    static const bool pair_on = [] {
-      const char *e = getenv("JB_MM_PAIR");
-      return e && e[0] == '1';
-    }();
-    // pair tile width: 256 (split-K 4 at 1024^3), or 128;
-    // JB_MM_BNP=128/256 forces one (A/B experiments)
-    static const int bnp_env = [] {
-      const char *e = getenv("JB_MM_BNP");
-      return e ? atoi(e) : 0;
-    }();
-    const long long tiles_m = (long long)((n + 2 * mm2::BM - 1) / (2 * mm2::BM));
-    const int kbl = (int)((m + mm2::BK - 1) / mm2::BK);
-    const int sms = sm_count();
-    // the splits of a tile wait for each other: the whole grid must be
-    // resident at once (one CTA per SM), else the single-CTA kernel runs
-    auto pick = [&](int bnp, int &sk) {
-      const long long pt = tiles_m * (long long)((l + bnp - 1) / bnp);
-      sk = 0;
-      if (pt * 8 <= sms && kbl >= 8) sk = 4;
-      else if (pt * 4 <= sms && kbl >= 4) sk = 2;
-      else if (pt * 2 <= sms) sk = 1;
-      return pt;
-    };
-    int sk = 0, bnp = bnp_env == 128 ? 128 : 256;
-    long long ptiles = pick(bnp, sk);
-    // (256-wide tiles with split-K 4 beat 128-wide tiles with split-K 2 at
-    // 1024^3: the narrower pair MMA is shared-memory bound, 16 vs 9 us of
-    // main loop, which outweighs the smaller partial exchange)
-    const int tiles_n = (int)((l + bnp - 1) / bnp);
-    const size_t part_bytes = (size_t)ptiles * sk * 2 * mm2::BM * bnp * 4;
-    const size_t cnt_bytes = (size_t)ptiles * 4 * sizeof(unsigned);
-    float *part = nullptr;
-    unsigned *cnt = nullptr;
-    bool async_scratch = false;  // a caller's capture: stream-ordered scratch inside the graph
-    if (pair_on && sk > 1) {
-      part = (float *)workspace(part_bytes, s);
-      cnt = part ? (unsigned *)zeroed_counters(/*tag*/ 1, cnt_bytes, s) : nullptr;
-      if (!part || !cnt) {
-        cudaStreamCaptureStatus cs0 = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(s, &cs0) != cudaSuccess || cs0 == cudaStreamCaptureStatusNone) return JB_ECUDA;
-        JB_CHECK_CUDA(cudaMallocAsync((void **)&part, part_bytes, s));
-        JB_CHECK_CUDA(cudaMallocAsync((void **)&cnt, cnt_bytes, s));
-        JB_CHECK_CUDA(cudaMemsetAsync(cnt, 0, cnt_bytes, s));
-        async_scratch = true;
-      }
-    }
-    if (pair_on && sk > 0) {
-      static bool pair_attr[64][6] = {};
-      const int si = (sk == 4 ? 2 : sk == 2 ? 1 : 0) + (bnp == 128 ? 3 : 0);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(ptiles * 2 * sk));
-      cfg.blockDim = dim3(mm2::THREADS);
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 2;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      void *tok = prof_begin("matmul_tcgen05", s);
-#define MM2_LAUNCH(BNP_, SK)                                                                              \
-  do {                                                                                                    \
-    cfg.dynamicSmemBytes = mm2::PairCfg<BNP_>::SMEM_BYTES;                                                \
-    if (!pair_attr[cdev][si]) {                                                                           \
-      JB_CHECK_CUDA(cudaFuncSetAttribute(mm2::gemm_3xtf32_pair_kernel<BNP_, SK>,                         \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
-                                         (int)mm2::PairCfg<BNP_>::SMEM_BYTES));                           \
-      pair_attr[cdev][si] = true;                                                                         \
-    }                                                                                                     \
-    JB_CHECK_CUDA(cudaLaunchKernelEx(&cfg, mm2::gemm_3xtf32_pair_kernel<BNP_, SK>, m_a, m_b, res, (int)n, \
-                                     (int)l, (int)m, tiles_n, part, cnt));                                \
-  } while (0)
-      if (bnp == 256) {
-        if (sk == 4) MM2_LAUNCH(256, 4);
-        else if (sk == 2) MM2_LAUNCH(256, 2);
-        else MM2_LAUNCH(256, 1);
-      } else {
-        if (sk == 4) MM2_LAUNCH(128, 4);
-        else if (sk == 2) MM2_LAUNCH(128, 2);
-        else MM2_LAUNCH(128, 1);
-      }
-#undef MM2_LAUNCH
-      prof_end(tok, s);
-      if (async_scratch) {
-        JB_CHECK_CUDA(cudaFreeAsync(part, s));
-        JB_CHECK_CUDA(cudaFreeAsync(cnt, s));
-      }
-      JB_LAUNCHED("matmul_tcgen05");
-      return JB_OK;
-    }
-  }
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);

@@ -10,7 +10,6 @@
 
 #include <atomic>
 #include <map>
-#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -109,44 +108,6 @@ void *workspace(size_t bytes, cudaStream_t s) {
   }
   a.cap = want;
   return a.ptr;
-}
-
-struct Counters {
-  void *ptr = nullptr;
-  size_t cap = 0;
-};
-static std::map<std::tuple<int, cudaStream_t, int>, Counters> g_counters;
-
-void *zeroed_counters(int tag, size_t bytes, cudaStream_t s) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return nullptr;
-  std::lock_guard<std::mutex> lk(g_arena_mu);
-  Counters &c = g_counters[{dev, s, tag}];
-  if (bytes <= c.cap) return c.ptr;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    set_error("counter block must grow to %zu bytes while the stream is capturing; "
-              "run the call once outside the capture first", bytes);
-    return nullptr;
-  }
-  if (c.ptr) {
-    cudaStreamSynchronize(s);
-    cudaFree(c.ptr);
-    c.ptr = nullptr;
-    c.cap = 0;
-  }
-  const size_t want = (bytes + 4095) & ~size_t(4095);
-  if (cudaMalloc(&c.ptr, want) != cudaSuccess || cudaMemset(c.ptr, 0, want) != cudaSuccess ||
-      cudaDeviceSynchronize() != cudaSuccess) {
-    cudaGetLastError();
-    if (c.ptr) cudaFree(c.ptr);
-    c.ptr = nullptr;
-    set_error("counter block: cudaMalloc/cudaMemset(%zu) failed", want);
-    return nullptr;
-  }
-  c.cap = want;
-  return c.ptr;
 }
 
 jb_status after_launch(const char *what) {
