@@ -21,7 +21,15 @@
 //  * newly claimed vertices go to a block-local queue in shared memory
 //    (shared-memory atomics), then one global atomicAdd per block reserves
 //    space in the next frontier (block-aggregated atomics);
-//  * a grid-wide barrier (cooperative groups) separates levels.
+//  * large levels skip the queue altogether ("dense output"): a claim is a
+//    level-byte check in L2 + a plain byte store (every writer of a vertex
+//    in one level writes the same level, so the race is benign) + a
+//    fire-and-forget red.or on the bitmap filter, no claiming atomics, no
+//    block barriers; the next level finds its frontier by scanning the
+//    level bytes (16 MiB, L2-resident), warps work independently;
+//  * one grid-wide barrier (cooperative groups) per level: the frontier
+//    sizes rotate through three counters, so the one two levels ahead is
+//    cleared while the current one is read.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -39,6 +47,9 @@ constexpr int LQ = 4096;  // block-local queue capacity
 #ifndef BFS_VPT
 #define BFS_VPT 2
 #endif
+#ifndef BFS_DENSE_SHIFT
+#define BFS_DENSE_SHIFT 3  // queue-less output for frontiers >= n / 2^shift
+#endif
 constexpr int EB = BFS_EB;       // edges per lane per batch
 constexpr int CAP = 32 * EB;     // per-warp edge-id buffer (one batch)
 constexpr int VPT = BFS_VPT;  // frontier vertices per thread per round
@@ -50,11 +61,15 @@ struct Args {
   uint8_t *level;     // [n] level byte (kUnseen / level / kDeep: see cost[])
   uint32_t *visited;  // bitmap
   uint32_t *q[2];     // frontier queues
-  uint32_t *qsize;    // [4]: size of q[0], q[1] (+ padding)
+  uint32_t *qsize;    // [8]: frontier sizes, slot level % 3; compaction counts at 4 + level % 2
   uint32_t n;
 };
 
-__device__ __forceinline__ void enqueue(const Args &a, uint32_t v, int nxt, uint32_t *lq, uint32_t &lcount,
+__device__ __forceinline__ void red_or(uint32_t *p, uint32_t v) {
+  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void enqueue(uint32_t *nsize, uint32_t v, uint32_t *lq, uint32_t &lcount,
                                         uint32_t *nq) {
   const uint32_t slot = atomicAdd(&lcount, 1u);
   if (slot < LQ) {
@@ -63,11 +78,26 @@ __device__ __forceinline__ void enqueue(const Args &a, uint32_t v, int nxt, uint
     const uint32_t mask = __activemask();
     const int leader = __ffs(mask) - 1;
     uint32_t base = 0;
-    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(a.qsize + nxt, __popc(mask));
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(nsize, __popc(mask));
     base = __shfl_sync(mask, base, leader);
     nq[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = v;
   }
 }
+
+#ifdef BFS_TRACE
+// per-level globaltimer stamps of block 0 (tools/bfs_trace.py)
+__device__ unsigned long long g_bfs_trace[64];
+#define BFS_T(level)                                                               \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (level) < 64) {                     \
+      unsigned long long t;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                        \
+      g_bfs_trace[level] = t;                                                      \
+    }                                                                              \
+  } while (0)
+#else
+#define BFS_T(level) do {} while (0)
+#endif
 
 __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
@@ -76,109 +106,235 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
   __shared__ uint32_t ebuf[THREADS / 32][CAP];
   const uint32_t gtid = blockIdx.x * THREADS + threadIdx.x;
   const uint32_t gsize = gridDim.x * THREADS;
-
+  const uint32_t gwarp = gtid >> 5, nwarps = gsize >> 5;
+  const int lane = threadIdx.x & 31;
+  uint32_t *eb = ebuf[threadIdx.x >> 5];
+  bool scan_in = false;  // this level's frontier is "level byte == level" (the previous level wrote no queue)
   for (int level = 0;; level++) {
-    const int cur = level & 1, nxt = cur ^ 1;
-    const uint32_t fsize = *((volatile uint32_t *)&a.qsize[cur]);
+    BFS_T(level);
+    const int qc = level & 1, qn = qc ^ 1;                        // queue buffers
+    const int sc = level % 3, sn = (level + 1) % 3, sf = (level + 2) % 3;  // size slots
+    const uint32_t fsize = *((volatile uint32_t *)&a.qsize[sc]);
     if (fsize == 0) break;
-    const uint32_t *fq = a.q[cur];
-    uint32_t *nq = a.q[nxt];
+    if (gtid == 0) {
+      a.qsize[sf] = 0;                     // last read as the previous level's "current" (before the barrier)
+      a.qsize[4 + ((level + 1) & 1)] = 0;  // the next level's compaction count, last read a level ago
+    }
+    const uint32_t *fq = a.q[qc];
+    uint32_t *nq = a.q[qn];
+    uint32_t *nsize = a.qsize + sn;
     const int32_t nl = level + 1;
     const uint8_t nb = nl < kDeep ? (uint8_t)nl : kDeep;
-    // Dense levels (a large share of all vertices in the frontier) scan the
-    // level bytes in vertex order instead of reading the queue: the node
-    // records and edge lists are then read nearly sequentially (coalesced)
-    // instead of one random sector pair per vertex.
-    const bool scan = level < kDeep && fsize > (a.n >> 2);
-    const uint32_t work = scan ? a.n : fsize;
-    // uniform trip count across the block so __syncthreads stays legal;
-    // VPT vertices per thread per round, their record loads issued together
-    const uint32_t per_round = gsize * VPT;
-    const uint32_t rounds = (work + per_round - 1) / per_round;
-    for (uint32_t r = 0; r < rounds; r++) {
-      if (threadIdx.x == 0) lcount = 0;
-      __syncthreads();
-      uint32_t e0[VPT], ne[VPT];
+    const uint8_t lb = (uint8_t)level;
+    // scan-in: the frontier is "level byte == level" (read in vertex order:
+    // node records and edge lists stream nearly sequentially)
+    bool scan = scan_in || (level < kDeep && fsize > (a.n >> 2));
+    uint32_t work = scan ? a.n : fsize;
+    if (scan_in && fsize <= (a.n >> 2)) {
+      // a small frontier after a queue-less level: compact its level bytes
+      // into the queue first (16 bytes per lane per load), then run it as a
+      // queue -- walking all n vertices would pay one dependent chain of
+      // loads per 64 vertices per warp
+      uint32_t *cnt = a.qsize + 4 + (level & 1);
+      uint32_t *cq = a.q[qc];
+      const uint32_t n16 = a.n >> 4;
+      for (uint32_t i0 = 0; i0 < n16 + 1; i0 += gsize) {  // uniform trip count: whole warps shuffle
+        const uint32_t i = i0 + gtid;
+        uint32_t hits[16];
+        int nh = 0;
+        if (i < n16) {
+          const uint4 b = __ldcg(reinterpret_cast<const uint4 *>(a.level) + i);
+          const uint32_t wds[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        const uint32_t i = r * per_round + k * gsize + gtid;
-        ne[k] = 0;
-        e0[k] = 0;
-        if (i < work) {
-          bool live = true;
-          uint32_t u = i;
-          if (scan) live = __ldcg(a.level + i) == (uint8_t)level;
-          else u = __ldcg(fq + i);
-          if (live) {
-            e0[k] = __ldg(a.starting + u);
-            ne[k] = __ldg(a.nedges + u);
-          }
+          for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int y = 0; y < 4; y++)
+              if (((wds[q] >> (8 * y)) & 0xffu) == lb) hits[nh++] = 16 * i + 4 * q + y;
+        } else if (i == n16) {  // the tail bytes
+          for (uint32_t v = 16 * n16; v < a.n; v++)
+            if (__ldcg(a.level + v) == lb) hits[nh++] = v;
         }
-      }
-      // warp-cooperative expansion: the warp's adjacency ranges are laid out
-      // back to back in a per-warp buffer of edge ids (a warp scan gives each
-      // range its offset), then all 32 lanes walk the buffer together --
-      // balanced across lanes whatever the degrees, and consecutive lanes
-      // read consecutive edges.  Ranges longer than the buffer continue in
-      // the next pass.
-      uint32_t *eb = ebuf[threadIdx.x >> 5];
-      const int lane = threadIdx.x & 31;
+        // warp-aggregated append
+        uint32_t inc = nh;
 #pragma unroll
-      for (int k = 0; k < VPT; k++) {
-        uint32_t cur = e0[k];
-        const uint32_t end = e0[k] + ne[k];
-#pragma unroll 1
-        for (;;) {
-          const uint32_t rem = min(end - cur, (uint32_t)CAP);
-          uint32_t inc = rem;
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += t;
-          }
-          const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-          if (total == 0) break;
-          const uint32_t off = inc - rem;
-          const uint32_t take = off >= (uint32_t)CAP ? 0u : min(rem, (uint32_t)CAP - off);
-          for (uint32_t j = 0; j < take; j++) eb[off + j] = cur + j;
-          cur += take;
-          __syncwarp();
-          const uint32_t cnt = min(total, (uint32_t)CAP);
-#pragma unroll 1
-          for (uint32_t b = 0; b < cnt; b += 32 * EB) {
-            uint32_t v[EB], w[EB];
-#pragma unroll
-            for (int j = 0; j < EB; j++) {
-              const uint32_t i = b + j * 32 + lane;
-              v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
-            }
-            // probes may come from L1 (stale only towards "unseen": the
-            // atomicOr below re-checks)
-#pragma unroll
-            for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
-#pragma unroll
-            for (int j = 0; j < EB; j++) {
-              if (v[j] == 0xffffffffu) continue;
-              const uint32_t bit = 1u << (v[j] & 31);
-              if (w[j] & bit) continue;
-              const uint32_t old = atomicOr(a.visited + (v[j] >> 5), bit);
-              if (old & bit) continue;  // someone else claimed v
-              a.level[v[j]] = nb;
-              if (nb == kDeep) a.cost[v[j]] = nl;
-              enqueue(a, v[j], nxt, lq, lcount, nq);
-            }
-          }
-          __syncwarp();
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += t;
         }
+        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        uint32_t base = 0;
+        if (lane == 31 && total) base = atomicAdd(cnt, total);
+        base = __shfl_sync(0xffffffffu, base, 31) + inc - nh;
+        for (int h = 0; h < nh; h++) cq[base + h] = hits[h];
       }
-      __syncthreads();
-      const uint32_t cnt = min(lcount, (uint32_t)LQ);
-      if (threadIdx.x == 0 && cnt) lbase = atomicAdd(a.qsize + nxt, cnt);
-      __syncthreads();
-      for (uint32_t k = threadIdx.x; k < cnt; k += THREADS) nq[lbase + k] = lq[k];
+      grid.sync();
+      work = *((volatile uint32_t *)cnt);
+      fq = cq;
+      scan = false;
     }
-    grid.sync();
-    if (gtid == 0) a.qsize[cur] = 0;  // consumed; becomes the next-next queue
+    // dense output: a large frontier writes only level bytes, the next level scans
+    const bool dense = nl < kDeep - 1 && fsize >= (a.n >> BFS_DENSE_SHIFT);
+
+    if (dense) {
+      // ---------------- warps independent: no queue, no block barrier
+      uint32_t claimed = 0;
+      for (uint32_t base = gwarp * (32u * VPT); base < work; base += nwarps * (32u * VPT)) {
+        uint32_t e0[VPT], ne[VPT];
+#pragma unroll
+        for (int k = 0; k < VPT; k++) {
+          const uint32_t i = base + k * 32 + lane;
+          ne[k] = 0;
+          e0[k] = 0;
+          if (i < work) {
+            bool live = true;
+            uint32_t u = i;
+            if (scan) live = __ldcg(a.level + i) == lb;
+            else u = __ldcg(fq + i);
+            if (live) {
+              e0[k] = __ldg(a.starting + u);
+              ne[k] = __ldg(a.nedges + u);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < VPT; k++) {
+          uint32_t cur = e0[k];
+          const uint32_t end = e0[k] + ne[k];
+#pragma unroll 1
+          for (;;) {
+            const uint32_t rem = min(end - cur, (uint32_t)CAP);
+            uint32_t inc = rem;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+              if (lane >= d) inc += t;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            if (total == 0) break;
+            const uint32_t off = inc - rem;
+            const uint32_t take = off >= (uint32_t)CAP ? 0u : min(rem, (uint32_t)CAP - off);
+            for (uint32_t j = 0; j < take; j++) eb[off + j] = cur + j;
+            cur += take;
+            __syncwarp();
+            const uint32_t cnt = min(total, (uint32_t)CAP);
+#pragma unroll 1
+            for (uint32_t b = 0; b < cnt; b += 32 * EB) {
+              uint32_t v[EB], w[EB];
+#pragma unroll
+              for (int j = 0; j < EB; j++) {
+                const uint32_t i = b + j * 32 + lane;
+                v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
+              }
+              // bitmap filter (may be stale towards "unseen": L1, lost races)
+#pragma unroll
+              for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
+              // the level byte in L2 decides; claims are plain stores
+              uint8_t lv[EB];
+#pragma unroll
+              for (int j = 0; j < EB; j++)
+                lv[j] = (v[j] != 0xffffffffu && !(w[j] & (1u << (v[j] & 31)))) ? __ldcg(a.level + v[j]) : (uint8_t)0;
+#pragma unroll
+              for (int j = 0; j < EB; j++) {
+                if (lv[j] != kUnseen) continue;
+                a.level[v[j]] = nb;
+                red_or(a.visited + (v[j] >> 5), 1u << (v[j] & 31));
+                claimed++;
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      // the count may include a vertex claimed twice in this level: it only
+      // steers the next level's mode
+      const uint32_t wc = warp_sum(claimed);
+      if (lane == 0 && wc) atomicAdd(nsize, wc);
+    } else {
+      // ---------------- queue output (claiming atomics, block-local queues)
+      const uint32_t per_round = gsize * VPT;
+      const uint32_t rounds = (work + per_round - 1) / per_round;
+      for (uint32_t r = 0; r < rounds; r++) {
+        if (threadIdx.x == 0) lcount = 0;
+        __syncthreads();
+        uint32_t e0[VPT], ne[VPT];
+#pragma unroll
+        for (int k = 0; k < VPT; k++) {
+          const uint32_t i = r * per_round + k * gsize + gtid;
+          ne[k] = 0;
+          e0[k] = 0;
+          if (i < work) {
+            bool live = true;
+            uint32_t u = i;
+            if (scan) live = __ldcg(a.level + i) == lb;
+            else u = __ldcg(fq + i);
+            if (live) {
+              e0[k] = __ldg(a.starting + u);
+              ne[k] = __ldg(a.nedges + u);
+            }
+          }
+        }
+        // warp-cooperative expansion: the warp's adjacency ranges are laid out
+        // back to back in a per-warp buffer of edge ids (a warp scan gives each
+        // range its offset), then all 32 lanes walk the buffer together --
+        // balanced across lanes whatever the degrees, and consecutive lanes
+        // read consecutive edges.  Ranges longer than the buffer continue in
+        // the next pass.
+#pragma unroll
+        for (int k = 0; k < VPT; k++) {
+          uint32_t cur = e0[k];
+          const uint32_t end = e0[k] + ne[k];
+#pragma unroll 1
+          for (;;) {
+            const uint32_t rem = min(end - cur, (uint32_t)CAP);
+            uint32_t inc = rem;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+              if (lane >= d) inc += t;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            if (total == 0) break;
+            const uint32_t off = inc - rem;
+            const uint32_t take = off >= (uint32_t)CAP ? 0u : min(rem, (uint32_t)CAP - off);
+            for (uint32_t j = 0; j < take; j++) eb[off + j] = cur + j;
+            cur += take;
+            __syncwarp();
+            const uint32_t cnt = min(total, (uint32_t)CAP);
+#pragma unroll 1
+            for (uint32_t b = 0; b < cnt; b += 32 * EB) {
+              uint32_t v[EB], w[EB];
+#pragma unroll
+              for (int j = 0; j < EB; j++) {
+                const uint32_t i = b + j * 32 + lane;
+                v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
+              }
+              // probes may come from L1 (stale only towards "unseen": the
+              // atomicOr below re-checks)
+#pragma unroll
+              for (int j = 0; j < EB; j++) w[j] = v[j] != 0xffffffffu ? a.visited[v[j] >> 5] : 0xffffffffu;
+#pragma unroll
+              for (int j = 0; j < EB; j++) {
+                if (v[j] == 0xffffffffu) continue;
+                const uint32_t bit = 1u << (v[j] & 31);
+                if (w[j] & bit) continue;
+                const uint32_t old = atomicOr(a.visited + (v[j] >> 5), bit);
+                if (old & bit) continue;  // someone else claimed v
+                a.level[v[j]] = nb;
+                if (nb == kDeep) a.cost[v[j]] = nl;
+                enqueue(nsize, v[j], lq, lcount, nq);
+              }
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        const uint32_t cnt = min(lcount, (uint32_t)LQ);
+        if (threadIdx.x == 0 && cnt) lbase = atomicAdd(nsize, cnt);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < cnt; k += THREADS) nq[lbase + k] = lq[k];
+      }
+    }
+    scan_in = dense;
     grid.sync();
   }
 }
@@ -192,6 +348,9 @@ __global__ void bfs_init_kernel(uint8_t *level, uint32_t *visited, uint32_t n, u
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     qsize[0] = 1;
     qsize[1] = 0;
+    qsize[2] = 0;
+    qsize[4] = 0;
+    qsize[5] = 0;
     q0[0] = source;
   }
 }
@@ -233,6 +392,12 @@ __global__ void bfs_expand_kernel(const uint8_t *level, int32_t *cost, uint32_t 
 
 using namespace jb;
 using namespace jb::bfs;
+
+#ifdef BFS_TRACE
+extern "C" JB_API void jb_bfs_trace(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, jb::bfs::g_bfs_trace, sizeof(jb::bfs::g_bfs_trace));
+}
+#endif
 
 extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, const uint32_t *nedges,
                             const uint32_t *edges, uint32_t source, int32_t *cost, void *stream) {
