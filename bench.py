@@ -242,10 +242,13 @@ class EdgeWorkload:
                                    [self.frames_host, *self.filters[:4], self.theta])
 
     def e2e_bytes(self):
-        return self.local * self.frame_bytes, self.local * self.frame_bytes
+        # D2H: the edge maps cross PCIe bit-packed (ceil(n*m/32) words per
+        # frame) and are expanded to f32 on the host inside the timed call
+        return self.local * self.frame_bytes, self.local * ((self.n * self.m + 31) // 32) * 4
 
     e2e_api = ("paper_2503_10855_b200.api.execute('edge_detection', ...) on numpy in/out "
-               "(input page-locked in place on first use, chunks of 16 frames overlap H2D/kernel/D2H)")
+               "(input page-locked in place on first use, chunks of 16 frames overlap H2D/kernel/D2H; "
+               "maps cross PCIe bit-packed and are expanded to the f32 result on the host thread pool)")
 
     def ref_step(self, oracle, sample=False):
         """The step on the host: the oracle restatement over the whole batch
@@ -264,7 +267,13 @@ class EdgeWorkload:
         g, st, sx, sy, th = self.filters
         ref = oracle.edge(self.frames_host[:1], g, st, sx, sy, th)[0]
         got = self.out[0].cpu().numpy()
-        return bool(np.array_equal(ref.view(np.uint32), got.view(np.uint32)))
+        ok = bool(np.array_equal(ref.view(np.uint32), got.view(np.uint32)))
+        e2e = getattr(self, "e2e_out", None)
+        if e2e is not None:  # the end-to-end result (bit-packed D2H + host expansion) too
+            ok = ok and bool(np.array_equal(ref.view(np.uint32), np.asarray(e2e[0]).view(np.uint32)))
+            ok = ok and bool(np.array_equal(np.asarray(e2e[-1]).view(np.uint32),
+                                            self.out[-1].cpu().numpy().view(np.uint32)))
+        return ok
 
 
 class MatmulWorkload:

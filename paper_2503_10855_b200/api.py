@@ -26,6 +26,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Any, Callable, Sequence
 
+import os
+
 import numpy as np
 
 from . import _lib, hostmem
@@ -256,29 +258,41 @@ def edge_detection(input, gaussian_filter, structure, sx, sy, theta):
 
 
 _PIPE_CACHE: dict = {}
+EXPAND_THREADS = int(os.environ.get("JB_EXPAND_THREADS", "3"))
 
 
-def _pipelined(x, out, chunk: int, key, launch, dev):
+def _pipelined(x, out, chunk: int, key, launch, dev, out_elem=None, finish=None):
     """Host-buffer batch through the device with copy/compute overlap.
 
     Frames of the host batch ``x`` move in chunks through two device slots on
     three streams -- H2D of chunk i+1 and D2H of chunk i-1 overlap the kernel
     of chunk i -- so a call is bound by the slower PCIe direction instead of
     the sum of copy and compute time.  ``launch(k, din, dout, stream)`` runs
-    the entry on the first k frames of the slot buffers."""
+    the entry on the first k frames of the slot buffers.
+
+    By default the device result of a chunk is copied into ``out`` directly.
+    With ``out_elem = (shape, torch dtype)`` and ``finish`` the device slots
+    hold that per-frame result instead; it lands in one of two pinned host
+    staging slots and ``finish(f0, k, staged)`` turns it into ``out[f0:f0+k]``
+    on the host, one chunk behind the device (so the host work of chunk i-1
+    overlaps the copies and kernel of chunk i)."""
     torch = _torch()
     B = int(x.shape[0])
-    key = (dev.index, x.dtype, tuple(x.shape[1:]), out.dtype, tuple(out.shape[1:]), chunk, key)
+    e_shape, e_dtype = out_elem if out_elem is not None else (tuple(out.shape[1:]), out.dtype)
+    key = (dev.index, x.dtype, tuple(x.shape[1:]), e_dtype, tuple(e_shape), chunk, key)
     st = _PIPE_CACHE.get(key)
     if st is None:
         st = dict(inb=[torch.empty((chunk, *x.shape[1:]), dtype=x.dtype, device=dev) for _ in range(2)],
-                  outb=[torch.empty((chunk, *out.shape[1:]), dtype=out.dtype, device=dev) for _ in range(2)],
+                  outb=[torch.empty((chunk, *e_shape), dtype=e_dtype, device=dev) for _ in range(2)],
+                  stage=[hostmem.pinned_empty((chunk, *e_shape), e_dtype) for _ in range(2)]
+                  if finish is not None else None,
                   s_in=torch.cuda.Stream(dev), s_out=torch.cuda.Stream(dev))
         _PIPE_CACHE[key] = st
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = st["s_in"], st["s_out"]
     c_done = [None, None]
     d_done = [None, None]
+    pending = None  # (f0, k, slot, event) of the chunk whose host finish is due
     for i, f0 in enumerate(range(0, B, chunk)):
         k = min(chunk, B - f0)
         slot = i & 1
@@ -298,22 +312,36 @@ def _pipelined(x, out, chunk: int, key, launch, dev):
         c_done[slot] = c_ev
         with torch.cuda.stream(s_out):
             s_out.wait_event(c_ev)
-            out[f0:f0 + k].copy_(dout[:k], non_blocking=True)
+            dst = out[f0:f0 + k] if finish is None else st["stage"][slot][:k]
+            dst.copy_(dout[:k], non_blocking=True)
             d_ev = torch.cuda.Event()
             d_ev.record(s_out)
         d_done[slot] = d_ev
+        if finish is not None:
+            # the staging slot of chunk i-1 is reused by chunk i+1's copy,
+            # which is only enqueued after this finish returns
+            if pending is not None:
+                pf0, pk, pslot, pev = pending
+                pev.synchronize()
+                finish(pf0, pk, st["stage"][pslot][:pk])
+            pending = (f0, k, slot, d_ev)
     s_out.synchronize()
+    if pending is not None:
+        pf0, pk, pslot, _ = pending
+        finish(pf0, pk, st["stage"][pslot][:pk])
     comp.wait_stream(s_out)
     return out
 
 
 def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, out=None, chunk: int = 16,
-                             device=None):
+                             device=None, bits: bool = True):
     """Host-buffer edge detection with copy/compute overlap (``_pipelined``).
 
     ``input`` is a host f32[batch,n,m] (numpy or CPU torch tensor; pinned
     memory gives full PCIe bandwidth).  Returns ``out`` (a host f32 tensor of
-    the input's shape)."""
+    the input's shape).  ``bits`` (default) moves each chunk's maps
+    device->host bit-packed (jb_edge_bits_f32) and expands them on the host
+    (jb_bits_expand_f32): the same values, 1/32 of the D2H bytes."""
     torch = _torch()
     x = input if isinstance(input, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(input, np.float32))
     _need(x.dtype == torch.float32 and x.dim() == 3 and not x.is_cuda,
@@ -328,12 +356,36 @@ def edge_detection_pipelined(input, gaussian_filter, structure, sx, sy, theta, o
             for f in (gaussian_filter, structure, sx, sy)]
     lib = _lib.load()
 
-    def launch(k, din, dout, stream):
-        _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
-                               filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(), stream),
-               "edge_detection")
+    if not bits:
+        def launch(k, din, dout, stream):
+            _check(lib.jb_edge_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(), filt[1].data_ptr(),
+                                   filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta), dout.data_ptr(),
+                                   stream), "edge_detection")
+        with torch.cuda.device(dev):
+            return _pipelined(x, out, chunk, "edge", launch, dev)
+
+    # the edge map is exactly 0/1: it crosses PCIe as bits (1/32 of the f32
+    # bytes) and is expanded into ``out`` on the host thread pool
+    _need(out.dtype == torch.float32 and out.is_contiguous() and tuple(out.shape) == (B, n, m),
+          "edge_detection_pipelined: out must be a contiguous host f32[batch,n,m]")
+    fw = (n * m + 31) // 32
+    out_ptr = out.data_ptr()
+
+    def launch_bits(k, din, dout, stream):
+        _check(lib.jb_edge_bits_f32(k, n, m, gs, sz, sb, din.data_ptr(), filt[0].data_ptr(),
+                                    filt[1].data_ptr(), filt[2].data_ptr(), filt[3].data_ptr(), _scalar(theta),
+                                    dout.data_ptr(), stream), "edge_detection")
+
+    # 3 host threads: measured best on the B200 box (tools/e2e_probe2.py,
+    # profiles/r02_e2e_probe.txt) -- the host's DRAM is shared by the DMA
+    # reading the next chunk's input and this expansion writing the result,
+    # and a full-pool expansion starves the DMA (55 -> 22-31 GB/s)
+    def finish(f0, k, staged):
+        _check(lib.jb_bits_expand_f32(staged.data_ptr(), k, n * m, out_ptr + f0 * n * m * 4, EXPAND_THREADS),
+               "edge_detection (bit expansion)")
     with torch.cuda.device(dev):
-        return _pipelined(x, out, chunk, "edge", launch, dev)
+        return _pipelined(x, out, chunk, "edge_bits", launch_bits, dev, out_elem=((fw,), torch.int32),
+                          finish=finish)
 
 
 def cava_pipelined(input, tstw, ctrl_pts, weights, coefs, tonemap, out=None, chunk: int = 8, device=None):

@@ -187,6 +187,8 @@ struct FusedArgs {
   long long frame_px, slot_px;
   int lag;              // tiles of frame f + lag run the reject units of frame f
   int opts;             // experiment bits (JB_EDGE_OPTS): 1 no discard
+  uint32_t *obits;      // bit-packed edge maps [frames][frame_words] (instead of out), or null
+  long long frame_words;// ceil(frame_px / 32): bit b of word w is pixel 32w + b
 };
 
 // fast-path data guard: every staged pixel is +0 or in [2^-60, 2^64].  On
@@ -692,6 +694,9 @@ __device__ int wait_frame(const FusedArgs &a, int f, int &acq) {
 __device__ __forceinline__ float reject_px(uint32_t p, int A) {
   return ((int)p >= A && (int)p <= (int)0xff800000u) ? 1.0f : 0.0f;
 }
+__device__ __forceinline__ uint32_t reject_bit(uint32_t p, int A) {
+  return ((int)p >= A && (int)p <= (int)0xff800000u) ? 1u : 0u;
+}
 
 // the whole CTA: reject unit `unit` with compare bound `A` (from thread 0)
 __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
@@ -699,7 +704,9 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   const long long b0 = (long long)u * a.unit_px;
   const long long cnt = min((long long)a.unit_px, a.frame_px - b0);
   const uint32_t *src = a.packed + (size_t)(f % a.ring) * a.slot_px + b0;
-  float *dst = a.out + (size_t)f * a.frame_px + b0;
+  float *dst = a.obits ? nullptr : a.out + (size_t)f * a.frame_px + b0;
+  // unit starts are multiples of 1024 pixels: whole words
+  uint32_t *wdst = a.obits ? a.obits + (size_t)f * a.frame_words + (b0 >> 5) : nullptr;
   if (a.vec4) {
     const int n4 = (int)(cnt >> 2);
     const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
@@ -720,9 +727,20 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
 #pragma unroll
       for (int k = 0; k < RB; k++) {
         const int i = base + k * THREADS + threadIdx.x;
-        if (i < n4)
+        if (a.obits) {
+          // bit-packed map: 8 lanes hold one word's 32 pixels (4 each)
+          uint32_t v = 0;
+          if (i < n4)
+            v = (reject_bit(p[k].x, A) | reject_bit(p[k].y, A) << 1 | reject_bit(p[k].z, A) << 2 |
+                 reject_bit(p[k].w, A) << 3) << (4 * (threadIdx.x & 7));
+          v |= __shfl_xor_sync(0xffffffffu, v, 1);
+          v |= __shfl_xor_sync(0xffffffffu, v, 2);
+          v |= __shfl_xor_sync(0xffffffffu, v, 4);
+          if (i < n4 && (threadIdx.x & 7) == 0) __stcs(wdst + (i >> 3), v);
+        } else if (i < n4) {
           __stcs(d4 + i, make_float4(reject_px(p[k].x, A), reject_px(p[k].y, A), reject_px(p[k].z, A),
                                      reject_px(p[k].w, A)));
+        }
       }
       __syncwarp();
       // the slot base and unit start are 4 KB aligned: lane 8k starts a line
@@ -736,6 +754,14 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
     // still in flight when the slot's next frame is stored would drop the
     // new lines
     if (!(a.opts & 1) && (threadIdx.x & 7) == 0) fence_acq_rel();
+  } else if (a.obits) {
+    // one ballot per 32 consecutive pixels (cnt is uniform: every warp
+    // runs every pass)
+    for (long long base = 0; base < cnt; base += THREADS) {
+      const long long i = base + threadIdx.x;
+      const unsigned w = __ballot_sync(0xffffffffu, i < cnt && reject_bit(__ldcg(src + i), A));
+      if ((threadIdx.x & 31) == 0 && i < cnt) wdst[i >> 5] = w;
+    }
   } else {
     for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), A);
   }
@@ -1126,18 +1152,25 @@ static jb_status validate(uint64_t batch, uint64_t n, uint64_t m, uint64_t gs, u
 using namespace jb;
 using namespace jb::edge;
 
-extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_t gs, uint64_t sz,
-                                 uint64_t sb, const float *in, const float *gf, const float *st,
-                                 const float *sx, const float *sy, float theta, float *out,
-                                 void *stream) {
-  jb_status v = validate(batch, n, m, gs, sz, sb, in, out);
-  if (v != JB_OK) return v;
-  if (batch == 0) return JB_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!(gs == 7 && sz == 3 && sb == 3))
-    return run_generic(batch, n, m, gs, sz, sb, in, gf, st, sx, sy, theta, out, nullptr, nullptr,
-                       nullptr, nullptr, nullptr, s);
+namespace jb {
+namespace edge {
 
+// f32 edge maps (exactly 0 or 1) -> bit-packed words, frame by frame
+__global__ void pack_bits_kernel(const float *__restrict__ maps, long long frame_px, long long frame_words,
+                                 long long words, uint32_t *__restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < words;
+       w += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long f = w / frame_words, j = (w - f * frame_words) * 32 + lane;
+    const unsigned b = __ballot_sync(0xffffffffu, j < frame_px && maps[f * frame_px + j] != 0.0f);
+    if (lane == 0) bits[w] = b;
+  }
+}
+
+// the fused path (gs = 7, sz = 3, sb = 3) writing f32 maps (out) or packed bits (obits)
+static jb_status run_fused(uint64_t batch, uint64_t n, uint64_t m, const float *in, const float *gf,
+                           const float *st, const float *sx, const float *sy, float theta, float *out,
+                           uint32_t *obits, cudaStream_t s) {
   const size_t frame_px = (size_t)n * m;
   const int tiles_x = (int)((m + TW - 1) / TW), tiles_y = (int)((n + TH - 1) / TH);
   const int tpf = tiles_x * tiles_y;
@@ -1208,7 +1241,9 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   // 1080p frames, so frame f is complete by the time frame f+4's tiles end;
   // lag <= ring - 2 keeps the slot of frame f + ring free when it is needed
   fa.lag = (int)(ring >= 6 ? 4 : (ring >= 3 ? ring - 2 : 1));
-  fa.vec4 = frame_px % 4 == 0 && ((uintptr_t)out % 16) == 0;
+  fa.obits = obits;
+  fa.frame_words = (long long)((frame_px + 31) / 32);
+  fa.vec4 = frame_px % 4 == 0 && (obits != nullptr || ((uintptr_t)out % 16) == 0);
   fa.frame_px = (long long)frame_px; fa.slot_px = (long long)slot_px;
   {
     const char *e = getenv("JB_EDGE_OPTS");
@@ -1235,6 +1270,49 @@ extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_
   if (!bank.ev) JB_CHECK_CUDA(cudaEventCreateWithFlags(&bank.ev, cudaEventDisableTiming));
   JB_CHECK_CUDA(cudaEventRecord(bank.ev, s));
   bank.stream = s;
+  return JB_OK;
+}
+
+}  // namespace edge
+}  // namespace jb
+
+extern "C" jb_status jb_edge_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_t gs, uint64_t sz,
+                                 uint64_t sb, const float *in, const float *gf, const float *st,
+                                 const float *sx, const float *sy, float theta, float *out,
+                                 void *stream) {
+  jb_status v = validate(batch, n, m, gs, sz, sb, in, out);
+  if (v != JB_OK) return v;
+  if (batch == 0) return JB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(gs == 7 && sz == 3 && sb == 3))
+    return run_generic(batch, n, m, gs, sz, sb, in, gf, st, sx, sy, theta, out, nullptr, nullptr,
+                       nullptr, nullptr, nullptr, s);
+  return run_fused(batch, n, m, in, gf, st, sx, sy, theta, out, nullptr, s);
+}
+
+extern "C" jb_status jb_edge_bits_f32(uint64_t batch, uint64_t n, uint64_t m, uint64_t gs, uint64_t sz,
+                                      uint64_t sb, const float *in, const float *gf, const float *st,
+                                      const float *sx, const float *sy, float theta, uint32_t *out_bits,
+                                      void *stream) {
+  jb_status v = validate(batch, n, m, gs, sz, sb, in, out_bits);
+  if (v != JB_OK) return v;
+  if (batch == 0) return JB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (gs == 7 && sz == 3 && sb == 3) return run_fused(batch, n, m, in, gf, st, sx, sy, theta, nullptr, out_bits, s);
+  // other filter sizes: the per-stage kernels into f32 maps at the arena's
+  // tail, then one packing pass.  run_generic asks the arena for its head
+  // only (<= the capacity reserved here, so the block does not move).
+  const size_t px = (size_t)batch * n * m;
+  const size_t head = (4 * px * 4 + batch * 4 + 256 + 255) / 256 * 256;
+  char *ws = (char *)workspace(head + px * 4, s);
+  if (!ws) return JB_ECUDA;
+  float *maps = (float *)(ws + head);
+  v = run_generic(batch, n, m, gs, sz, sb, in, gf, st, sx, sy, theta, maps, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, s);
+  if (v != JB_OK) return v;
+  const long long fw = (long long)((n * m + 31) / 32), words = fw * (long long)batch;
+  pack_bits_kernel<<<grid_for(words * 32, 256), 256, 0, s>>>(maps, (long long)(n * m), fw, words, out_bits);
+  JB_LAUNCHED("edge pack_bits");
   return JB_OK;
 }
 

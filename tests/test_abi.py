@@ -48,3 +48,25 @@ def test_oracle_execute_signature_parity():
     import paper_2503_10855_b200 as jb
     params = list(inspect.signature(jb.oracle_execute).parameters)
     assert params == ["module", "entry", "dyn_consts", "args", "max_steps"]
+
+
+@pytest.mark.parametrize("frames,frame_px", [(1, 1), (2, 31), (3, 32), (2, 33), (4, 1000), (2, 8192 * 32 + 5),
+                                             (1, 1080 * 1920)])
+@pytest.mark.parametrize("threads", [1, 3, 0])
+def test_bits_expand_host(frames, frame_px, threads):
+    """jb_bits_expand_f32 (host code, no GPU): bit b of word w of a frame is
+    pixel 32w+b -> 1.0f / 0.0f, ragged last words included, every output
+    element written (sentinel-filled buffer)."""
+    lib = _lib.load()
+    fw = (frame_px + 31) // 32
+    rng = np.random.default_rng(frame_px)
+    words = rng.integers(0, 2 ** 32, size=(frames, fw), dtype=np.uint64).astype(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8).reshape(frames, fw * 4), axis=1, bitorder="little")
+    want = bits[:, :frame_px].astype(np.float32)
+    out = np.full((frames, frame_px), np.float32(7.0))
+    assert lib.jb_bits_expand_f32(words.ctypes.data, frames, frame_px, out.ctypes.data, threads) == 0
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+    # an output that is not 16-byte aligned takes the unaligned stores
+    buf = np.full(frames * frame_px + 1, np.float32(7.0))
+    assert lib.jb_bits_expand_f32(words.ctypes.data, frames, frame_px, buf[1:].ctypes.data, threads) == 0
+    assert np.array_equal(buf[1:].reshape(frames, frame_px), want)

@@ -132,3 +132,53 @@ def test_edge_pipelined_matches_single_call(jb):
     ref = jb.edge_detection(x, g, st, sx, sy, th)
     got = api.edge_detection_pipelined(torch.from_numpy(x).pin_memory(), g, st, sx, sy, th, chunk=3)
     _bits_equal(got.numpy(), ref)
+
+
+def _pack_words(maps):
+    """f32 maps [b, n, m] (0/1) -> u32 words [b, ceil(n*m/32)], bit b of word w = pixel 32w+b."""
+    b = maps.shape[0]
+    flat = (maps.reshape(b, -1) != 0).astype(np.uint8)
+    fw = (flat.shape[1] + 31) // 32
+    pad = np.zeros((b, fw * 32), np.uint8)
+    pad[:, :flat.shape[1]] = flat
+    return np.packbits(pad, axis=1, bitorder="little").view(np.uint32)
+
+
+@pytest.mark.parametrize("shape,gs", [((3, 1080, 1920), 7), ((2, 61, 59), 7), ((5, 121, 245), 7), ((2, 7, 5), 7),
+                                      ((3, 1080, 1918), 7), ((1, 1, 1), 7), ((2, 50, 77), 5)])
+def test_edge_bits_entry_matches_f32_entry(jb, shape, gs):
+    """jb_edge_bits_f32 writes exactly the bits of jb_edge_f32's maps: fused
+    path (TMA and scalar reject units, ragged last word) and the generic
+    per-stage path + packing kernel (gs=5)."""
+    import torch
+    from paper_2503_10855_b200 import _lib
+    b, n, m = shape
+    g, st, sx, sy, th = W.edge_filters(gs=gs)
+    x = np.stack([W.edge_frame(n, m, seed=30 + s) for s in range(b)])
+    d = [torch.from_numpy(a).cuda() for a in (x, g, st, sx, sy)]
+    out = torch.empty_like(d[0])
+    fw = (n * m + 31) // 32
+    bits = torch.full((b, fw), -1, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    s = torch.cuda.current_stream().cuda_stream
+    ptrs = [t.data_ptr() for t in d]
+    assert lib.jb_edge_f32(b, n, m, gs, 3, 3, *ptrs, th, out.data_ptr(), s) == 0
+    assert lib.jb_edge_bits_f32(b, n, m, gs, 3, 3, *ptrs, th, bits.data_ptr(), s) == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    want = _pack_words(out.cpu().numpy())
+    got = bits.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want), f"{np.count_nonzero(got != want)} words differ"
+    assert np.count_nonzero(out.cpu().numpy()) > 0 or n * m < 64
+
+
+def test_edge_pipelined_bits_equals_f32_transfer(jb):
+    """The bit-packed D2H + host expansion returns the same f32 maps as the
+    f32 transfer (several chunks, ragged last chunk, odd frame size)."""
+    import torch
+    from paper_2503_10855_b200 import api
+    g, st, sx, sy, th = W.edge_filters()
+    x = torch.from_numpy(np.stack([W.edge_frame(135, 241, seed=s) for s in range(9)])).pin_memory()
+    a = api.edge_detection_pipelined(x, g, st, sx, sy, th, chunk=4, bits=False)
+    b = api.edge_detection_pipelined(x, g, st, sx, sy, th, chunk=4, bits=True)
+    _bits_equal(a.numpy(), b.numpy())
+    assert a.numpy().any()
