@@ -279,6 +279,100 @@ __device__ __noinline__ void gauss_fast(int warp, int lane) {
   for (int o = 0; o < 8; o++) *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
 }
 
+// end of a tile's compute: the packed tile leaves by bulk tensor store (TMA
+// path), the block max goes to the frame's atomicMax (thread 0's return value
+// is consumed a tile later, flush_done)
+__device__ __forceinline__ unsigned tile_tail(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
+                                              int lane, int warp, float bmax) {
+  unsigned amax = 0;
+  if (a.use_tma) tc::fence_proxy_async_smem();  // P -> async proxy
+  bmax = warp_max(bmax);
+  if (lane == 0) S.wmax[warp] = bmax;
+  __syncthreads();
+  if (tid == 0) {
+    if (a.use_tma) {
+      tc::tma_store_3d_hint(&a.pmap, &S.P[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
+      tc::bulk_commit();
+    }
+    float v = S.wmax[0];
+#pragma unroll
+    for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
+    // thread 0's atom: its return value (consumed a tile later, flush_done)
+    // tells that the max has been performed before the tile is counted
+    if (!(v != v)) amax = atomicMax(a.fmax + f, __float_as_uint(v));
+  }
+  EDGE_T(4);
+  return amax;
+}
+
+// stages 2b + 2c of an interior tile with the standard sobel pair (TMA path):
+// zero crossings and gradient per warp, no block barrier between them.
+//  * warp w owns 8 output rows (k0 = 8w; warp 7 rows 52..59, overlapping
+//    warp 6 by 4 rows: duplicate, identical stores);
+//  * zero crossings: lane k < 8 derives row k0+k's 64-bit mask from three
+//    laplacian sign rows; the row loop broadcasts it with two shuffles;
+//  * gradient: lane l owns columns l and l+32 (lanes 28..31 repeat column
+//    59 in the second slot, not stored) as one f32x2 pair, so every sobel
+//    step is one packed FADD2/FFMA2 for two pixels.  The fold is the
+//    oracle's 9-tap order with the x*0 taps dropped (they only change the
+//    sign of a zero, which the square erases) and x*(+-1), x*(+-2) exact; gy
+//    is carried negated (ny = -gy: every rounding is sign-symmetric).  The
+//    squares are FMUL2, the sum a scalar add.rn (single rounding each).
+__device__ __forceinline__ unsigned sobel_pairs(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
+                                             int lane, int warp) {
+  const int k0 = warp < 7 ? warp * 8 : TH - 8;
+  unsigned zlo = 0, zhi = 0;
+  if (lane < 8) {
+    unsigned long long orr = 0, andd = ~0ull;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const unsigned long long b = *reinterpret_cast<const unsigned long long *>(&S.lapbits[k0 + lane + i][0]);
+      orr |= b;
+      andd &= b;
+    }
+    const unsigned long long zc = (orr | (orr >> 1) | (orr >> 2)) & ~(andd & (andd >> 1) & (andd >> 2));
+    zlo = (unsigned)zc;
+    zhi = (unsigned)(zc >> 32);
+  }
+  const int ca = lane, cb = min(lane + 32, TW - 1);
+  const bool b_ok = lane + 32 < TW;
+  const f2 two = bc2(2.0f), mtwo = bc2(-2.0f);
+  float bmax = 0.0f;
+  f2 gx[3], ny[3];
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const int sr = k0 + 1 + r;  // smoothed row
+    const f2 v0 = pk2(S.sm[sr][ca + 1], S.sm[sr][cb + 1]);
+    const f2 v1 = pk2(S.sm[sr][ca + 2], S.sm[sr][cb + 2]);
+    const f2 v2 = pk2(S.sm[sr][ca + 3], S.sm[sr][cb + 3]);
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const int k = r - q;  // output row k0 + k gets tap row q
+      if (k < 0 || k >= 8) continue;
+      const int s = k % 3;
+      if (q == 0) {
+        gx[s] = sub2n(v2, v0);
+        ny[s] = add2n(fma2(v1, two, v0), v2);
+      } else if (q == 1) {
+        gx[s] = fma2(v2, two, fma2(v0, mtwo, gx[s]));
+      } else {
+        gx[s] = add2n(sub2n(gx[s], v0), v2);
+        ny[s] = sub2n(fma2(v1, mtwo, sub2n(ny[s], v0)), v2);
+        const f2 sx2 = mul2(gx[s], gx[s]), sy2 = mul2(ny[s], ny[s]);
+        const float ga = add_rn(lo2(sx2), lo2(sy2)), gb = add_rn(hi2(sx2), hi2(sy2));
+        const unsigned zl = __shfl_sync(0xffffffffu, zlo, k), zh = __shfl_sync(0xffffffffu, zhi, k);
+        S.P[k0 + k][ca] = __float_as_uint(ga) | ((zl << (31 - lane)) & 0x80000000u);
+        if (b_ok) S.P[k0 + k][lane + 32] = __float_as_uint(gb) | ((zh << (31 - lane)) & 0x80000000u);
+        bmax = fmaxf(bmax, fmaxf(ga, gb));
+      }
+    }
+    // keep the next rows' loads from being hoisted (register pressure: the
+    // persistent loop's state must not spill)
+    asm volatile("" ::: "memory");
+  }
+  return tile_tail(S, a, f, y0, x0, tid, lane, warp, bmax);
+}
+
 // stages 1-2 of one 60x60 tile whose clamped input is staged in S.inA/S.raw.
 // FAST: packed/FTZ gaussian, FMNMX morphology, FFMA sobel (guarded exact);
 // otherwise the oracle's operation order with single-rounding scalar ops.
@@ -409,6 +503,8 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   __syncthreads();
   EDGE_T(2);
 
+  if (SOBEL_STD) return sobel_pairs(S, a, f, y0, x0, tid, lane, warp);
+
   // ---- stage 2b: zero crossings (bit masks), one thread per output row
   if (tid < TH) {
     const int orow = tid;
@@ -465,7 +561,6 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
 
   // ---- stage 2c: sobel gradient, pack with zc, block max
   float bmax = 0.0f;
-  unsigned amax = 0;
   {
     const int cc = warp & 1, rb = warp >> 1;
     const int oc = cc * 32 + lane;
@@ -490,20 +585,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
         const int k = r - q;  // output row k (0..14) gets tap row q
         if (k >= 0 && k < 15) {
           float gx = q == 0 ? 0.0f : gxs[k % 3], gy = q == 0 ? 0.0f : gys[k % 3];
-          if (FAST && SOBEL_STD) {
-            // the standard sobel pair: the oracle's 9-tap folds with the
-            // x*0 taps dropped (they only change the sign of a zero, which
-            // the squares erase) and x*(+-1), x*(+-2) exact -> 10 ops, not 18
-            if (q == 0) {
-              gx = add_rn(-v0, v2);
-              gy = sub_rn(fmaf(-2.0f, v1, -v0), v2);
-            } else if (q == 1) {
-              gx = fmaf(2.0f, v2, fmaf(-2.0f, v0, gx));
-            } else {
-              gx = add_rn(sub_rn(gx, v0), v2);
-              gy = add_rn(fmaf(2.0f, v1, add_rn(gy, v0)), v2);
-            }
-          } else if (FAST) {
+          if (FAST) {
             gx = fmaf(v0, sx[q * 3 + 0], gx); gy = fmaf(v0, sy[q * 3 + 0], gy);
             gx = fmaf(v1, sx[q * 3 + 1], gx); gy = fmaf(v1, sy[q * 3 + 1], gy);
             gx = fmaf(v2, sx[q * 3 + 2], gx); gy = fmaf(v2, sy[q * 3 + 2], gy);
@@ -530,24 +612,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
       }
     }
   }
-  if (a.use_tma) tc::fence_proxy_async_smem();  // P -> async proxy
-  bmax = warp_max(bmax);
-  if (lane == 0) S.wmax[warp] = bmax;
-  __syncthreads();
-  if (tid == 0) {
-    if (a.use_tma) {
-      tc::tma_store_3d_hint(&a.pmap, &S.P[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
-      tc::bulk_commit();
-    }
-    float v = S.wmax[0];
-#pragma unroll
-    for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
-    // thread 0's atom: its return value (consumed a tile later, flush_done)
-    // tells that the max has been performed before the tile is counted
-    if (!(v != v)) amax = atomicMax(a.fmax + f, __float_as_uint(v));
-  }
-  EDGE_T(4);
-  return amax;
+  return tile_tail(S, a, f, y0, x0, tid, lane, warp, bmax);
 }
 
 // ------------------------------------------------ in-kernel reject (stage 3)
@@ -691,13 +756,6 @@ __device__ int wait_frame(const FusedArgs &a, int f, int &acq) {
   }
 }
 
-__device__ __forceinline__ float reject_px(uint32_t p, int A) {
-  return ((int)p >= A && (int)p <= (int)0xff800000u) ? 1.0f : 0.0f;
-}
-__device__ __forceinline__ uint32_t reject_bit(uint32_t p, int A) {
-  return ((int)p >= A && (int)p <= (int)0xff800000u) ? 1u : 0u;
-}
-
 // the whole CTA: reject unit `unit` with compare bound `A` (from thread 0)
 __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   const int f = unit / a.units, u = unit - f * a.units;
@@ -707,6 +765,13 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   float *dst = a.obits ? nullptr : a.out + (size_t)f * a.frame_px + b0;
   // unit starts are multiples of 1024 pixels: whole words
   uint32_t *wdst = a.obits ? a.obits + (size_t)f * a.frame_words + (b0 >> 5) : nullptr;
+  // read once (the discards' memory clobbers would reload it from the
+  // parameter block every pass)
+  const bool disc = !(a.opts & 1);
+  // pass <=> A <= (int)p <= (int)0xff800000  <=>  p - Au < Ku (unsigned;
+  // Ku = 0 when nothing can pass)
+  const unsigned Au = (unsigned)A;
+  const unsigned Ku = A <= (int)0xff800000u ? (unsigned)((int)0xff800000u - A) + 1u : 0u;
   if (a.vec4) {
     const int n4 = (int)(cnt >> 2);
     const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
@@ -731,15 +796,15 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
           // bit-packed map: 8 lanes hold one word's 32 pixels (4 each)
           uint32_t v = 0;
           if (i < n4)
-            v = (reject_bit(p[k].x, A) | reject_bit(p[k].y, A) << 1 | reject_bit(p[k].z, A) << 2 |
-                 reject_bit(p[k].w, A) << 3) << (4 * (threadIdx.x & 7));
+            v = ((p[k].x - Au < Ku ? 1u : 0u) | (p[k].y - Au < Ku ? 2u : 0u) | (p[k].z - Au < Ku ? 4u : 0u) |
+                 (p[k].w - Au < Ku ? 8u : 0u)) << (4 * (threadIdx.x & 7));
           v |= __shfl_xor_sync(0xffffffffu, v, 1);
           v |= __shfl_xor_sync(0xffffffffu, v, 2);
           v |= __shfl_xor_sync(0xffffffffu, v, 4);
           if (i < n4 && (threadIdx.x & 7) == 0) __stcs(wdst + (i >> 3), v);
         } else if (i < n4) {
-          __stcs(d4 + i, make_float4(reject_px(p[k].x, A), reject_px(p[k].y, A), reject_px(p[k].z, A),
-                                     reject_px(p[k].w, A)));
+          __stcs(d4 + i, make_float4(p[k].x - Au < Ku ? 1.0f : 0.0f, p[k].y - Au < Ku ? 1.0f : 0.0f,
+                                     p[k].z - Au < Ku ? 1.0f : 0.0f, p[k].w - Au < Ku ? 1.0f : 0.0f));
         }
       }
       __syncwarp();
@@ -747,23 +812,23 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
 #pragma unroll
       for (int k = 0; k < RB; k++) {
         const int i = base + k * THREADS + threadIdx.x;
-        if (!(a.opts & 1) && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
+        if (disc && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
       }
     }
     // the discards must be performed before the unit is counted: a discard
     // still in flight when the slot's next frame is stored would drop the
     // new lines
-    if (!(a.opts & 1) && (threadIdx.x & 7) == 0) fence_acq_rel();
+    if (disc && (threadIdx.x & 7) == 0) fence_acq_rel();
   } else if (a.obits) {
     // one ballot per 32 consecutive pixels (cnt is uniform: every warp
     // runs every pass)
     for (long long base = 0; base < cnt; base += THREADS) {
       const long long i = base + threadIdx.x;
-      const unsigned w = __ballot_sync(0xffffffffu, i < cnt && reject_bit(__ldcg(src + i), A));
+      const unsigned w = __ballot_sync(0xffffffffu, i < cnt && __ldcg(src + i) - Au < Ku);
       if ((threadIdx.x & 31) == 0 && i < cnt) wdst[i >> 5] = w;
     }
   } else {
-    for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = reject_px(__ldcg(src + i), A);
+    for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = __ldcg(src + i) - Au < Ku ? 1.0f : 0.0f;
   }
   // every read of the unit's slot lines has returned (the values were
   // stored): the count needs no fence
@@ -946,7 +1011,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     unsigned amax;
     if (filters_fast && all_ok) {
       if (border) amax = edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
-      else if (sobel_std) amax = edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+      else if (sobel_std && a.use_tma) amax = edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
       else amax = edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     } else {
       amax = edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
