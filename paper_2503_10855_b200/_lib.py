@@ -33,6 +33,7 @@ SIGNATURES = {
     "jb_matmul_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp],
     "jb_matmul_exact_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp],
     "jb_edge_f32": [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _vp],
+    "jb_matmul_sched_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _u32, _u32, _u32, _vp],
     "jb_edge_bits_f32": [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _vp],
     "jb_bits_expand_f32": [_vp, _u64, _u64, _vp, ctypes.c_int],
     "jb_edge_stages_f32": [_u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _f32, _vp,

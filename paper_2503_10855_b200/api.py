@@ -24,7 +24,7 @@ inconsistent dynamic constants (dynconst.py:16-17,179-204) and
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Any, Callable, Sequence
+from typing import Any, Callable, Optional, Sequence
 
 import os
 
@@ -207,22 +207,34 @@ def _scalar(x, ty=float):
 
 
 # ---------------------------------------------------------------------- matmul
-def matmul(a, b, exact: bool = False):
+def matmul(a, b, exact: bool = False, tile_n: int = 128, tree: Sequence[int] = (1, 1)):
     """matmul<n,m,l>(a: f32[n,m], b: f32[m,l]) -> f32[n,l]  (PAPER.md:121-132).
 
     Default: 3xTF32 on tcgen05 tensor cores (fp32 tolerance, the k-reduce is
     re-associated).  ``exact=True``: SIMT kernel in the oracle's k order,
-    bit-identical to the reference interpreter."""
+    bit-identical to the reference interpreter.  ``tile_n`` / ``tree`` are a
+    schedule's launch parameters (planner.select_kernel): the CTA tile width
+    from the J fork's fork-tile factor, and the K reduction tree of
+    fork-fission (partial counts per level, outermost first; the partial
+    products are folded in that order, jb_matmul_sched_f32)."""
     _need(len(_shape(a)) == 2 and len(_shape(b)) == 2, "matmul: a and b must be 2-D")
     n, m = _shape(a)
     m2, l = _shape(b)
     _need(m == m2, f"matmul: inner extents differ ({m} vs {m2})")
+    tree = tuple(int(x) for x in tree) + (1,) * (2 - len(tree))
+    _need(len(tree) == 2, "matmul: reduction trees deeper than two partial levels are not supported")
     c = _Call([a, b])
     da, db = c.dev(a, np.float32, "a"), c.dev(b, np.float32, "b")
     out = c.empty((n, l), np.float32)
-    fn = _lib.load().jb_matmul_exact_f32 if exact else _lib.load().jb_matmul_f32
+    lib = _lib.load()
     with c.on_device():
-        _check(fn(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+        if exact:
+            _check(lib.jb_matmul_exact_f32(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+        elif tile_n == 128 and tree == (1, 1):
+            _check(lib.jb_matmul_f32(n, m, l, _ptr(da), _ptr(db), _ptr(out), c.s), "matmul")
+        else:
+            _check(lib.jb_matmul_sched_f32(n, m, l, _ptr(da), _ptr(db), _ptr(out), int(tile_n), tree[0], tree[1],
+                                           c.s), "matmul")
     return c.out(out)
 
 
@@ -600,7 +612,7 @@ def _sh(*pairs):
 ENTRIES: dict[str, Entry] = {
     "matmul": Entry(("n", "m", "l"),
                     lambda d, a: _sh((0, (d[0], d[1])), (1, (d[1], d[2]))),
-                    lambda d, a: matmul(*a)),
+                    lambda d, a, **kw: matmul(*a, **kw)),
     "edge_detection": Entry(("n", "m", "gs", "sz", "sb"),
                             lambda d, a: _sh((0, (d[0], d[1])), (1, (d[2], d[2])), (2, (d[3], d[3])),
                                              (3, (d[4], d[4])), (4, (d[4], d[4]))),
@@ -625,10 +637,14 @@ ENTRIES: dict[str, Entry] = {
 }
 
 
-def execute(entry: str, dyn_consts, args):
+def execute(entry: str, dyn_consts, args, params: Optional[dict] = None):
     """Run Juno ``entry`` on the B200: ``oracle_execute`` without the module
-    (the entry names the benchmark program of SURVEY.md §8 (a.2))."""
+    (the entry names the benchmark program of SURVEY.md §8 (a.2)).
+    ``params``: launch parameters a schedule implies (planner.select_kernel;
+    matmul: ``tile_n``, ``tree``)."""
     dcs, args = validate(entry, dyn_consts, args)
+    if params:
+        return ENTRIES[entry].run(dcs, args, **params)
     return ENTRIES[entry].run(dcs, args)
 
 
@@ -695,4 +711,4 @@ def oracle_execute(module, entry: str, dyn_consts, args, max_steps: int = 50_000
     if rec is None:
         raise _err(UnsupportedError, f"no B200 kernel computes function {entry!r}: " +
                    "; ".join(f"not {k} ({v})" for k, v in why.items()))
-    return execute(rec.entry, rec.dyn_consts, args)
+    return execute(rec.entry, rec.dyn_consts, args, rec.params)

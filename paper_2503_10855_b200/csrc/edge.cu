@@ -1306,6 +1306,10 @@ static jb_status run_fused(uint64_t batch, uint64_t n, uint64_t m, const float *
   // 1080p frames, so frame f is complete by the time frame f+4's tiles end;
   // lag <= ring - 2 keeps the slot of frame f + ring free when it is needed
   fa.lag = (int)(ring >= 6 ? 4 : (ring >= 3 ? ring - 2 : 1));
+  if (const char *e = getenv("JB_EDGE_LAG")) {  // experiments: 1 <= lag <= ring - 2
+    const int l = atoi(e);
+    if (l >= 1 && l <= (int)ring - 2) fa.lag = l;
+  }
   fa.obits = obits;
   fa.frame_words = (long long)((frame_px + 31) / 32);
   fa.vec4 = frame_px % 4 == 0 && (obits != nullptr || ((uintptr_t)out % 16) == 0);

@@ -37,6 +37,7 @@
 // (the second split waits: 0.0309 ms).
 // Shapes the TMA path cannot take (row pitch not a multiple of 16 bytes) run
 // an exact SIMT kernel that follows the oracle's k order bit for bit.
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -71,7 +72,7 @@ constexpr int B_ATOM = BK * 32 * 4;           // one 32-column MN atom of B: 4 K
 constexpr int STAGES = 4;                   // raw tiles (TMA ring, also the hi operands)
 constexpr int LO_STAGES = 2;                // converted lo operands
 constexpr int A_TILE = BM * BK * 4;         // 16 KiB
-constexpr int B_TILE = BK * BN * 4;         // BN/32 atoms
+template <int BNT> constexpr int b_tile() { return BK * BNT * 4; }  // BNT/32 atoms
 constexpr int THREADS = 320;
 constexpr int CONVERTERS = 256;             // warps 2..9 (warps 2..5 also run the epilogue)
 #ifndef MM1_A_SMEM
@@ -85,13 +86,14 @@ constexpr uint32_t TMEM_COLS = 128;
 #endif
 constexpr uint32_t ALO_COL1 = 128;
 
-struct Smem {
+template <int BNT>
+struct SmemT {
   // raw fp32 tiles straight from TMA; the tensor core reads them as the tf32
   // "hi" operands (it ignores the 13 low mantissa bits, tools/mma_probe.cu)
   uint8_t a_raw[STAGES][A_TILE];  // [128 m][32 k] K-major, 128B swizzle
-  uint8_t b_raw[STAGES][B_TILE];  // 4 MN atoms x [32 k][32 n], 128B swizzle / 32B atoms
+  uint8_t b_raw[STAGES][b_tile<BNT>()];  // BNT/32 MN atoms x [32 k][32 n], 128B swizzle / 32B atoms
   uint8_t a_lo[LO_STAGES][A_TILE];  // x - trunc_tf32(x), same layouts
-  uint8_t b_lo[LO_STAGES][B_TILE];
+  uint8_t b_lo[LO_STAGES][b_tile<BNT>()];
   uint64_t full[STAGES];            // TMA -> converters
   uint64_t empty[STAGES];           // MMA -> TMA (raw slot free)
   uint64_t conv[LO_STAGES];         // converters -> MMA
@@ -99,8 +101,8 @@ struct Smem {
   uint64_t tmem_full;
   uint32_t tmem_base;
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + manual 1 KiB alignment
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+template <int BNT> constexpr size_t smem_bytes() { return sizeof(SmemT<BNT>) + 1024; }  // + manual 1 KiB alignment
+static_assert(smem_bytes<128>() <= 232448, "shared memory budget");
 
 // residual of the tensor core's tf32 truncation: exact in f32
 __device__ __forceinline__ float tf32_residual(float x) {
@@ -119,10 +121,17 @@ __device__ __forceinline__ uint64_t desc_b_mn(uint32_t saddr) {
   return (d & ~(7ull << 61)) | (1ull << 61);
 }
 
-// grid (N/128, M/128, splitk); blockIdx.z takes k-blocks [kb0, kb1)
+// grid (N/BNT, M/128, splitk); blockIdx.z takes k-blocks [kb0, kb1).
+// partials == nullptr: the z slices meet in c (plain stores for one slice,
+// f32 reductions onto a zeroed c for two); otherwise slice z stores its
+// partial tile to partials + z*M*N and a fixed-order fold sums them
+// (mm_fold_kernel: the schedule's reduction tree, any slice count).
+template <int BNT>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                   float *__restrict__ c, int M, int N, int K) {
+                   float *__restrict__ c, int M, int N, int K, float *__restrict__ partials) {
+  constexpr int BN = BNT, B_TILE = b_tile<BNT>();
+  using Smem = SmemT<BNT>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1 KiB alignment by offsetting within the __shared__ array, so the compiler
   // keeps the shared address space (LDS/STS, not generic LD/ST)
@@ -135,6 +144,8 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
   const int kb0 = (int)((long long)kblocks * blockIdx.z / splitk);
   const int kb1 = (int)((long long)kblocks * (blockIdx.z + 1) / splitk);
   const int nkb = kb1 - kb0;
+  if (partials) c = partials + (size_t)blockIdx.z * M * N;
+  const bool reduce_c = splitk > 1 && !partials;
   if (threadIdx.x == 0) MM_T(0);
 
   if (warp == 0 && lane == 0) {
@@ -310,7 +321,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
             for (int v = 0; v < 4; v++) {
               const float a0 = __uint_as_float(r[4 * v]), a1 = __uint_as_float(r[4 * v + 1]);
               const float a2 = __uint_as_float(r[4 * v + 2]), a3 = __uint_as_float(r[4 * v + 3]);
-              if (splitk > 1)
+              if (reduce_c)
                 red_add_v4(dst + 4 * v, a0, a1, a2, a3);
               else
                 reinterpret_cast<float4 *>(dst)[v] = make_float4(a0, a1, a2, a3);
@@ -318,7 +329,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
           } else {
             for (int v = 0; v < 16; v++)
               if (n0 + cb + v < N) {
-                if (splitk > 1)
+                if (reduce_c)
                   atomicAdd(dst + v, __uint_as_float(r[v]));
                 else
                   dst[v] = __uint_as_float(r[v]);
@@ -338,6 +349,58 @@ done:
   }
 }
 
+
+// res = fold of the partial tiles in the reduction tree's order: counts
+// (n1, n2) = partials per level, outermost first (n2 = 1 for one fission):
+//   res = 0 + sum_{p1 < n1} (0 + sum_{p2 < n2} part[p1 * n2 + p2])
+// (fork-fission's bottom fold over the partials array, passes/fissfuse.py
+// :134-145; the second level is reduction_tree! applied to that fold)
+__global__ void mm_fold_kernel(const float *__restrict__ part, float *__restrict__ res, long long mn, int n1,
+                               int n2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn;
+       i += (long long)gridDim.x * blockDim.x) {
+    float r = 0.0f;
+    for (int p1 = 0; p1 < n1; p1++) {
+      float t = 0.0f;
+      for (int p2 = 0; p2 < n2; p2++) t = add_rn(t, __ldcs(part + (size_t)(p1 * n2 + p2) * mn + i));
+      r = add_rn(r, t);
+    }
+    res[i] = r;
+  }
+}
+
+// exact SIMT path: the oracle's sequential k order with single roundings,
+// over k in [k_lo, k_lo + K) of the K_stride-wide operands (a partial sum of
+// a reduction tree, or the whole product)
+__global__ void matmul_exact_range_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                          float *__restrict__ c, int M, int N, int K, int K_stride, int k_lo) {
+  a += k_lo;
+  b += (size_t)k_lo * N;
+  __shared__ float As[32][33];
+  __shared__ float Bs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int col = blockIdx.x * 32 + tx;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const int ar = blockIdx.y * 32 + r, ak = k0 + tx;
+      As[r][tx] = (ar < M && ak < K) ? a[(size_t)ar * K_stride + ak] : 0.f;
+      const int bk = k0 + r;
+      Bs[r][tx] = (bk < K && col < N) ? b[(size_t)bk * N + col] : 0.f;
+    }
+    __syncthreads();
+    const int kmax = min(32, K - k0);
+    for (int kk = 0; kk < kmax; kk++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) acc[i] = add_rn(acc[i], mul_rn(As[ty + 8 * i][kk], Bs[kk][tx]));
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int row = blockIdx.y * 32 + ty + 8 * i;
+    if (row < M && col < N) c[(size_t)row * N + col] = acc[i];
+  }
+}
 
 // exact SIMT path: the oracle's sequential k order with single roundings
 __global__ void matmul_exact_kernel(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ c,
@@ -448,8 +511,8 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    JB_CHECK_CUDA(cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SMEM_BYTES));
+    JB_CHECK_CUDA(cudaFuncSetAttribute(gemm_3xtf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes<BN>()));
     attr_set[dev] = true;
   }
   const long long tiles = (long long)((l + BN - 1) / BN) * (long long)((n + BM - 1) / BM);
@@ -490,7 +553,7 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
     cudaGraph_t graph = nullptr;
     JB_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     if (splitk > 1) cudaMemsetAsync(res, 0, n * l * 4, cs);
-    gemm_3xtf32_kernel<<<grid, THREADS, SMEM_BYTES, cs>>>(m_a, m_b, res, (int)n, (int)l, (int)m);
+    gemm_3xtf32_kernel<BN><<<grid, THREADS, smem_bytes<BN>(), cs>>>(m_a, m_b, res, (int)n, (int)l, (int)m, nullptr);
     const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
     if (ce == cudaSuccess && graph) {
       if (cudaGraphInstantiate(&gc.exec, graph, 0) != cudaSuccess) gc.exec = nullptr;
@@ -514,8 +577,85 @@ extern "C" jb_status jb_matmul_f32(uint64_t n, uint64_t m, uint64_t l, const flo
   }
   if (splitk > 1) JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
   void *tok = prof_begin("matmul_tcgen05", s);
-  gemm_3xtf32_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(m_a, m_b, res, (int)n, (int)l, (int)m);
+  gemm_3xtf32_kernel<BN><<<grid, THREADS, smem_bytes<BN>(), s>>>(m_a, m_b, res, (int)n, (int)l, (int)m, nullptr);
   prof_end(tok, s);
   JB_LAUNCHED("matmul_tcgen05");
+  return JB_OK;
+}
+
+// ------------------------------------------------- schedule-parametrised entry
+// The launch a scheduled matmul asks for (planner.select_kernel):
+//   tile_n   the CTA's output tile width from the J fork's fork-tile factor
+//            (64 or 128 columns; the tcgen05 tile is 128 rows: M = 128 is
+//            the single-CTA MMA atom);
+//   n1, n2   the reduction tree of fork-fission (reduction_tree!): n1 * n2
+//            contiguous K chunks, each a partial product (3xTF32 on the
+//            tensor cores when the chunk is a whole number of 32-wide
+//            k-blocks and the operands suit TMA, else the exact SIMT kernel),
+//            folded in the tree's order by mm_fold_kernel.
+// n1 * n2 == 1 is the plain entry (its own split heuristics).
+namespace jb {
+namespace mm {
+template <int BNT>
+static jb_status launch_partials(const CUtensorMap &ma, const CUtensorMap &mb, float *part, uint64_t n,
+                                 uint64_t m, uint64_t l, int parts, cudaStream_t s) {
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    JB_CHECK_CUDA(cudaFuncSetAttribute(gemm_3xtf32_kernel<BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes<BNT>()));
+    attr_set[dev] = true;
+  }
+  dim3 grid((unsigned)((l + BNT - 1) / BNT), (unsigned)((n + BM - 1) / BM), (unsigned)parts);
+  void *tok = prof_begin("matmul_tcgen05", s);
+  gemm_3xtf32_kernel<BNT><<<grid, THREADS, smem_bytes<BNT>(), s>>>(ma, mb, part, (int)n, (int)l, (int)m, part);
+  prof_end(tok, s);
+  JB_LAUNCHED("matmul_tcgen05");
+  return JB_OK;
+}
+}  // namespace mm
+}  // namespace jb
+
+extern "C" jb_status jb_matmul_sched_f32(uint64_t n, uint64_t m, uint64_t l, const float *a, const float *b,
+                                         float *res, uint32_t tile_n, uint32_t n1, uint32_t n2, void *stream) {
+  JB_REQUIRE(n < (1ull << 31) && m < (1ull << 31) && l < (1ull << 31), "matmul: extents too large");
+  JB_REQUIRE(tile_n == 64 || tile_n == 128, "matmul: tile_n must be 64 or 128 (got %u)", tile_n);
+  JB_REQUIRE(n1 >= 1 && n2 >= 1 && (uint64_t)n1 * n2 <= 4096, "matmul: bad reduction tree %u x %u", n1, n2);
+  const uint64_t parts = (uint64_t)n1 * n2;
+  JB_REQUIRE(m % parts == 0, "matmul: %llu partials do not divide m = %llu (the schedule's constraint)",
+             (unsigned long long)parts, (unsigned long long)m);
+  if (parts == 1 && tile_n == 128) return jb_matmul_f32(n, m, l, a, b, res, stream);
+  if (n == 0 || l == 0) return JB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  JB_REQUIRE(res, "matmul: null result pointer");
+  if (m == 0) {
+    JB_CHECK_CUDA(cudaMemsetAsync(res, 0, n * l * 4, s));
+    return JB_OK;
+  }
+  JB_REQUIRE(a && b, "matmul: null pointer");
+  const uint64_t chunk = m / parts;
+  const uint64_t mn = n * l;
+  float *part = (float *)workspace(parts * mn * 4, s);
+  if (!part) return JB_ECUDA;
+  const bool tma_ok = (m % 4 == 0) && (l % 4 == 0) && chunk % BK == 0 && ((uintptr_t)a % 16 == 0) &&
+                      ((uintptr_t)b % 16 == 0) && tmap_encode_fn() != nullptr;
+  CUtensorMap ma, mb;
+  if (tma_ok && make_map(&ma, a, n, m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+      make_map(&mb, b, m, l, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+    jb_status st = tile_n == 64 ? launch_partials<64>(ma, mb, part, n, m, l, (int)parts, s)
+                                : launch_partials<128>(ma, mb, part, n, m, l, (int)parts, s);
+    if (st != JB_OK) return st;
+  } else {
+    dim3 grid((unsigned)((l + 31) / 32), (unsigned)((n + 31) / 32));
+    for (uint64_t p = 0; p < parts; p++) {
+      matmul_exact_range_kernel<<<grid, 256, 0, s>>>(a, b, part + p * mn, (int)n, (int)l, (int)chunk, (int)m,
+                                                     (int)(p * chunk));
+      JB_LAUNCHED("matmul_exact_range");
+    }
+  }
+  const long long blocks = std::min<long long>((long long)(mn + 255) / 256, (long long)sm_count() * 8);
+  mm_fold_kernel<<<(unsigned)blocks, 256, 0, s>>>(part, res, (long long)mn, (int)n1, (int)n2);
+  JB_LAUNCHED("matmul_fold");
   return JB_OK;
 }

@@ -327,6 +327,10 @@ class KernelChoice:
     plan: LaunchPlan     # the schedule's §4.4 plan of the function
     dyn_consts: list = field(default_factory=list)   # the entry's dyn-consts
     detail: str = ""
+    # launch parameters the schedule implies (recognize.py): matmul's CTA
+    # tile width from the J fork's fork-tile factor and the K reduction tree
+    # of fork-fission (partials per level), SURVEY.md §8(f)1
+    params: dict = field(default_factory=dict)
 
 
 def select_kernel(module, entry: str, dyn_consts: Sequence[int]) -> KernelChoice:
@@ -350,7 +354,13 @@ def select_kernel(module, entry: str, dyn_consts: Sequence[int]) -> KernelChoice
         raise _err(UnsupportedError, f"no B200 kernel computes function {entry!r}: " +
                    "; ".join(f"not {k} ({v})" for k, v in why.items()))
     sym, geo = B200_KERNELS[rec.entry]
-    return KernelChoice(rec.entry, sym, geo, "structure", plan, rec.dyn_consts, rec.detail)
+    if rec.entry == "matmul":
+        tn, (n1, n2) = rec.params.get("tile_n", 128), rec.params.get("tree", (1, 1))
+        if tn != 128 or n1 * n2 > 1:
+            sym = "jb_matmul_sched_f32"
+            geo = (f"grid (l/{tn}, n/128, {n1 * n2} K partials), 320 threads, 3xTF32 tcgen05 128x{tn} tiles; "
+                   f"partials folded {n1}x{n2} in the tree's order (mm_fold_kernel)")
+    return KernelChoice(rec.entry, sym, geo, "structure", plan, rec.dyn_consts, rec.detail, dict(rec.params))
 
 
 def execute_module(module, entry: str, dyn_consts, args, max_steps: int = 50_000_000):
@@ -359,4 +369,4 @@ def execute_module(module, entry: str, dyn_consts, args, max_steps: int = 50_000
     from .api import execute
     del max_steps
     choice = select_kernel(module, entry, [int(x) for x in dyn_consts])
-    return execute(choice.entry, choice.dyn_consts, args), choice
+    return execute(choice.entry, choice.dyn_consts, args, choice.params), choice

@@ -49,7 +49,7 @@ imports the reference on its own.
 from __future__ import annotations
 
 import importlib
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 COMMUTATIVE = frozenset({"add", "mul", "min", "max", "eq", "ne", "and", "or", "xor"})
@@ -111,6 +111,7 @@ class Recognised:
     entry: str                 # B200 entry (api.ENTRIES key)
     dyn_consts: list           # the entry's dyn-consts, in ITS order
     detail: str
+    params: dict = field(default_factory=dict)  # launch parameters the schedule implies
 
 
 class _Graph:
@@ -264,6 +265,158 @@ def _expr(g: _Graph, i, chain, reads):
     raise NotRecognised(f"value node %{i} ({n.kind})")
 
 
+# ---------------------------------------------------- scalar-accumulator folds
+# ``let s = 0; for k { s += a[i,k]*b[k,j]; } res[i,j] = s;`` and what the
+# reduction_tree! macro (fork-chunk, fork-reshape,
+# monoid-reassociate, fork-fission) makes of it: the written value is a fold
+# (a reduce over a fork, or a loop phi) starting at 0.0 whose term is either
+# the product or a read of a partials array, itself written once per thread
+# of a "top" fork with the fold of one K chunk (passes/fissfuse.py:134-145).
+@dataclass
+class _Fold:
+    levels: list     # [("fork", f) | ("loop", region)], outermost first: one sequential fold
+    term: int        # the summand node
+    digits: list     # mixed-radix digits of the fold's iteration, most significant first
+
+
+def _fold_step(g: _Graph, v):
+    """(level, init, body) of a reduce / loop phi."""
+    n = g.node(v)
+    if n.kind == "reduce" and len(n.inputs) == 2:
+        if n.control not in g.fork_of_join:
+            raise NotRecognised(f"reduce %{v} hangs off an unmatched join")
+        return ("fork", g.fork_of_join[n.control]), n.inputs[0], n.inputs[1]
+    if n.kind == "phi" and len(n.inputs) == 2:
+        g.loop_induction(n.control)  # a counted loop
+        return ("loop", n.control), n.inputs[0], n.inputs[1]
+    raise NotRecognised(f"%{v} ({n.kind}) is not a fold")
+
+
+def _level_digits(g: _Graph, lv) -> list:
+    kind, x = lv
+    if kind == "fork":
+        fk = g.node(x)
+        return [(("tid", x, d), int(g.ev(e, g.dcs))) for d, e in enumerate(fk.factors)]
+    phi, trip = g.loop_induction(x)
+    return [(("loop", x), trip)]
+
+
+def _is_zero_f32(g: _Graph, i) -> bool:
+    n = g.node(i)
+    return (n.kind == "constant" and n.const is not None and not n.const.is_zero_collection and
+            _scalar_name(n.ty) == "f32" and float(n.const.value) == 0.0)
+
+
+def _fold(g: _Graph, v) -> _Fold:
+    """A sequential f32 sum starting at 0.0: one fold level, or several whose
+    inner levels start from the enclosing level's running value (fork-chunk
+    without monoid-reassociate)."""
+    lv, init, body = _fold_step(g, v)
+    if not _is_zero_f32(g, init):
+        raise NotRecognised(f"fold %{v} does not start at 0.0")
+    levels, cur = [lv], v
+    while True:
+        b = g.node(body)
+        if b.kind == "binary" and b.op == "add" and _scalar_name(b.ty) == "f32" and len(b.inputs) == 2 \
+                and list(b.inputs).count(cur) == 1:
+            term = b.inputs[0] if b.inputs[1] == cur else b.inputs[1]
+            break
+        inner_lv, inner_init, inner_body = _fold_step(g, body)  # a carried inner level
+        if inner_init != cur:
+            raise NotRecognised(f"fold level %{body} does not continue %{cur}")
+        levels.append(inner_lv)
+        cur, body = body, inner_body
+    digits = [d for lv_ in levels for d in _level_digits(g, lv_)]
+    return _Fold(levels, term, digits)
+
+
+def _partials(g: _Graph, arr):
+    """A partials array: one reduce over a one-dimensional top fork G whose
+    body writes element [tid_G] once from a constant (zero / no-reset)
+    collection.  Returns (G, N, inner fold value)."""
+    n = g.node(arr)
+    if n.kind != "reduce" or n.control not in g.fork_of_join or len(n.inputs) != 2:
+        raise NotRecognised(f"partials %{arr} is not a fork reduce")
+    G = g.fork_of_join[n.control]
+    fk = g.node(G)
+    if len(fk.factors) != 1:
+        raise NotRecognised(f"top fork %{G} is not one-dimensional")
+    N = int(g.ev(fk.factors[0], g.dcs))
+    c = g.node(n.inputs[0])
+    if c.kind != "constant" or c.const is None or not c.const.is_zero_collection:
+        raise NotRecognised(f"partials %{arr} do not start from a constant collection")
+    w = g.node(n.inputs[1])
+    if w.kind != "write" or w.inputs[0] != arr or len(w.indices) != 1 or len(w.indices[0].ids) != 1:
+        raise NotRecognised(f"partials %{arr} are not written once per thread")
+    if g.digits(w.indices[0].ids[0]) != [(("tid", G, 0), N)]:
+        raise NotRecognised(f"partials %{arr} are not indexed by the top fork's thread")
+    return G, N, w.inputs[1]
+
+
+def _partials_read(g: _Graph, t):
+    r = g.node(t)
+    if r.kind != "read" or len(r.indices) != 1 or not hasattr(r.indices[0], "ids") or len(r.indices[0].ids) != 1:
+        raise NotRecognised(f"term %{t} is neither a product nor a partials read")
+    return r.inputs[0], g.digits(r.indices[0].ids[0])
+
+
+def _product_reads(g: _Graph, t):
+    """mul(read P0[x, y], read P1[y', z]) -> (P0 ids, P1 ids)"""
+    m_ = g.node(t)
+    if m_.kind != "binary" or m_.op != "mul" or _scalar_name(m_.ty) != "f32" or len(m_.inputs) != 2:
+        raise NotRecognised(f"term %{t} is not a product")
+    by = {}
+    for x in m_.inputs:
+        r = g.node(x)
+        c = g.node(r.inputs[0]) if r.kind == "read" else None
+        if c is None or c.kind != "param" or len(r.indices) != 1 or not hasattr(r.indices[0], "ids") \
+                or len(r.indices[0].ids) != 2:
+            raise NotRecognised(f"product operand %{x} is not a 2-D parameter read")
+        by[c.index] = tuple(r.indices[0].ids)
+    if set(by) != {0, 1}:
+        raise NotRecognised("the product does not read parameters 0 and 1")
+    return by[0], by[1]
+
+
+def _accumulator_form(g: _Graph, value):
+    """The written value as a fold tree.  Returns (P0 ids, P1 ids, K digits
+    the kernel must see, levels used, tree counts [n1, n2]) where the K
+    index is (partition p) * chunk + k' with p = p1 * n2 + p2 folded
+    outermost level first."""
+    top = _fold(g, value)
+    used = list(top.levels)
+    if g.node(top.term).kind == "binary":
+        a_ids, b_ids = _product_reads(g, top.term)
+        return a_ids, b_ids, top.digits, used, [1, 1]
+    arr1, idx1 = _partials_read(g, top.term)
+    if idx1 != top.digits:
+        raise NotRecognised("the bottom fold does not read its own partial")
+    G1, N1, v1 = _partials(g, arr1)
+    if _span(idx1) != N1:
+        raise NotRecognised("the bottom fold does not cover the partials")
+    used.append(("fork", G1))
+    f1 = _fold(g, v1)
+    used += f1.levels
+    if g.node(f1.term).kind == "binary":  # one fission: tree [N1]
+        a_ids, b_ids = _product_reads(g, f1.term)
+        return a_ids, b_ids, [(("tid", G1, 0), N1)] + f1.digits, used, [N1, 1]
+    # reduction_tree! applied to the bottom fold again: the middle fold sums
+    # partials [q * c + p'] of the deeper array (q = the middle top fork)
+    arr2, idx2 = _partials_read(g, f1.term)
+    if idx2 != [(("tid", G1, 0), N1)] + f1.digits:
+        raise NotRecognised("the middle fold does not read its chunk of the partials")
+    G2, N2, v2 = _partials(g, arr2)
+    if _span(idx2) != N2:
+        raise NotRecognised("the middle folds do not cover the partials")
+    used.append(("fork", G2))
+    f2 = _fold(g, v2)
+    used += f2.levels
+    if g.node(f2.term).kind != "binary":
+        raise NotRecognised("reduction trees deeper than three layers are not supported")
+    a_ids, b_ids = _product_reads(g, f2.term)
+    return a_ids, b_ids, [(("tid", G2, 0), N2)] + f2.digits, used, [N1, N2 // N1]
+
+
 def _recognise_matmul(g: _Graph) -> Recognised:
     fn = g.fn
     ret = [i for i, n in g.nodes.items() if n.kind == "return"]
@@ -276,6 +429,9 @@ def _recognise_matmul(g: _Graph) -> Recognised:
     w = g.node(next(iter(writes)))
     if len(w.indices) != 1 or not hasattr(w.indices[0], "ids") or len(w.indices[0].ids) != 2:
         raise NotRecognised("the write is not a 2-D positional write")
+    wn = g.node(w.inputs[1])
+    if wn.kind in ("reduce", "phi"):
+        return _recognise_matmul_acc(g, w, levels)
     reads: list = []
     tree = _expr(g, w.inputs[1], chain, reads)
     want = ("add", "f32", ("mul", "f32", ("read", "P0", 1), ("read", "P1", 2)), ("read", "ACC", 0))
@@ -321,7 +477,63 @@ def _recognise_matmul(g: _Graph) -> Recognised:
     if len(fn.param_types) != 2:
         raise NotRecognised("matmul takes exactly two parameters")
     return Recognised("matmul", [n, m, l],
-                      f"res[i,j] += a[i,k]*b[k,j] over I={_fmt(wi)} J={_fmt(wj)} K={_fmt(a1)}")
+                      f"res[i,j] += a[i,k]*b[k,j] over I={_fmt(wi)} J={_fmt(wj)} K={_fmt(a1)}",
+                      {"tile_n": _tile_n(wj), "tree": (1, 1)})
+
+
+def _check_extents(g: _Graph, n, m, l):
+    fn = g.fn
+    ev = lambda ty: tuple(int(g.ev(e, g.dcs)) for e in ty.extents)  # noqa: E731
+    if len(fn.param_types) != 2:
+        raise NotRecognised("matmul takes exactly two parameters")
+    pa, pb = fn.param_types[0], fn.param_types[1]
+    for ty, want_ext, what in ((pa, (n, m), "a"), (pb, (m, l), "b"), (fn.return_type, (n, l), "result")):
+        if type(ty).__name__ != "ArrayType" or ev(ty) != want_ext:
+            raise NotRecognised(f"{what} extents differ from the iteration space {want_ext}")
+        if _elem(ty) != "f32":
+            raise NotRecognised(f"{what} is not f32")
+
+
+def _tile_n(wj) -> int:
+    """CTA tile width from the J axis: the innermost digit of a tiled J
+    (fork-tile's inner factor, passes/forks.py:58-62) <= 64 -> 64 columns,
+    otherwise (or untiled) 128."""
+    return 64 if len(wj) > 1 and wj[-1][1] <= 64 else 128
+
+
+def _recognise_matmul_acc(g: _Graph, w, coll_levels) -> Recognised:
+    """res[i, j] = (fold tree over k of a[i, k] * b[k, j]) written once per
+    (i, j): the scalar-accumulator form, plain or as a reduction tree."""
+    a_ids, b_ids, kdig, used, tree = _accumulator_form(g, w.inputs[1])
+    wi, wj = (g.digits(x) for x in w.indices[0].ids)
+    a0, a1 = (g.digits(x) for x in a_ids)
+    b0, b1 = (g.digits(x) for x in b_ids)
+    if a0 != wi or b1 != wj:
+        raise NotRecognised("operand indices are not a[i, .], b[., j] of the written element")
+    if a1 != kdig or b0 != kdig:
+        raise NotRecognised("the k index is not (partition, chunk offset) of the fold tree "
+                            f"(a: {_fmt(a1)}, b: {_fmt(b0)}, tree: {_fmt(kdig)})")
+    srcs = [s_ for d in (wi, wj) for s_, _ in d]
+    want = set()
+    for kind, lv in coll_levels:
+        want |= {s_ for s_, _ in _level_digits(g, (kind, lv))}
+    if len(srcs) != len(set(srcs)) or set(srcs) != want:
+        raise NotRecognised("the write's indices are not the result chain's loop levels")
+    ksrcs = [s_ for s_, _ in kdig]
+    used_srcs = {s_ for lv in used for s_, _ in _level_digits(g, lv)}
+    # every fold level's variable either indexes K or (bottom/middle folds)
+    # only selects partials; no level repeats the update
+    if len(ksrcs) != len(set(ksrcs)) or not set(ksrcs) <= used_srcs or set(ksrcs) & set(srcs):
+        raise NotRecognised("the k index reuses an induction variable")
+    n, l, m = _span(wi), _span(wj), _span(kdig)
+    _check_extents(g, n, m, l)
+    parts = tree[0] * tree[1]
+    if parts > 1 and m % parts:
+        raise NotRecognised(f"{parts} partials do not divide m = {m}")
+    params = {"tile_n": _tile_n(wj), "tree": tuple(tree)}
+    return Recognised("matmul", [n, m, l],
+                      f"res[i,j] = fold over k of a[i,k]*b[k,j], I={_fmt(wi)} J={_fmt(wj)} K={_fmt(kdig)}, "
+                      f"reduction tree {tree[0]}x{tree[1]}", params)
 
 
 def _canon(t):
