@@ -62,6 +62,8 @@ SIGNATURES = {
     "jb_bfs": [_u64, _u64, _vp, _vp, _vp, _u32, _vp, _vp],
     "jb_bp_train_f32": [_u64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "jb_host_register": [_vp, _u64],
+    "jb_bind_workspace": [_vp, _u64, _vp],
+    "jb_workspace_stats": [_vp, _vp, _vp],
     "jb_host_unregister": [_vp],
     "jb_selftest_fastmath": [_u64, _u64, ctypes.c_int, ctypes.c_int, _vp, _vp],
 }

@@ -27,6 +27,7 @@ from dataclasses import dataclass
 from typing import Any, Callable, Optional, Sequence
 
 import os
+import threading
 
 import numpy as np
 
@@ -159,7 +160,8 @@ class _Call:
             if not t.is_contiguous():
                 t = t.contiguous()
             elif copy and t.data_ptr() == x.data_ptr():
-                t = t.clone()
+                slot = _arena_take(t.shape, np_dtype)   # a runner's working copy
+                t = slot.copy_(t) if slot is not None else t.clone()
             return t
         h = hostmem.pinned_view(self.host_array(x, np_dtype, name))
         with torch.cuda.stream(self.stream):
@@ -167,6 +169,9 @@ class _Call:
 
     def empty(self, shape, np_dtype):
         torch = _torch()
+        slot = _arena_take(shape, np_dtype)  # inside Runner.run: the result lives in its arena
+        if slot is not None:
+            return slot
         return torch.empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np_dtype), device=self.device)
 
     def out(self, t):
@@ -267,6 +272,17 @@ def edge_detection(input, gaussian_filter, structure, sx, sy, theta):
         _check(_lib.load().jb_edge_f32(batch, n, m, gs, sz, sb, _ptr(din), _ptr(dg), _ptr(dst), _ptr(dsx),
                                        _ptr(dsy), _scalar(theta), _ptr(out), c.s), "edge_detection")
     return c.out(out)
+
+
+# Runner.run's arena (runner.py): while it is active, results and working
+# copies of the entry functions are carved out of the runner's one device
+# allocation instead of the caching allocator
+_ARENA = threading.local()
+
+
+def _arena_take(shape, np_dtype):
+    alloc = getattr(_ARENA, "alloc", None)
+    return alloc(tuple(int(x) for x in shape), np_dtype) if alloc is not None else None
 
 
 _PIPE_CACHE: dict = {}
@@ -603,6 +619,10 @@ class Entry:
     dyn_consts: tuple[str, ...]
     shapes: Callable[[Sequence[int], Sequence[Any]], list]  # expected (arg idx, shape) pairs
     run: Callable[..., Any]
+    # device memory the entry function takes for its results and working
+    # copies, as (shape, dtype) in request order, from the dyn-consts and
+    # arguments alone: the runner's allocation plan (runner.py)
+    results: Callable[[Sequence[int], Sequence[Any]], list] = lambda d, a: []
 
 
 def _sh(*pairs):
@@ -612,28 +632,38 @@ def _sh(*pairs):
 ENTRIES: dict[str, Entry] = {
     "matmul": Entry(("n", "m", "l"),
                     lambda d, a: _sh((0, (d[0], d[1])), (1, (d[1], d[2]))),
-                    lambda d, a, **kw: matmul(*a, **kw)),
+                    lambda d, a, **kw: matmul(*a, **kw),
+                    lambda d, a: [((d[0], d[2]), np.float32)]),
     "edge_detection": Entry(("n", "m", "gs", "sz", "sb"),
                             lambda d, a: _sh((0, (d[0], d[1])), (1, (d[2], d[2])), (2, (d[3], d[3])),
                                              (3, (d[4], d[4])), (4, (d[4], d[4]))),
-                            lambda d, a: edge_detection(*a)),
+                            lambda d, a: edge_detection(*a),
+                            lambda d, a: [(_shape(a[0]), np.float32)]),
     "cava": Entry(("r", "c", "num_ctrl_pts"),
                   lambda d, a: _sh((0, (3, d[0], d[1])), (1, (3, 3)), (2, (d[2], 3)), (3, (d[2], 3)),
                                    (4, (4, 3)), (5, (256, 3))),
-                  lambda d, a: cava(*a)),
+                  lambda d, a: cava(*a),
+                  lambda d, a: [(_shape(a[0]), np.uint8)]),
     "srad": Entry(("nrows", "ncols"),
                   lambda d, a: _sh((2, (d[0], d[1]))),
-                  lambda d, a: srad(*a)),
+                  lambda d, a: srad(*a),
+                  lambda d, a: [((d[0], d[1]), np.float32), ((max(int(a[0]), 1),), np.float32)]),
     "euler": Entry(("nelr",),
                    lambda d, a: _sh((1, (d[0],)), (2, (4, d[0])), (3, (4, 3, d[0])), (4, (5,)), (5, (5, d[0]))),
-                   lambda d, a: euler(*a)),
+                   lambda d, a: euler(*a),
+                   lambda d, a: [((5, d[0]), np.float32)]),
     "bfs": Entry(("n", "m"),
                  lambda d, a: _sh((0, (d[0],)), (1, (d[0],)), (2, (d[1],))),
-                 lambda d, a: bfs(*a)),
+                 lambda d, a: bfs(*a),
+                 lambda d, a: ([((1,), np.int32)] if d[1] == 0 else []) + [((d[0],), np.int32)]),
     "backprop": Entry(("input_n", "hidden_n", "output_n"),
                       lambda d, a: _sh((0, (d[0] + 1,)), (1, (d[0] + 1, d[1] + 1)), (2, (d[1] + 1, d[2] + 1)),
                                        (3, (d[2] + 1,)), (4, (d[0] + 1, d[1] + 1)), (5, (d[1] + 1, d[2] + 1))),
-                      lambda d, a: backprop(*a)),
+                      lambda d, a: backprop(*a),
+                      lambda d, a: [((d[0] + 1,), np.float32), ((d[0] + 1, d[1] + 1), np.float32),
+                                    ((d[1] + 1, d[2] + 1), np.float32), ((d[0] + 1, d[1] + 1), np.float32),
+                                    ((d[1] + 1, d[2] + 1), np.float32), ((d[1] + 1,), np.float32),
+                                    ((d[2] + 1,), np.float32), ((2,), np.float32)]),
 }
 
 

@@ -79,10 +79,31 @@ struct Arena {
 static std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
 static std::mutex g_arena_mu;
 
+// A caller-owned region bound as a stream's scratch (jb_bind_workspace: the
+// runner's single arena).  Requests it cannot hold take the
+// library's own arena below; the high-water mark tells the caller how much
+// to reserve next time.
+struct Bound {
+  void *ptr = nullptr;
+  size_t cap = 0;
+  size_t high = 0;      // largest request since binding
+  uint64_t spills = 0;  // requests larger than cap (served by the library arena)
+};
+static std::map<std::pair<int, cudaStream_t>, Bound> g_bound;
+
 void *workspace(size_t bytes, cudaStream_t s) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return nullptr;
   std::lock_guard<std::mutex> lk(g_arena_mu);
+  {
+    auto it = g_bound.find({dev, s});
+    if (it != g_bound.end()) {
+      Bound &b = it->second;
+      if (bytes > b.high) b.high = bytes;
+      if (bytes <= b.cap) return b.ptr;
+      b.spills++;
+    }
+  }
   Arena &a = g_arenas[{dev, s}];
   if (bytes <= a.cap) return a.ptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -218,6 +239,40 @@ jb_status jb_prof_read(const char *name, double *ms, uint64_t *count) {
   auto it = jb::g_prof_acc.find(name ? name : "");
   *ms = it == jb::g_prof_acc.end() ? 0.0 : it->second.first;
   *count = it == jb::g_prof_acc.end() ? 0 : it->second.second;
+  return JB_OK;
+}
+
+jb_status jb_bind_workspace(void *ptr, uint64_t bytes, void *stream) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
+    jb::set_error("jb_bind_workspace: no current device");
+    return JB_ECUDA;
+  }
+  JB_REQUIRE(((uintptr_t)ptr & 255) == 0, "jb_bind_workspace: region must be 256-byte aligned");
+  std::lock_guard<std::mutex> lk(jb::g_arena_mu);
+  const auto key = std::make_pair(dev, (cudaStream_t)stream);
+  if (!ptr) {
+    jb::g_bound.erase(key);
+    return JB_OK;
+  }
+  jb::Bound &b = jb::g_bound[key];
+  b.ptr = ptr;
+  b.cap = bytes;
+  b.high = 0;
+  b.spills = 0;
+  return JB_OK;
+}
+
+jb_status jb_workspace_stats(void *stream, uint64_t *high, uint64_t *spills) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
+    jb::set_error("jb_workspace_stats: no current device");
+    return JB_ECUDA;
+  }
+  std::lock_guard<std::mutex> lk(jb::g_arena_mu);
+  auto it = jb::g_bound.find({dev, (cudaStream_t)stream});
+  *high = it == jb::g_bound.end() ? 0 : it->second.high;
+  *spills = it == jb::g_bound.end() ? 0 : it->second.spills;
   return JB_OK;
 }
 
