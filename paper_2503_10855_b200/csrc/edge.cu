@@ -165,7 +165,7 @@ __global__ void edge_check_kernel(const float *__restrict__ gf, const float *__r
 }
 
 struct FusedArgs {
-  CUtensorMap tmap;     // [frames*n][m] input, box {76, 70} (valid if use_tma)
+  CUtensorMap tmap;     // [frames][n][m] input, box {76, 70, 1} (valid if use_tma)
   CUtensorMap pmap;     // [ring][n][m] packed ring, box {60, 60, 1} (valid if use_tma)
   int use_tma;
   const float *in;      // [frames][n][m]
@@ -231,10 +231,39 @@ __device__ __forceinline__ bool tile_interior(const FusedArgs &a, int y0, int x0
 __device__ __forceinline__ void stage_tile_tma(Smem &S, const FusedArgs &a, int f, int y0, int x0) {
   tc::fence_proxy_async_smem();  // the generic-proxy accesses of raw/inA are done
   tc::mbar_arrive_expect_tx(&S.tma_bar, IR * RP * 4);
-  // the chunk is a 2-D [frames*n][m] tensor: interior tiles never cross frames
-  // the input is read once: evict it first, so the packed ring (evict last)
-  // survives in L2 until its reject units read it
-  tc::tma_load_2d_hint(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, f * a.n + y0 - 5, tc::policy_evict_first());
+  // [frames][n][m] tensor: out-of-frame rows and columns of a border tile's
+  // box arrive as zeros (TMA out-of-bounds fill) and are replaced by the
+  // clamped replicas in smem (stage 0).  The input is read once: evict it
+  // first, so the packed ring (evict last) survives in L2 until its reject
+  // units read it
+  tc::tma_load_3d_hint(&S.raw[0][0], &a.tmap, &S.tma_bar, x0 - 8, y0 - 5, f, tc::policy_evict_first());
+}
+
+// stage 0 of a border tile: its TMA box holds zeros where it leaves the
+// frame; give those positions the clamped in-frame value, which is what the
+// gaussian's clamp-to-edge indexing reads.  The clamped source of every
+// out-of-frame position is an in-frame position of the box (never written
+// here), so one pass suffices; only out-of-frame rows and columns are
+// visited.
+__device__ __noinline__ void replicate_box_edges(Smem &S, const FusedArgs &a, int y0, int x0, int tid) {
+  const int ylo = max(0, 5 - y0), yhi = min(IR, a.n - (y0 - 5));  // in-frame box rows [ylo, yhi)
+  const int xlo = max(0, 8 - x0), xhi = min(RP, a.m - (x0 - 8));  // in-frame box columns
+  const int nr = ylo + (IR - yhi), nc = xlo + (RP - xhi);
+  const int rows_px = nr * RP, total = rows_px + (yhi - ylo) * nc;
+  for (int idx = tid; idx < total; idx += THREADS) {
+    int r, c;
+    if (idx < rows_px) {  // whole out-of-frame rows
+      const int k = idx / RP;
+      c = idx - k * RP;
+      r = k < ylo ? k : yhi + (k - ylo);
+    } else {              // out-of-frame columns of in-frame rows
+      const int j = idx - rows_px, q = j / nc, k = j - q * nc;
+      r = ylo + q;
+      c = k < xlo ? k : xhi + (k - xlo);
+    }
+    S.raw[r][c] = S.raw[min(max(r, ylo), yhi - 1)][min(max(c, xlo), xhi - 1)];
+  }
+  __syncthreads();
 }
 
 extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -279,6 +308,30 @@ __device__ __noinline__ void gauss_fast(int warp, int lane) {
   for (int o = 0; o < 8; o++) *reinterpret_cast<unsigned long long *>(&S.sm[r0 + o][2 * lane]) = acc[o];
 }
 
+// out-of-frame positions of a border tile's 64x64 smoothed region: NaN
+// (pads = true) or the clamped in-frame value.  Only those positions are
+// visited; their clamped sources are in-frame, so one pass suffices.
+__device__ __noinline__ void smooth_oob(Smem &S, const FusedArgs &a, int y0, int x0, int tid, bool pads) {
+  const int ylo = max(0, 2 - y0), yhi = min(SR, a.n - (y0 - 2));  // in-frame rows [ylo, yhi)
+  const int xlo = max(0, 2 - x0), xhi = min(SR, a.m - (x0 - 2));
+  const int nr = ylo + (SR - yhi), nc = xlo + (SR - xhi);
+  const int rows_px = nr * SR, total = rows_px + (yhi - ylo) * nc;
+  for (int idx = tid; idx < total; idx += THREADS) {
+    int r, c;
+    if (idx < rows_px) {  // whole out-of-frame rows
+      const int k = idx >> 6;
+      c = idx & 63;
+      r = k < ylo ? k : yhi + (k - ylo);
+    } else {              // out-of-frame columns of in-frame rows
+      const int j = idx - rows_px, q = j / nc, k = j - q * nc;
+      r = ylo + q;
+      c = k < xlo ? k : xhi + (k - xlo);
+    }
+    S.sm[r][c] = pads ? __int_as_float(0x7fffffff)
+                      : S.sm[min(max(r, ylo), yhi - 1)][min(max(c, xlo), xhi - 1)];
+  }
+}
+
 // end of a tile's compute: the packed tile leaves by bulk tensor store (TMA
 // path), the block max goes to the frame's atomicMax (thread 0's return value
 // is consumed a tile later, flush_done)
@@ -318,17 +371,28 @@ __device__ __forceinline__ unsigned tile_tail(Smem &S, const FusedArgs &a, int f
 //    sign of a zero, which the square erases) and x*(+-1), x*(+-2) exact; gy
 //    is carried negated (ny = -gy: every rounding is sign-symmetric).  The
 //    squares are FMUL2, the sum a scalar add.rn (single rounding each).
+template <bool BORDER>
 __device__ __forceinline__ unsigned sobel_pairs(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
                                              int lane, int warp) {
   const int k0 = warp < 7 ? warp * 8 : TH - 8;
   unsigned zlo = 0, zhi = 0;
   if (lane < 8) {
+    // border tiles: out-of-frame laplacian positions pad the dilation with 0
+    // and the erosion with 1 (masked out of both folds)
+    unsigned long long colmask = ~0ull;
+    if (BORDER) {
+      const int lo = max(0, 1 - x0), hi = min(LR - 1, a.m - x0);  // frame columns x0-1+lc in [0, m)
+      colmask = hi >= lo ? (((hi - lo + 1) >= 64 ? ~0ull : ((1ull << (hi - lo + 1)) - 1)) << lo) : 0ull;
+    }
     unsigned long long orr = 0, andd = ~0ull;
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-      const unsigned long long b = *reinterpret_cast<const unsigned long long *>(&S.lapbits[k0 + lane + i][0]);
-      orr |= b;
-      andd &= b;
+      const int lr = k0 + lane + i, gy = y0 - 1 + lr;
+      if (!BORDER || (gy >= 0 && gy < a.n)) {
+        const unsigned long long b = *reinterpret_cast<const unsigned long long *>(&S.lapbits[lr][0]);
+        orr |= b & colmask;
+        andd &= b | ~colmask;
+      }
     }
     const unsigned long long zc = (orr | (orr >> 1) | (orr >> 2)) & ~(andd & (andd >> 1) & (andd >> 2));
     zlo = (unsigned)zc;
@@ -363,7 +427,12 @@ __device__ __forceinline__ unsigned sobel_pairs(Smem &S, const FusedArgs &a, int
         const unsigned zl = __shfl_sync(0xffffffffu, zlo, k), zh = __shfl_sync(0xffffffffu, zhi, k);
         S.P[k0 + k][ca] = __float_as_uint(ga) | ((zl << (31 - lane)) & 0x80000000u);
         if (b_ok) S.P[k0 + k][lane + 32] = __float_as_uint(gb) | ((zh << (31 - lane)) & 0x80000000u);
-        bmax = fmaxf(bmax, fmaxf(ga, gb));
+        if (!BORDER) {
+          bmax = fmaxf(bmax, fmaxf(ga, gb));
+        } else if (y0 + k0 + k < a.n) {  // only in-frame pixels enter the max
+          if (x0 + ca < a.m) bmax = fmaxf(bmax, ga);
+          if (x0 + cb < a.m) bmax = fmaxf(bmax, gb);
+        }
       }
     }
     // keep the next rows' loads from being hoisted (register pressure: the
@@ -418,8 +487,15 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   // raw/inA are free from here on: prefetch the next (interior) tile by TMA
   if (prefetch && tid == 0) stage_tile_tma(S, a, nf, ny0, nx0);
   // out-of-frame smoothed positions take the clamped in-frame value, which is
-  // what the gradient's clamp-to-edge indexing reads
-  if (BORDER) {
+  // what the gradient's clamp-to-edge indexing reads.  The paired path first
+  // gives them NaN instead: FMNMX ignores NaN, so the plain separable
+  // laplacian then pads exactly like the oracle (0 for the dilation's max, 1
+  // for the erosion's min, both folds starting there); the replicas follow
+  // after the laplacian.
+  if (BORDER && SOBEL_STD) {
+    smooth_oob(S, a, y0, x0, tid, true);
+    __syncthreads();
+  } else if (BORDER) {
     for (int idx = tid; idx < SR * SR; idx += THREADS) {
       const int r = idx >> 6, c = idx & 63;
       const int gy = y0 - 2 + r, gx = x0 - 2 + c;
@@ -440,7 +516,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
       // separable 3x3 max/min rolled down the column
       float hx0 = 0.f, hx1 = 0.f, hn0 = 0.f, hn1 = 0.f, cprev = 0.f;
       bool i0 = true, i1 = true, i2 = true;
-      if (BORDER) {
+      if (BORDER && !SOBEL_STD) {
         i0 = gxc - 1 >= 0 && gxc - 1 < m;
         i1 = gxc >= 0 && gxc < m;
         i2 = gxc + 1 >= 0 && gxc + 1 < m;
@@ -450,7 +526,7 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
         const int sr = min(rb * 16 + k, SR - 1);
         const float a0 = S.sm[sr][scol], a1 = S.sm[sr][scol + 1], a2 = S.sm[sr][scol + 2];
         float hx2, hn2;
-        if (BORDER) {
+        if (BORDER && !SOBEL_STD) {
           const int gy = y0 - 2 + rb * 16 + k;
           const bool rin = gy >= 0 && gy < n;
           hx2 = fmaxf(fmaxf(rin && i0 ? a0 : -INFINITY, rin && i1 ? a1 : -INFINITY), rin && i2 ? a2 : -INFINITY);
@@ -503,7 +579,13 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
   __syncthreads();
   EDGE_T(2);
 
-  if (SOBEL_STD) return sobel_pairs(S, a, f, y0, x0, tid, lane, warp);
+  if (SOBEL_STD) {
+    if (BORDER) {  // the sobel's clamp-to-edge replicas (the NaN pads are no longer read)
+      smooth_oob(S, a, y0, x0, tid, false);
+      __syncthreads();
+    }
+    return sobel_pairs<BORDER>(S, a, f, y0, x0, tid, lane, warp);
+  }
 
   // ---- stage 2b: zero crossings (bit masks), one thread per output row
   if (tid < TH) {
@@ -908,8 +990,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     tc::mbar_init(&S.tma_bar, 1);
     tc::fence_mbar_init();
     publish_desc((int)atomicAdd(a.sched, 1u));
-    if (S.next_tile < total && a.use_tma && tile_interior(a, S.nt_y0, S.nt_x0))
-      stage_tile_tma(S, a, S.nt_f, S.nt_y0, S.nt_x0);
+    if (S.next_tile < total && a.use_tma) stage_tile_tma(S, a, S.nt_f, S.nt_y0, S.nt_x0);
   }
   __syncthreads();
   int tile = S.next_tile, f = S.nt_f, y0 = S.nt_y0, x0 = S.nt_x0;  // current tile
@@ -944,12 +1025,12 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       }
     }
     EDGE_T(6);
-    const bool interior = tile_interior(a, y0, x0);
     PixGuard pg;
-    if (a.use_tma && interior) {
-      // ---- stage 0 (interior): the TMA issued during the previous tile
+    if (a.use_tma) {
+      // ---- stage 0: the TMA issued during the previous tile
       tc::mbar_wait(&S.tma_bar, tma_phase);
       tma_phase ^= 1u;
+      if (!tile_interior(a, y0, x0)) replicate_box_edges(S, a, y0, x0, tid);
       // inA = raw shifted by 3 columns, checking the guard on the way
 #pragma unroll
       for (int i = 0; i < RPW; i++) {
@@ -1006,12 +1087,14 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     const int all_ok = __syncthreads_and(pg.ok());
     EDGE_T(0);
     const int t2 = S.next_tile, f2 = S.nt_f, y2 = S.nt_y0, x2 = S.nt_x0;
-    const bool prefetch = t1 < total && a.use_tma && tile_interior(a, y1, x1);
+    const bool prefetch = t1 < total && a.use_tma;
     const bool border = (y0 < 2) || (x0 < 2) || (y0 + SR - 2 > n) || (x0 + SR - 2 > m);
     unsigned amax;
     if (filters_fast && all_ok) {
-      if (border) amax = edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
-      else if (sobel_std && a.use_tma) amax = edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+      if (sobel_std && a.use_tma) {
+        if (border) amax = edge_tile<true, true, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+        else amax = edge_tile<true, false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
+      } else if (border) amax = edge_tile<true, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
       else amax = edge_tile<true, false>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     } else {
       amax = edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
@@ -1320,10 +1403,10 @@ static jb_status run_fused(uint64_t batch, uint64_t n, uint64_t m, const float *
   }
   fa.use_tma = 0;
   if (m % 4 == 0 && ((uintptr_t)in % 16) == 0 && tmap_encode_fn() != nullptr) {
-    const uint64_t dims[2] = {m, n * (uint64_t)batch};
-    const uint64_t strides[1] = {m * 4};
-    const uint32_t box[2] = {(uint32_t)RP, (uint32_t)IR};
-    fa.use_tma = make_tmap_f32(&fa.tmap, in, 2, dims, strides, box, 0) ? 1 : 0;
+    const uint64_t dims[3] = {m, n, (uint64_t)batch};
+    const uint64_t strides[2] = {m * 4, n * m * 4};
+    const uint32_t box[3] = {(uint32_t)RP, (uint32_t)IR, 1};
+    fa.use_tma = make_tmap_f32(&fa.tmap, in, 3, dims, strides, box, 0) ? 1 : 0;
     // the packed ring as [ring][n][m] u32 (bit copies: the f32 map type is fine)
     const uint64_t pdims[3] = {m, n, (uint64_t)ring};
     const uint64_t pstrides[2] = {m * 4, slot_px * 4};
