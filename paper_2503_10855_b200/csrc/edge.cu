@@ -186,7 +186,7 @@ struct FusedArgs {
   int vec4;             // frame_px % 4 == 0 and out 16-byte aligned
   long long frame_px, slot_px;
   int lag;              // tiles of frame f + lag run the reject units of frame f
-  int opts;             // experiment bits (JB_EDGE_OPTS): 1 no discard
+  int opts;             // experiment bits (JB_EDGE_OPTS): 2 discard the ring lines after their unit
   uint32_t *obits;      // bit-packed edge maps [frames][frame_words] (instead of out), or null
   long long frame_words;// ceil(frame_px / 32): bit b of word w is pixel 32w + b
 };
@@ -847,9 +847,13 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   float *dst = a.obits ? nullptr : a.out + (size_t)f * a.frame_px + b0;
   // unit starts are multiples of 1024 pixels: whole words
   uint32_t *wdst = a.obits ? a.obits + (size_t)f * a.frame_words + (b0 >> 5) : nullptr;
-  // read once (the discards' memory clobbers would reload it from the
-  // parameter block every pass)
-  const bool disc = !(a.opts & 1);
+  // Ring lines are NOT discarded by default: the slot is rewritten in place a
+  // few frames later (its lines stay L2-resident, evict_last), and the
+  // discards plus the gpu-scope fence each discarding lane needs before the
+  // unit is counted cost more than they save (68.3 k vs 69.2 k frames/s,
+  // profiles/r02_kernel_experiments.txt).  Read once: the discards' memory
+  // clobbers would reload the flag from the parameter block every pass.
+  const bool disc = (a.opts & 2) != 0;
   // pass <=> A <= (int)p <= (int)0xff800000  <=>  p - Au < Ku (unsigned;
   // Ku = 0 when nothing can pass)
   const unsigned Au = (unsigned)A;
@@ -1100,24 +1104,31 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       amax = edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     }
     // ---- tile done + help the reject queue along (at most one unit per
-    // tile).  TMA path: this tile's bulk store was just issued and the
-    // previous tile is counted (its store has landed by now).  STG path: the
-    // barrier at the end of edge_tile orders the CTA's stores before thread
-    // 0's release fence (cumulative).
+    // tile).  Thread 0 first decides the unit (its frame's probes were
+    // issued at the tile top) and releases the CTA; it counts the previous
+    // tile -- its bulk store has landed by now; the count's gpu-scope fences
+    // are the slow part -- after the barrier, while the other warps already
+    // run the reject unit.  STG path: the barrier at the end of edge_tile
+    // orders the CTA's stores before thread 0's release fence (cumulative).
+    bool counted = false;
     if (tid == 0) {
-      if (a.use_tma) {
-        flush_done(a, q, pd_max, true);
-        q.pd = f;
-        pd_max = amax;  // a register: consumed (waited for) one tile later
-      } else {
+      if (!a.use_tma) {
         fence_acq_rel();
         red_add(a.done + f, 1u);
+        counted = true;
       }
       int v = q.ru, A = 0;
       if (v >= 0) {
         const int rf = v / a.units;
         if (!frame_bound(a, rf, rf_.rr, rf_.rdn, A, q.acq)) {
-          flush_done(a, q, pd_max, false);
+          // rare: count this CTA's tiles before waiting (others may wait on them)
+          if (!counted) {
+            flush_done(a, q, pd_max, true);
+            q.pd = f;
+            pd_max = amax;
+            flush_done(a, q, pd_max, false);
+            counted = true;
+          }
           A = wait_frame(a, rf, q.acq);
         }
       }
@@ -1125,6 +1136,11 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       S.lo = A;
     }
     __syncthreads();
+    if (tid == 0 && !counted) {
+      flush_done(a, q, pd_max, true);
+      q.pd = f;
+      pd_max = amax;  // a register: consumed (waited for) one tile later
+    }
     EDGE_T(7);
     if (S.hflag >= 0) reject_unit(a, S.hflag, S.lo);
     EDGE_T(5);
