@@ -332,30 +332,31 @@ __device__ __noinline__ void smooth_oob(Smem &S, const FusedArgs &a, int y0, int
   }
 }
 
-// end of a tile's compute: the packed tile leaves by bulk tensor store (TMA
-// path), the block max goes to the frame's atomicMax (thread 0's return value
-// is consumed a tile later, flush_done)
+// end of a tile's compute, before the CTA barrier that the main loop shares
+// with the reject-unit decision: P is handed to the async proxy (its bulk
+// tensor store is issued by thread 0 after the barrier, with the block max's
+// atomicMax: tile_store)
 __device__ __forceinline__ unsigned tile_tail(Smem &S, const FusedArgs &a, int f, int y0, int x0, int tid,
                                               int lane, int warp, float bmax) {
-  unsigned amax = 0;
   if (a.use_tma) tc::fence_proxy_async_smem();  // P -> async proxy
   bmax = warp_max(bmax);
   if (lane == 0) S.wmax[warp] = bmax;
-  __syncthreads();
-  if (tid == 0) {
-    if (a.use_tma) {
-      tc::tma_store_3d_hint(&a.pmap, &S.P[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
-      tc::bulk_commit();
-    }
-    float v = S.wmax[0];
-#pragma unroll
-    for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
-    // thread 0's atom: its return value (consumed a tile later, flush_done)
-    // tells that the max has been performed before the tile is counted
-    if (!(v != v)) amax = atomicMax(a.fmax + f, __float_as_uint(v));
+  return 0;
+}
+
+// thread 0, after the barrier: the packed tile leaves by bulk tensor store
+// (TMA path), the block max goes to the frame's atomicMax; its return value
+// (consumed a tile later, flush_done) tells that the max has been performed
+// before the tile is counted
+__device__ __forceinline__ unsigned tile_store(Smem &S, const FusedArgs &a, int f, int y0, int x0) {
+  if (a.use_tma) {
+    tc::tma_store_3d_hint(&a.pmap, &S.P[0][0], x0, y0, f % a.ring, tc::policy_evict_last());
+    tc::bulk_commit();
   }
-  EDGE_T(4);
-  return amax;
+  float v = S.wmax[0];
+#pragma unroll
+  for (int w = 1; w < THREADS / 32; w++) v = fmaxf(v, S.wmax[w]);
+  return !(v != v) ? atomicMax(a.fmax + f, __float_as_uint(v)) : 0u;
 }
 
 // stages 2b + 2c of an interior tile with the standard sobel pair (TMA path):
@@ -1104,31 +1105,22 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       amax = edge_tile<false, true>(S, a, f, y0, x0, tid, lane, warp, prefetch, f1, y1, x1);
     }
     // ---- tile done + help the reject queue along (at most one unit per
-    // tile).  Thread 0 first decides the unit (its frame's probes were
-    // issued at the tile top) and releases the CTA; it counts the previous
-    // tile -- its bulk store has landed by now; the count's gpu-scope fences
-    // are the slow part -- after the barrier, while the other warps already
-    // run the reject unit.  STG path: the barrier at the end of edge_tile
-    // orders the CTA's stores before thread 0's release fence (cumulative).
-    bool counted = false;
+    // tile).  Before the CTA barrier that completes the tile, thread 0
+    // decides the unit (its frame's probes were issued at the tile top); the
+    // one barrier then publishes P, the warp maxima and the unit.  After it,
+    // thread 0 issues the tile's bulk store and atomicMax and counts the
+    // previous tile (its store has landed by now; the count's gpu-scope
+    // fences are the slow part) while the other warps already run the
+    // reject unit.  STG path: the barrier orders the CTA's stores before
+    // thread 0's release fence (cumulative).
     if (tid == 0) {
-      if (!a.use_tma) {
-        fence_acq_rel();
-        red_add(a.done + f, 1u);
-        counted = true;
-      }
       int v = q.ru, A = 0;
       if (v >= 0) {
         const int rf = v / a.units;
         if (!frame_bound(a, rf, rf_.rr, rf_.rdn, A, q.acq)) {
-          // rare: count this CTA's tiles before waiting (others may wait on them)
-          if (!counted) {
-            flush_done(a, q, pd_max, true);
-            q.pd = f;
-            pd_max = amax;
-            flush_done(a, q, pd_max, false);
-            counted = true;
-          }
+          // rare: count the previous tile before waiting (others may wait on
+          // it; this tile is of frame f != rf and is counted after the wait)
+          if (a.use_tma) flush_done(a, q, pd_max, false);
           A = wait_frame(a, rf, q.acq);
         }
       }
@@ -1136,11 +1128,19 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
       S.lo = A;
     }
     __syncthreads();
-    if (tid == 0 && !counted) {
-      flush_done(a, q, pd_max, true);
-      q.pd = f;
-      pd_max = amax;  // a register: consumed (waited for) one tile later
+    EDGE_T(4);
+    if (tid == 0) {
+      const unsigned am = tile_store(S, a, f, y0, x0);
+      if (a.use_tma) {
+        flush_done(a, q, pd_max, true);
+        q.pd = f;
+        pd_max = am;  // a register: consumed (waited for) one tile later
+      } else {
+        fence_acq_rel();  // orders the CTA's stores (barrier) and the atom before the count
+        red_add(a.done + f, 1u);
+      }
     }
+    (void)amax;
     EDGE_T(7);
     if (S.hflag >= 0) reject_unit(a, S.hflag, S.lo);
     EDGE_T(5);
