@@ -65,6 +65,14 @@ struct Args {
   uint32_t n;
 };
 
+// the CSR arrays are streamed (each edge id read once per traversal):
+// evict-first loads keep the L2-resident level bytes and visited bitmap in L2
+#ifdef BFS_LDG
+#define CSR_LD(p) __ldg(p)
+#else
+#define CSR_LD(p) __ldcs(p)
+#endif
+
 __device__ __forceinline__ void red_or(uint32_t *p, uint32_t v) {
   asm volatile("red.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -191,8 +199,8 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
             if (scan) live = __ldcg(a.level + i) == lb;
             else u = __ldcg(fq + i);
             if (live) {
-              e0[k] = __ldg(a.starting + u);
-              ne[k] = __ldg(a.nedges + u);
+              e0[k] = CSR_LD(a.starting + u);
+              ne[k] = CSR_LD(a.nedges + u);
             }
           }
         }
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
 #pragma unroll
               for (int j = 0; j < EB; j++) {
                 const uint32_t i = b + j * 32 + lane;
-                v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
+                v[j] = i < cnt ? CSR_LD(a.edges + eb[i]) : 0xffffffffu;
               }
               // bitmap filter (may be stale towards "unseen": L1, lost races)
 #pragma unroll
@@ -268,8 +276,8 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
             if (scan) live = __ldcg(a.level + i) == lb;
             else u = __ldcg(fq + i);
             if (live) {
-              e0[k] = __ldg(a.starting + u);
-              ne[k] = __ldg(a.nedges + u);
+              e0[k] = CSR_LD(a.starting + u);
+              ne[k] = CSR_LD(a.nedges + u);
             }
           }
         }
@@ -306,7 +314,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
 #pragma unroll
               for (int j = 0; j < EB; j++) {
                 const uint32_t i = b + j * 32 + lane;
-                v[j] = i < cnt ? __ldg(a.edges + eb[i]) : 0xffffffffu;
+                v[j] = i < cnt ? CSR_LD(a.edges + eb[i]) : 0xffffffffu;
               }
               // probes may come from L1 (stale only towards "unseen": the
               // atomicOr below re-checks)
