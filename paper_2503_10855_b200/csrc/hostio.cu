@@ -13,6 +13,7 @@
 #include <emmintrin.h>
 #include <stdint.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -31,9 +32,20 @@ namespace hostio {
 // returning when all are done.  One job at a time (callers serialise on mu).
 class Pool {
  public:
+  // One pool per process: a child created by fork() inherits the pool
+  // object but none of its threads, so it builds its own (the parent's
+  // object is left alone, never joined from the child).
   static Pool &get() {
-    static Pool p;
-    return p;
+    static std::mutex m;
+    static Pool *p = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> lk(m);
+    const pid_t me = getpid();
+    if (!p || owner != me) {
+      p = new Pool();  // intentionally never destroyed: workers wait until process exit
+      owner = me;
+    }
+    return *p;
   }
   int size() const { return (int)workers_.size() + 1; }
   void run(int n, const std::function<void(int)> &fn) {
@@ -57,17 +69,12 @@ class Pool {
   Pool() {
     unsigned hw = std::thread::hardware_concurrency();
     int k = (int)std::min(hw ? hw : 4u, 32u) - 1;
-    for (int i = 0; i < k; i++) workers_.emplace_back([this] { loop(); });
-  }
-  ~Pool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
+    for (int i = 0; i < k; i++) {
+      workers_.emplace_back([this] { loop(); });
+      workers_.back().detach();  // the pool lives until process exit
     }
-    cv_.notify_all();
-    for (auto &t : workers_) t.join();
   }
+  ~Pool() = default;
   void work() {
     for (int i; (i = next_.fetch_add(1)) < n_;) (*fn_)(i);
   }

@@ -199,16 +199,18 @@ class Runner:
                 return self._dev[sl.offset:sl.offset + nb].view(_torch_dtype(np_dtype)).view(shape)
             s_lo, s_hi = plan.scratch
             sc = ctypes.c_void_p(base + s_lo) if s_hi > s_lo else None
-            _check(lib.jb_bind_workspace(sc, s_hi - s_lo, ctypes.c_void_p(stream.cuda_stream)))
+            cs = ctypes.c_void_p(stream.cuda_stream)
+            high, spills = ctypes.c_uint64(0), ctypes.c_uint64(0)
+            _check(lib.jb_bind_workspace(sc, s_hi - s_lo, cs))
             _ARENA.alloc = alloc
             try:
                 res = ENTRIES[entry].run(dcs, dev_args, **params) if params else ENTRIES[entry].run(dcs, dev_args)
+                _check(lib.jb_workspace_stats(cs, ctypes.byref(high), ctypes.byref(spills)))
             finally:
+                # never leave the arena bound: a later call on this stream
+                # could otherwise scribble on it after it is freed or regrown
                 _ARENA.alloc = None
-            high, spills = ctypes.c_uint64(0), ctypes.c_uint64(0)
-            _check(lib.jb_workspace_stats(ctypes.c_void_p(stream.cuda_stream), ctypes.byref(high),
-                                          ctypes.byref(spills)))
-            _check(lib.jb_bind_workspace(None, 0, ctypes.c_void_p(stream.cuda_stream)))
+                lib.jb_bind_workspace(None, 0, cs)
             key = (entry, tuple(dcs), tuple(_shape(a) for a in args if isinstance(a, np.ndarray)))
             if high.value > self._scratch.get(key, 0):
                 self._scratch[key] = int(high.value)  # the next call's plan reserves it

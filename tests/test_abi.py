@@ -70,3 +70,29 @@ def test_bits_expand_host(frames, frame_px, threads):
     buf = np.full(frames * frame_px + 1, np.float32(7.0))
     assert lib.jb_bits_expand_f32(words.ctypes.data, frames, frame_px, buf[1:].ctypes.data, threads) == 0
     assert np.array_equal(buf[1:].reshape(frames, frame_px), want)
+
+
+@pytest.mark.filterwarnings("ignore:This process:DeprecationWarning")
+def test_bits_expand_after_fork():
+    """The host thread pool is per process: a forked child (multiprocessing
+    'fork', torchrun helpers) gets its own workers instead of waiting on the
+    parent's, which do not exist in the child."""
+    import multiprocessing as mp
+    lib = _lib.load()
+    words = np.full((2, 64), 0xA5A5A5A5, np.uint32)
+    out = np.zeros((2, 2048), np.float32)
+    assert lib.jb_bits_expand_f32(words.ctypes.data, 2, 2048, out.ctypes.data, 0) == 0  # parent pool exists
+
+    def child(q):
+        o = np.zeros((2, 2048), np.float32)
+        rc = _lib.load().jb_bits_expand_f32(words.ctypes.data, 2, 2048, o.ctypes.data, 0)
+        q.put((rc, float(o.sum())))
+
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    p = ctx.Process(target=child, args=(q,))
+    p.start()
+    p.join(60)
+    assert not p.is_alive(), "the child's expansion hung"
+    rc, total = q.get(timeout=5)
+    assert rc == 0 and total == float(out.sum()) == 2 * 2048 / 2
