@@ -186,7 +186,7 @@ struct FusedArgs {
   int vec4;             // frame_px % 4 == 0 and out 16-byte aligned
   long long frame_px, slot_px;
   int lag;              // tiles of frame f + lag run the reject units of frame f
-  int opts;             // experiment bits (JB_EDGE_OPTS): 2 discard the ring lines after their unit
+  int opts;             // experiment bits (JB_EDGE_OPTS): 1 keep the ring lines (no discards)
   uint32_t *obits;      // bit-packed edge maps [frames][frame_words] (instead of out), or null
   long long frame_words;// ceil(frame_px / 32): bit b of word w is pixel 32w + b
 };
@@ -848,13 +848,11 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
   float *dst = a.obits ? nullptr : a.out + (size_t)f * a.frame_px + b0;
   // unit starts are multiples of 1024 pixels: whole words
   uint32_t *wdst = a.obits ? a.obits + (size_t)f * a.frame_words + (b0 >> 5) : nullptr;
-  // Ring lines are NOT discarded by default: the slot is rewritten in place a
-  // few frames later (its lines stay L2-resident, evict_last), and the
-  // discards plus the gpu-scope fence each discarding lane needs before the
-  // unit is counted cost more than they save (68.3 k vs 69.2 k frames/s,
-  // profiles/r02_kernel_experiments.txt).  Read once: the discards' memory
-  // clobbers would reload the flag from the parameter block every pass.
-  const bool disc = (a.opts & 2) != 0;
+  // Ring lines are discarded after their unit reads them, so the dead packed
+  // scratch is never written back to HBM (without the discards the launch
+  // moves 7.0 instead of 4.9 GB).  Read once: the discards' memory clobbers
+  // would reload the flag from the parameter block every pass.
+  const bool disc = !(a.opts & 1);
   // pass <=> A <= (int)p <= (int)0xff800000  <=>  p - Au < Ku (unsigned;
   // Ku = 0 when nothing can pass)
   const unsigned Au = (unsigned)A;
@@ -902,10 +900,6 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
         if (disc && i < n4 && (threadIdx.x & 7) == 0) discard_l2(s4 + i);
       }
     }
-    // the discards must be performed before the unit is counted: a discard
-    // still in flight when the slot's next frame is stored would drop the
-    // new lines
-    if (disc && (threadIdx.x & 7) == 0) fence_acq_rel();
   } else if (a.obits) {
     // one ballot per 32 consecutive pixels (cnt is uniform: every warp
     // runs every pass)
@@ -918,9 +912,17 @@ __device__ __noinline__ void reject_unit(const FusedArgs &a, int unit, int A) {
     for (long long i = threadIdx.x; i < cnt; i += THREADS) dst[i] = __ldcg(src + i) - Au < Ku ? 1.0f : 0.0f;
   }
   // every read of the unit's slot lines has returned (the values were
-  // stored): the count needs no fence
+  // stored).  The discards must be performed before the unit is counted (a
+  // discard still in flight when the slot's next frame is stored would drop
+  // the new lines): the CTA barrier orders every thread's discards before
+  // thread 0's gpu-scope fence, which is cumulative over them -- the pattern
+  // a grid barrier uses to publish a whole CTA's writes -- so one fence per
+  // unit suffices, not one per discarding lane
   __syncthreads();
-  if (threadIdx.x == 0) red_add(a.rdone + f, 1u);
+  if (threadIdx.x == 0) {
+    if (disc && a.vec4) fence_acq_rel();
+    red_add(a.rdone + f, 1u);
+  }
 }
 
 // thread 0's in-flight load results: registers, so that nothing waits for
