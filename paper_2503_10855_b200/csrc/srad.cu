@@ -318,7 +318,10 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
 // Arithmetic per pixel is the oracle's, op for op; the few fused forms
 // (0.25 L folded into the numerator/denominator) are exact rewrites that
 // only apply scalings by powers of two to normal values.
-constexpr int SW = 124, SH = 32, SWARPS = 8;
+#ifndef SRAD_SWARPS
+#define SRAD_SWARPS 8
+#endif
+constexpr int SW = 124, SH = 32, SWARPS = SRAD_SWARPS;
 #ifndef SRAD_MINB
 #define SRAD_MINB 2
 #endif
