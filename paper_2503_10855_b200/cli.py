@@ -122,6 +122,7 @@ def cmd_run(args) -> int:
         return 2
     launches0 = _lib.launch_count()
     t0 = time.perf_counter()
+    extra = {}
     try:
         if args.oracle:
             result, kernel = _reference_oracle(module, args.entry, dcs, inputs), "skiff.oracle_execute"
@@ -129,6 +130,9 @@ def cmd_run(args) -> int:
             from .planner import execute_module
             result, choice = execute_module(module, args.entry, dcs, inputs)
             kernel = choice.entry
+            # the C entry and the launch parameters the schedule implied
+            extra = {"c_symbol": choice.c_symbol,
+                     "params": {k: list(v) if isinstance(v, tuple) else v for k, v in choice.params.items()}}
         else:
             result = api.execute(args.entry, dcs, inputs)
             kernel = args.entry
@@ -142,7 +146,7 @@ def cmd_run(args) -> int:
     d2h = sum(int(np.asarray(x).nbytes) for x in outs)
     print(json.dumps({"entry": args.entry, "kernel": kernel, "dyn_consts": dcs, "wall_ms": round(wall, 3),
                       "gpu_launches": _lib.launch_count() - launches0, "h2d_bytes": h2d, "d2h_bytes": d2h,
-                      "outputs": paths}))
+                      "outputs": paths, **extra}))
     return 0
 
 

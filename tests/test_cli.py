@@ -209,3 +209,42 @@ def test_oracle_ab_matches_gpu_arm(tmp_path, capsys):
     u, m = 2.0 ** -24, 48
     gam = m * u / (1 - m * u)
     assert np.all(np.abs(gpu - ref) <= (2 * gam + 8 * u) * (np.abs(a) @ np.abs(b)))
+
+
+_ACC_JN = """
+#[entry]
+fn matmul<n, m, l: usize>(a: f32[n, m], b: f32[m, l]) -> f32[n, l] {
+  let res : f32[n, l];
+  @outer for i in 0..n {
+    @middle for j in 0..l {
+      let s : f32 = 0.0;
+      @inner for k in 0..m {
+        s += a[i, k] * b[k, j];
+      }
+      res[i, j] = s;
+    }
+  }
+  return res;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_cli_reduction_tree_schedule_reports_its_launch(tmp_path, capsys):
+    """A reduction_tree! schedule through the CLI: the metrics line names the
+    schedule-parametrised C entry and its K partials, and the result stays
+    within the fp32 bound of the exact product."""
+    _ref_values()
+    sch = ("forkify(*); forkify(*); forkify(*); infer-attributes(*); macro reduction_tree![N](F) { "
+           "fork-chunk![N](F); let (outer, inner) = fork-reshape[[0], [1]](F); monoid-reassociate(inner); "
+           "let (top, bottom) = fork-fission(outer); } reduction_tree![4](matmul@inner);")
+    argv = _ab_files(tmp_path, 64, 128, 96, sch)
+    (tmp_path / "matmul.jn").write_text(_ACC_JN)
+    assert cli.main(argv + ["-o", str(tmp_path / "gpu.json")]) == 0
+    metrics = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert metrics["c_symbol"] == "jb_matmul_sched_f32" and metrics["params"]["tree"] == [4, 1]
+    gpu = tensor_io.load_tensor(str(tmp_path / "gpu.json")).astype(np.float64)
+    a, b = (tensor_io.load_tensor(str(tmp_path / f"{x}.json")).astype(np.float64) for x in "ab")
+    u, m = 2.0 ** -24, 128
+    gam = m * u / (1 - m * u)
+    assert np.all(np.abs(gpu - a @ b) <= (2 * gam + 8 * u) * (np.abs(a) @ np.abs(b)))
