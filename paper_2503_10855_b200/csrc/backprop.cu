@@ -18,7 +18,10 @@
 // The layer sums are the associative reduction the paper's schedule
 // parallelises; both sides accumulate them in f64, the rest is
 // op-for-op the oracle's single-rounding f32 arithmetic.
+#include <stdlib.h>
+
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace jb {
 namespace bp {
@@ -77,6 +80,111 @@ __global__ void __launch_bounds__(THREADS) bp_forward_kernel(FwdArgs a) {
     a.sums[1 + threadIdx.x] = v;
   }
   if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+// The same layer sum with the weight rows streamed into shared memory by
+// 1-D bulk copies (TMA), two chunks of THREADS rows in flight per CTA: HBM
+// sees whole 16-byte-aligned chunks instead of every thread's 68-byte rows
+// through scalar loads.  Thread t takes row t of a chunk (odd row pitch NH+1
+// words: conflict-free LDS).  Rows after the last whole chunk take the
+// direct loads.  Same per-thread f64 accumulation and reduction order per
+// thread as bp_forward_kernel, so the f64 sums round to the same f32 values.
+template <int NH>
+__global__ void __launch_bounds__(THREADS) bp_forward_tma_kernel(FwdArgs a) {
+  constexpr int RW = NH + 1;                        // row pitch (words)
+  constexpr uint32_t CB = THREADS * RW * 4;         // chunk bytes (a multiple of 16)
+  extern __shared__ __align__(128) float fbuf[];    // [2][THREADS * RW]
+  __shared__ __align__(8) uint64_t bar[2];
+  double acc[NH];
+#pragma unroll
+  for (int j = 0; j < NH; j++) acc[j] = 0.0;
+  const long long chunks = a.rows / THREADS;
+  const long long mine = chunks > blockIdx.x ? (chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint64_t pol = tc::policy_evict_first();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+    for (int b = 0; b < 2 && b < mine; b++) {
+      const long long c = blockIdx.x + (long long)b * gridDim.x;
+      tc::mbar_arrive_expect_tx(&bar[b], CB);
+      tc::bulk_load_1d(fbuf + b * THREADS * RW, a.w + c * THREADS * RW, CB, &bar[b], pol);
+    }
+  }
+  __syncthreads();
+  for (long long i = 0; i < mine; i++) {
+    const int b = (int)(i & 1);
+    const long long c = blockIdx.x + i * gridDim.x;
+    const long long k = c * THREADS + threadIdx.x;
+    const float xk = k == 0 ? 1.0f : __ldg(a.x + k);
+    tc::mbar_wait(&bar[b], (uint32_t)((i >> 1) & 1));
+    const float *row = fbuf + b * THREADS * RW + threadIdx.x * RW;
+#pragma unroll
+    for (int j = 0; j < NH; j++) acc[j] += (double)mul_rn(row[1 + j], xk);
+    __syncthreads();  // every thread is done with buffer b
+    if (threadIdx.x == 0 && i + 2 < mine) {
+      const long long c2 = c + 2 * (long long)gridDim.x;
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive_expect_tx(&bar[b], CB);
+      tc::bulk_load_1d(fbuf + b * THREADS * RW, a.w + c2 * THREADS * RW, CB, &bar[b], pol);
+    }
+  }
+  // the rows after the last whole chunk: the CTA and thread the direct
+  // kernel's grid-stride gives them, so every thread folds the same rows in
+  // the same order as bp_forward_kernel
+  if (blockIdx.x == (unsigned)(chunks % gridDim.x)) {
+    const long long k = chunks * THREADS + threadIdx.x;
+    if (k < a.rows) {
+      const float xk = k == 0 ? 1.0f : __ldg(a.x + k);
+      const float *row = a.w + k * RW;
+#pragma unroll
+      for (int j = 0; j < NH; j++) acc[j] += (double)mul_rn(__ldg(row + 1 + j), xk);
+    }
+  }
+  __shared__ double sh[THREADS / 32][NH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NH; j++) {
+    const double v = warp_sum(acc[j]);
+    if (lane == 0) sh[warp][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NH) {
+    double v = 0.0;
+    for (int w = 0; w < THREADS / 32; w++) v += sh[w][threadIdx.x];
+    a.partials[(size_t)blockIdx.x * MAXH + threadIdx.x] = v;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < NH) {
+    double v = 0.0;
+    for (unsigned b = 0; b < gridDim.x; b++) v += ((volatile double *)a.partials)[(size_t)b * MAXH + threadIdx.x];
+    a.sums[1 + threadIdx.x] = v;
+  }
+  if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+template <int NH>
+static jb_status launch_forward(const FwdArgs &fa, int grid, cudaStream_t s, bool tma) {
+  if (!tma) {
+    bp_forward_kernel<NH><<<grid, THREADS, 0, s>>>(fa);
+    return JB_OK;
+  }
+  const int smem = 2 * THREADS * (NH + 1) * 4;
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr[dev]) {
+    JB_CHECK_CUDA(cudaFuncSetAttribute(bp_forward_tma_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr[dev] = true;
+  }
+  bp_forward_tma_kernel<NH><<<grid, THREADS, smem, s>>>(fa);
+  return JB_OK;
 }
 
 // hidden side of the step, one CTA (n_hid, n_out <= MAXH)
@@ -202,12 +310,21 @@ extern "C" jb_status jb_bp_train_f32(uint64_t n_in, uint64_t n_hid, uint64_t n_o
   JB_CHECK_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   FwdArgs fa{input, in_w, partials, ticket, sums, (long long)n_in + 1, (int)n_hid + 1};
   void *tok = prof_begin("bp_forward", s);
+  // the weight rows stream through shared memory by bulk copy when the
+  // matrix is 16-byte aligned (JB_BP_DIRECT=1: the direct-load kernel)
+  static const bool direct = [] {
+    const char *e = getenv("JB_BP_DIRECT");
+    return e && atoi(e) == 1;
+  }();
+  const bool tma = !direct && ((uintptr_t)in_w % 16) == 0;
+  jb_status fs;
   switch (n_hid) {
-    case 4: bp_forward_kernel<4><<<grid, THREADS, 0, s>>>(fa); break;
-    case 8: bp_forward_kernel<8><<<grid, THREADS, 0, s>>>(fa); break;
-    case 16: bp_forward_kernel<16><<<grid, THREADS, 0, s>>>(fa); break;
-    default: bp_forward_kernel<32><<<grid, THREADS, 0, s>>>(fa); break;
+    case 4: fs = launch_forward<4>(fa, grid, s, tma); break;
+    case 8: fs = launch_forward<8>(fa, grid, s, tma); break;
+    case 16: fs = launch_forward<16>(fa, grid, s, tma); break;
+    default: fs = launch_forward<32>(fa, grid, s, tma); break;
   }
+  if (fs != JB_OK) return fs;
   prof_end(tok, s);
   JB_LAUNCHED("bp_forward");
   bp_small_kernel<<<1, 64, 0, s>>>(sums, input, hid_w, hid_prev_w, target, hidden, output, delta_h, errs,
