@@ -1349,8 +1349,17 @@ static jb_status run_fused(uint64_t batch, uint64_t n, uint64_t m, const float *
   size_t ring = ((size_t)EDGE_RING_MB << 20) / (slot_px * 4);
   if (ring < 2) ring = 2;
   if (ring > batch) ring = batch;
-  // reject units: one per ~two compute tiles, whole 4 KB blocks of lines
-  const size_t unit_px = ((2 * frame_px + tpf - 1) / tpf + 1023) / 1024 * 1024;
+  // reject units: about seven compute tiles' pixels each (one unit per ~7
+  // tiles), whole 4 KB blocks of lines.  A unit's fixed cost (its CTA
+  // barrier, the discard fence, the count) favours large units, load
+  // balance small ones: JB_EDGE_UNIT_PX A/B at 1080p (frames/s): 8192 69.7 k,
+  // 16384 72.3 k, 24576-28672 73.1 k, 32768 73.0 k, 65536 67.2 k.
+  size_t unit_px = ((7 * frame_px + tpf - 1) / tpf + 1023) / 1024 * 1024;
+  if (const char *e = getenv("JB_EDGE_UNIT_PX")) {  // experiments: a multiple of 1024
+    const long long u = atoll(e);
+    if (u >= 1024 && u % 1024 == 0) unit_px = (size_t)u;
+  }
+  if (unit_px > ((frame_px + 1023) / 1024) * 1024) unit_px = ((frame_px + 1023) / 1024) * 1024;
   const size_t units = (frame_px + unit_px - 1) / unit_px;
   const size_t ring_bytes = ring * slot_px * 4;
   const size_t pf = ((batch * 8 + 255) / 256) * 256;  // one per-frame array (<= 8 B/frame)
