@@ -577,6 +577,11 @@ __device__ __forceinline__ unsigned edge_tile(Smem &S, const FusedArgs &a, int f
       }
     }
   }
+  // the previous tile's packed tile has left S.P before the sobel stage
+  // refills it (the barrier below orders this for every warp); waited for as
+  // late as possible, so the bulk store's smem reads overlap the gaussian
+  // and the laplacian instead of thread 0's tile top
+  if (tid == 0) tc::bulk_wait_read<0>();
   __syncthreads();
   EDGE_T(2);
 
@@ -1016,7 +1021,6 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     // ---- the ring slot of frame f must be rejected; probe this tile's
     // reject frame (consumed at the tile's end)
     if (tid == 0) {
-      tc::bulk_wait_read<0>();  // the last packed tile has left S.P (the stage-0 barrier orders this before the sobel stage refills it)
       if (!slot_free(a, q, rf_, f)) {
         flush_done(a, q, pd_max, false);  // someone may be waiting on it
         while (ld_relaxed(a.rdone + f - a.ring) < (unsigned)a.units) __nanosleep(128);
@@ -1132,12 +1136,16 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
     __syncthreads();
     EDGE_T(4);
     if (tid == 0) {
-      const unsigned am = tile_store(S, a, f, y0, x0);
       if (a.use_tma) {
-        flush_done(a, q, pd_max, true);
+        // count the previous tile first (its bulk store completed long ago:
+        // wait_group 0 before this tile's store is committed), so its fences
+        // do not also wait for this tile's fresh atomicMax; then issue this
+        // tile's bulk store and max
+        flush_done(a, q, pd_max, false);
+        pd_max = tile_store(S, a, f, y0, x0);  // a register: consumed (waited for) one tile later
         q.pd = f;
-        pd_max = am;  // a register: consumed (waited for) one tile later
       } else {
+        (void)tile_store(S, a, f, y0, x0);
         fence_acq_rel();  // orders the CTA's stores (barrier) and the atom before the count
         red_add(a.done + f, 1u);
       }
