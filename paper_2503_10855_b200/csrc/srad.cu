@@ -321,7 +321,10 @@ __global__ void __launch_bounds__(THREADS) srad_iter_kernel(Args a) {
 #ifndef SRAD_SWARPS
 #define SRAD_SWARPS 8
 #endif
-constexpr int SW = 124, SH = 32, SWARPS = SRAD_SWARPS;
+#ifndef SRAD_SH
+#define SRAD_SH 32
+#endif
+constexpr int SW = 124, SH = SRAD_SH, SWARPS = SRAD_SWARPS;
 #ifndef SRAD_MINB
 #define SRAD_MINB 2
 #endif
