@@ -73,6 +73,12 @@ struct Args {
 #define CSR_LD(p) __ldcs(p)
 #endif
 
+// bit i set where byte i of x is not kUnseen (0xFF)
+__device__ __forceinline__ uint32_t seen4(uint32_t x) {
+  const uint32_t r = __vcmpne4(x, 0xFFFFFFFFu) & 0x80808080u;
+  return (r * 0x00204081u) >> 28;
+}
+
 __device__ __forceinline__ void red_or(uint32_t *p, uint32_t v) {
   asm volatile("red.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -138,6 +144,21 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
     // node records and edge lists stream nearly sequentially)
     bool scan = scan_in || (level < kDeep && fsize > (a.n >> 2));
     uint32_t work = scan ? a.n : fsize;
+    if (scan_in) {
+      // the previous level claimed through level bytes only (no atomics):
+      // rebuild the visited bitmap from them, 32 vertices per word.  A queue
+      // level (after the compaction below) claims by atomicOr on the bitmap
+      // and needs it exact: the compaction's grid barrier orders the
+      // rebuild first.  A scan level only filters with it (the level byte
+      // decides), so words it reads half-rebuilt are harmless.
+      const uint32_t nw = (a.n + 31) >> 5;
+      for (uint32_t w = gtid; w < nw; w += gsize) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(a.level) + 2 * w;
+        const uint4 b0 = __ldcg(p), b1 = __ldcg(p + 1);
+        a.visited[w] = seen4(b0.x) | seen4(b0.y) << 4 | seen4(b0.z) << 8 | seen4(b0.w) << 12 |
+                       seen4(b1.x) << 16 | seen4(b1.y) << 20 | seen4(b1.z) << 24 | seen4(b1.w) << 28;
+      }
+    }
     if (scan_in && fsize <= (a.n >> 2)) {
       // a small frontier after a queue-less level: compact its level bytes
       // into the queue first (16 bytes per lane per load), then run it as a
@@ -244,8 +265,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
 #pragma unroll
               for (int j = 0; j < EB; j++) {
                 if (lv[j] != kUnseen) continue;
-                a.level[v[j]] = nb;
-                red_or(a.visited + (v[j] >> 5), 1u << (v[j] & 31));
+                a.level[v[j]] = nb;  // the bitmap is rebuilt from the level bytes next level
                 claimed++;
               }
             }
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
 
 __global__ void bfs_init_kernel(uint8_t *level, uint32_t *visited, uint32_t n, uint32_t words, uint32_t source,
                                 uint32_t *q0, uint32_t *qsize) {
-  const uint32_t n4 = (n + 3) / 4;  // the level array is padded to whole words
+  const uint32_t n4 = 8 * ((n + 31) / 32);  // padded to whole 32-vertex groups (the bitmap rebuild reads them)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
     reinterpret_cast<uint32_t *>(level)[i] = 0xFFFFFFFFu;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gridDim.x * blockDim.x) visited[i] = 0;
