@@ -47,8 +47,11 @@ constexpr int LQ = 4096;  // block-local queue capacity
 #ifndef BFS_VPT
 #define BFS_VPT 2
 #endif
+#ifndef BFS_SCAN_SHIFT
+#define BFS_SCAN_SHIFT 1  // frontiers > n / 2^shift are read by scanning the level bytes, smaller ones compacted into a queue (A/B: 0 83.7, 1 83.4, 2 80.8, 3 80.6 GTEPS)
+#endif
 #ifndef BFS_DENSE_SHIFT
-#define BFS_DENSE_SHIFT 3  // queue-less output for frontiers >= n / 2^shift
+#define BFS_DENSE_SHIFT 4  // queue-less output for frontiers >= n / 2^shift (A/B: 3 79.1, 4 80.5, 5 80.0 GTEPS)
 #endif
 constexpr int EB = BFS_EB;       // edges per lane per batch
 constexpr int CAP = 32 * EB;     // per-warp edge-id buffer (one batch)
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
     const uint8_t lb = (uint8_t)level;
     // scan-in: the frontier is "level byte == level" (read in vertex order:
     // node records and edge lists stream nearly sequentially)
-    bool scan = scan_in || (level < kDeep && fsize > (a.n >> 2));
+    bool scan = scan_in || (level < kDeep && fsize > (a.n >> BFS_SCAN_SHIFT));
     uint32_t work = scan ? a.n : fsize;
     if (scan_in) {
       // the previous level claimed through level bytes only (no atomics):
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
                        seen4(b1.x) << 16 | seen4(b1.y) << 20 | seen4(b1.z) << 24 | seen4(b1.w) << 28;
       }
     }
-    if (scan_in && fsize <= (a.n >> 2)) {
+    if (scan_in && fsize <= (a.n >> BFS_SCAN_SHIFT)) {
       // a small frontier after a queue-less level: compact its level bytes
       // into the queue first (16 bytes per lane per load), then run it as a
       // queue -- walking all n vertices would pay one dependent chain of
