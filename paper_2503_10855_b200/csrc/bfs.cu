@@ -23,10 +23,11 @@
 //    space in the next frontier (block-aggregated atomics);
 //  * large levels skip the queue altogether ("dense output"): a claim is a
 //    level-byte check in L2 + a plain byte store (every writer of a vertex
-//    in one level writes the same level, so the race is benign) + a
-//    fire-and-forget red.or on the bitmap filter, no claiming atomics, no
-//    block barriers; the next level finds its frontier by scanning the
-//    level bytes (16 MiB, L2-resident), warps work independently;
+//    in one level writes the same level, so the race is benign), no
+//    claiming atomics, no bitmap update, no block barriers; the next level
+//    rebuilds the bitmap from the level bytes (32 vertices per word) and
+//    finds its frontier in them: by scanning all n level bytes when it is
+//    large, else by compacting them into a queue first;
 //  * one grid-wide barrier (cooperative groups) per level: the frontier
 //    sizes rotate through three counters, so the one two levels ahead is
 //    cleared while the current one is read.
@@ -116,7 +117,10 @@ __device__ unsigned long long g_bfs_trace[64];
 #define BFS_T(level) do {} while (0)
 #endif
 
-__global__ void __launch_bounds__(THREADS) bfs_kernel(Args a) {
+#ifndef BFS_MINB
+#define BFS_MINB 1  // A/B: 3 CTAs/SM (40 registers) 75.5 vs 82.5 GTEPS
+#endif
+__global__ void __launch_bounds__(THREADS, BFS_MINB) bfs_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t lq[LQ];
   __shared__ uint32_t lcount, lbase;
