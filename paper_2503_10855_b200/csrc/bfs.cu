@@ -118,7 +118,7 @@ __device__ unsigned long long g_bfs_trace[64];
 #endif
 
 #ifndef BFS_MINB
-#define BFS_MINB 1  // A/B: 3 CTAs/SM (40 registers) 75.5 vs 82.5 GTEPS
+#define BFS_MINB 2  // 2 CTAs/SM at <= 64 registers; A/B: 1 CTA/SM (80 registers) 72.5, 2 82.5, 3 (40 registers) 75.5 GTEPS
 #endif
 __global__ void __launch_bounds__(THREADS, BFS_MINB) bfs_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
@@ -459,8 +459,22 @@ extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, co
   JB_LAUNCHED("bfs_init");
   bfs_seed_kernel<<<1, 1, 0, s>>>(a.level, a.visited, source);
   JB_LAUNCHED("bfs_seed");
+  static int carve = [] {
+    // experiments: the shared-memory carveout (percent); the rest of the
+    // 256 KB is L1, which caches the visited-bitmap probes
+    const char *e = getenv("JB_BFS_CARVE");
+    const int c = e ? atoi(e) : -1;
+    if (c >= 0) cudaFuncSetAttribute(bfs_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    return c;
+  }();
+  (void)carve;
   int per_sm = 0;
   JB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, THREADS, 0));
+  if (const char *e = getenv("JB_BFS_CTAS")) {  // experiments: fewer CTAs per SM than fit
+    const int k = atoi(e);
+    if (k >= 1 && k < per_sm) per_sm = k;
+  }
+  if (getenv("JB_BFS_VERBOSE")) fprintf(stderr, "bfs: %d CTAs/SM of %d threads\n", per_sm, THREADS);
   if (per_sm < 1) per_sm = 1;
   const int grid = sm_count() * per_sm;
   void *args[] = {&a};

@@ -20,6 +20,8 @@ lib.jb_bfs_trace(ctypes.c_void_p(buf.ctypes.data))
 t = buf.astype(np.int64)
 nz = np.nonzero(t)[0]
 last = nz.max()
+sizes = np.bincount(cost.cpu().numpy()[cost.cpu().numpy() >= 0])
 for i in range(last):
-    print(f"level {i:2d}: {(t[i + 1] - t[i]) / 1e3:8.2f} us")
+    f = sizes[i] if i < len(sizes) else 0
+    print(f"level {i:2d}: {(t[i + 1] - t[i]) / 1e3:8.2f} us  frontier {f:9d}")
 print(f"total to last level start: {(t[last] - t[0]) / 1e3:.1f} us")
