@@ -57,7 +57,7 @@
 
 // -DEDGE_STAGE_CLOCKS: per-stage SM-cycle accounting (tools/edge_stage_clocks.py)
 #ifdef EDGE_STAGE_CLOCKS
-__device__ unsigned long long g_edge_clk[8];
+__device__ unsigned long long g_edge_clk[16];
 __shared__ long long s_edge_clk;
 #define EDGE_T(i)                                                            \
   do {                                                                       \
@@ -1026,6 +1026,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         while (ld_relaxed(a.rdone + f - a.ring) < (unsigned)a.units) __nanosleep(128);
         q.free_upto = f;
       }
+      EDGE_T(8);
       slot_probe(a, q, rf_, f);
       const int j = tile - f * tpf;
       q.ru = -1;
@@ -1142,6 +1143,7 @@ edge_fused_kernel(const __grid_constant__ FusedArgs a) {
         // do not also wait for this tile's fresh atomicMax; then issue this
         // tile's bulk store and max
         flush_done(a, q, pd_max, false);
+        EDGE_T(9);
         pd_max = tile_store(S, a, f, y0, x0);  // a register: consumed (waited for) one tile later
         q.pd = f;
       } else {
@@ -1505,7 +1507,7 @@ extern "C" jb_status jb_edge_bits_f32(uint64_t batch, uint64_t n, uint64_t m, ui
 
 #ifdef EDGE_STAGE_CLOCKS
 extern "C" JB_API void jb_edge_stage_clocks(unsigned long long *out) {
-  cudaMemcpyFromSymbol(out, g_edge_clk, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out, g_edge_clk, sizeof(unsigned long long) * 16);
 }
 #endif
 
