@@ -23,11 +23,12 @@ def test_cava_matches_oracle(jb, oracle, shape, P):
     assert bad == 0, f"{bad}/{got.size} u8 values differ (max |d| {np.abs(got.astype(int) - ref).max()})"
 
 
-@pytest.mark.parametrize("P", [255, 256, 257, 1024, 4096])
+@pytest.mark.parametrize("P", [63, 64, 255, 256, 257, 1024, 4096])
 def test_cava_many_control_points(jb, oracle, P):
     """Control-point counts either side of the shared-memory table limit
     (PMAX_SMEM = 256 in cava.cu; larger tables stream from global memory)
-    up to the compute variant's thousands of points."""
+    up to the compute variant's thousands of points, and either side of the
+    switch to the fma(d, w, +0) weight products (CAVA_FMA0_MIN_P = 64)."""
     raw = W.cava_raw(2, 40, 72, seed=P)
     params = W.cava_params(P=P, seed=P)
     got = jb.cava(raw, *params)
