@@ -970,7 +970,7 @@ __device__ __forceinline__ void slot_probe(const FusedArgs &a, Sched &q, Infligh
 }
 
 #ifndef EDGE_MINB
-#define EDGE_MINB 3  // CTAs per SM (80 registers); A/B: 2 CTAs/SM (128 registers) 61.6k vs 73.1k frames/s
+#define EDGE_MINB 3  // CTAs per SM (80 registers); A/B: 2 CTAs/SM (128 registers) 61.6k, 4 (64 registers, spills) 67.8k vs 73.1k frames/s
 #endif
 __global__ void __launch_bounds__(THREADS, EDGE_MINB)
 edge_fused_kernel(const __grid_constant__ FusedArgs a) {
