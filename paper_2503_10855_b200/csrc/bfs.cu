@@ -60,8 +60,13 @@ constexpr int CAP = 32 * EB;     // per-warp edge-id buffer (one batch)
 constexpr int VPT = BFS_VPT;  // frontier vertices per thread per round
 constexpr uint8_t kUnseen = 0xFF, kDeep = 0xFE;  // level byte codes
 
+#ifndef BFS_PACK
+#define BFS_PACK 0  // 1: (starting, no_of_edges) packed into one 8-byte record per vertex by a prologue
+#endif
+
 struct Args {
   const uint32_t *starting, *nedges, *edges;
+  const uint2 *rec;   // BFS_PACK: [n] (starting, no_of_edges)
   int32_t *cost;
   uint8_t *level;     // [n] level byte (kUnseen / level / kDeep: see cost[])
   uint32_t *visited;  // bitmap
@@ -228,8 +233,14 @@ __global__ void __launch_bounds__(THREADS, BFS_MINB) bfs_kernel(Args a) {
             if (scan) live = __ldcg(a.level + i) == lb;
             else u = __ldcg(fq + i);
             if (live) {
+#if BFS_PACK
+              const uint2 r = __ldcg(a.rec + u);
+              e0[k] = r.x;
+              ne[k] = r.y;
+#else
               e0[k] = CSR_LD(a.starting + u);
               ne[k] = CSR_LD(a.nedges + u);
+#endif
             }
           }
         }
@@ -302,8 +313,14 @@ __global__ void __launch_bounds__(THREADS, BFS_MINB) bfs_kernel(Args a) {
             if (scan) live = __ldcg(a.level + i) == lb;
             else u = __ldcg(fq + i);
             if (live) {
+#if BFS_PACK
+              const uint2 r = __ldcg(a.rec + u);
+              e0[k] = r.x;
+              ne[k] = r.y;
+#else
               e0[k] = CSR_LD(a.starting + u);
               ne[k] = CSR_LD(a.nedges + u);
+#endif
             }
           }
         }
@@ -433,6 +450,14 @@ extern "C" JB_API void jb_bfs_trace(unsigned long long *out) {
 }
 #endif
 
+#if BFS_PACK
+__global__ void bfs_pack_kernel(const uint32_t *__restrict__ starting, const uint32_t *__restrict__ nedges,
+                                uint2 *__restrict__ rec, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    rec[i] = make_uint2(__ldcs(starting + i), __ldcs(nedges + i));
+}
+#endif
+
 extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, const uint32_t *nedges,
                             const uint32_t *edges, uint32_t source, int32_t *cost, void *stream) {
   JB_REQUIRE(n < (1ull << 32) - 64 && m < (1ull << 32), "bfs: graph too large for u32 indices");
@@ -444,7 +469,8 @@ extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, co
   const size_t qbytes = ((n * 4 + 255) / 256) * 256;
   const size_t vbytes = ((words * 4 + 255) / 256) * 256;
   const size_t lbytes = ((n + 255) / 256) * 256;
-  char *ws = (char *)workspace(2 * qbytes + vbytes + lbytes + 256, s);
+  const size_t rbytes = BFS_PACK ? ((n * 8 + 255) / 256) * 256 : 0;
+  char *ws = (char *)workspace(2 * qbytes + vbytes + lbytes + 256 + rbytes, s);
   if (!ws) return JB_ECUDA;
   Args a;
   a.starting = starting; a.nedges = nedges; a.edges = edges; a.cost = cost;
@@ -454,6 +480,11 @@ extern "C" jb_status jb_bfs(uint64_t n, uint64_t m, const uint32_t *starting, co
   a.level = (uint8_t *)(ws + 2 * qbytes + vbytes);
   a.qsize = (uint32_t *)(ws + 2 * qbytes + vbytes + lbytes);
   a.n = (uint32_t)n;
+  a.rec = (const uint2 *)(ws + 2 * qbytes + vbytes + lbytes + 256);
+#if BFS_PACK
+  bfs_pack_kernel<<<sm_count() * 8, 256, 0, s>>>(starting, nedges, (uint2 *)a.rec, (uint32_t)n);
+  JB_LAUNCHED("bfs_pack");
+#endif
   bfs_init_kernel<<<sm_count() * 4, 256, 0, s>>>(a.level, a.visited, (uint32_t)n, words, source, a.q[0], a.qsize);
   JB_LAUNCHED("bfs_init");
   bfs_seed_kernel<<<1, 1, 0, s>>>(a.level, a.visited, source);
